@@ -854,3 +854,57 @@ def level_sets(lev):
         blocks += list(b)
         ptr[l + 1] = ptr[l] + len(b)
     return ptr, np.array(blocks, dtype=np.int32)
+
+
+def a_pattern(net, part):
+    """Topological CSR pattern of A = ∂[r; h]/∂[u; x] (R19): an r row of bus i
+    depends on the variables of i and its neighbours, an h row of line ℓ on
+    the variables of its two end buses."""
+    adj = bus_adjacency(net)
+    zv, zth = z_index(part)
+    rows = []
+    for (i, t) in part["r_rows"]:
+        cols = set()
+        for j in adj[i] | {i}:
+            cols.add(int(zv[j]))
+            if zth[j] >= 0:
+                cols.add(int(zth[j]))
+        rows.append(sorted(cols))
+    for (l, e) in part["h_rows"]:
+        cols = set()
+        for j in (int(net["line_from"][l]), int(net["line_to"][l])):
+            cols.add(int(zv[j]))
+            if zth[j] >= 0:
+                cols.add(int(zth[j]))
+        rows.append(sorted(cols))
+    ptr = np.zeros(len(rows) + 1, dtype=np.int32)
+    for k, r in enumerate(rows):
+        ptr[k + 1] = ptr[k] + len(r)
+    return ptr, np.array([c for r in rows for c in r], dtype=np.int32)
+
+
+def filled_csr(F):
+    """CSR (ptr, idx) of a boolean filled pattern."""
+    ptr = np.zeros(F.shape[0] + 1, dtype=np.int32)
+    idx = []
+    for r in range(F.shape[0]):
+        c = np.nonzero(F[r])[0]
+        idx.append(c)
+        ptr[r + 1] = ptr[r] + len(c)
+    return ptr, np.concatenate(idx).astype(np.int32) if idx else np.zeros(0, np.int32)
+
+
+def reduce_columns(K, Gx, Gu, cols):
+    """O7' for selected unit directions (sampled full-size parity): the three
+    steps of PAPER.md L1203–1222 with R11 for V = I[:, cols], using a sparse
+    LU (SuperLU) of G_x as the solve primitive."""
+    n_u = Gu.shape[1]
+    V = np.zeros((n_u, len(cols)))
+    V[cols, np.arange(len(cols))] = 1.0
+    lu = spla.splu(sp.csc_matrix(Gx))
+    Gu = sp.csr_matrix(Gu)
+    Z = -lu.solve(np.asarray((Gu @ V)))
+    H = sp.csr_matrix(K) @ np.vstack([V, Z])
+    Hu, Hx = H[:n_u], H[n_u:]
+    Psi = lu.solve(np.asarray(Hx), trans="T")
+    return Hu - Gu.T @ Psi

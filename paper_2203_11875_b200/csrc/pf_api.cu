@@ -1,0 +1,271 @@
+// pf_api.cu — the C-ABI of include/pf.h: handle lifetime, host→device upload
+// of the plan, capacity/state checks, and stream-ordered kernel launches.
+#include "../../include/pf.h"
+#include "pf_launch.h"
+#include "pf_plan.h"
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace pf;
+
+struct pf_net {
+  Plan P;
+  DevNet dn{};
+  Work w{};
+  int device = 0;
+  int C = 8;
+  int max_batch = 0, max_scen = 0;
+  int lu_scen = 0;  // scenarios factorized by the last pf_jacobian (0 = none)
+  std::vector<void*> allocs;
+  std::string err;
+  long long launches = 0;
+};
+
+static std::string g_build_err;
+
+namespace {
+
+template <class T>
+bool up(pf_net* h, const std::vector<T>& v, const T** out) {
+  void* p = nullptr;
+  size_t bytes = std::max<size_t>(1, v.size()) * sizeof(T);
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return false;
+  h->allocs.push_back(p);
+  if (!v.empty() && cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess) return false;
+  *out = static_cast<const T*>(p);
+  return true;
+}
+
+template <class T>
+bool alloc(pf_net* h, size_t count, T** out) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(T)) != cudaSuccess) return false;
+  h->allocs.push_back(p);
+  *out = static_cast<T*>(p);
+  return true;
+}
+
+pf_status cuda_check(pf_net* h, const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    h->err = std::string(where) + ": " + cudaGetErrorString(e);
+    return PF_ERR_CUDA;
+  }
+  return PF_OK;
+}
+
+bool set_device(pf_net* h) {
+  if (h->device < 0) { h->err = "host-only handle (device < 0): no compute"; return false; }
+  return cudaSetDevice(h->device) == cudaSuccess;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pf_build_error(void) { return g_build_err.c_str(); }
+
+pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t* line_from,
+                           const int32_t* line_to, const double* Y_ff, const double* Y_ft,
+                           const double* Y_tf, const double* Y_tt, const double* Y_sh,
+                           const int32_t* gen_bus, int32_t ref_bus, const double* p_d,
+                           const double* q_d, const double* F_max, const double* c_quad,
+                           const double* c_lin, int32_t max_batch, int32_t max_scen,
+                           int32_t device, pf_net** out) {
+  g_build_err.clear();
+  if (!out || !line_from || !line_to || !Y_ff || !Y_ft || !Y_tf || !Y_tt || !Y_sh || !gen_bus || !p_d ||
+      !q_d || !F_max || !c_quad || !c_lin) {
+    g_build_err = "null argument";
+    return PF_ERR_ARG;
+  }
+  *out = nullptr;
+  if (max_batch < 1 || max_scen < 1) { g_build_err = "max_batch and max_scen must be >= 1"; return PF_ERR_ARG; }
+  pf_net* h = new pf_net();
+  bool topo = false;
+  std::string e = build_plan(n_b, n_l, n_g, line_from, line_to, gen_bus, ref_bus, F_max, h->P, &topo);
+  if (!e.empty()) {
+    g_build_err = e;
+    delete h;
+    return topo ? PF_ERR_TOPOLOGY : PF_ERR_ARG;
+  }
+  h->device = device;
+  const Plan& P = h->P;
+  h->max_batch = max_batch;
+  h->max_scen = max_scen;
+  h->C = pick_tile_cols(P.n_x, max_batch * max_scen);
+  if (device < 0) {  // host analysis only: structure queries work, compute calls return PF_ERR_STATE
+    *out = h;
+    return PF_OK;
+  }
+  if (!set_device(h)) { g_build_err = "cudaSetDevice failed"; delete h; return PF_ERR_CUDA; }
+
+  DevNet& d = h->dn;
+  d.n_b = P.n_b; d.n_l = P.n_l; d.n_g = P.n_g; d.n_x = P.n_x; d.n_u = P.n_u; d.m = P.m;
+  d.n_r = P.n_r; d.n_h = P.n_h; d.r0 = P.r0; d.g_r = P.g_r; d.n_gb = P.n_gb;
+  d.nblk = (int)P.blk_bus.size();
+  d.nnz_jb = (int)P.jb_idx.size(); d.nnz_gx = (int)P.gx_idx.size(); d.nnz_gu = (int)P.gu_idx.size();
+  d.nnz_a = (int)P.a_idx.size(); d.nnz_lu = (int)P.lu_idx.size();
+  d.nlevL = (int)P.levL_ptr.size() - 1; d.nlevU = (int)P.levU_ptr.size() - 1;
+
+  std::vector<double> coef(8 * (size_t)n_l), gsh(n_b), bsh(n_b), cq(c_quad, c_quad + n_g), cl(c_lin, c_lin + n_g);
+  for (int l = 0; l < n_l; ++l) {
+    coef[0 * n_l + l] = Y_ff[2 * l]; coef[1 * n_l + l] = Y_ff[2 * l + 1];
+    coef[2 * n_l + l] = Y_ft[2 * l]; coef[3 * n_l + l] = Y_ft[2 * l + 1];
+    coef[4 * n_l + l] = Y_tf[2 * l]; coef[5 * n_l + l] = Y_tf[2 * l + 1];
+    coef[6 * n_l + l] = Y_tt[2 * l]; coef[7 * n_l + l] = Y_tt[2 * l + 1];
+  }
+  for (int i = 0; i < n_b; ++i) { gsh[i] = Y_sh[2 * i]; bsh[i] = Y_sh[2 * i + 1]; }
+  std::vector<double> pd(p_d, p_d + n_b), qd(q_d, q_d + n_b);
+  std::vector<int> lf(line_from, line_from + n_l), lt(line_to, line_to + n_l), gb(gen_bus, gen_bus + n_g);
+  std::vector<int> gbus;
+  for (int i = 0; i < n_b; ++i) if (P.bus_gen[i] >= 0) gbus.push_back(i);
+
+  bool ok = up(h, lf, &d.lf) && up(h, lt, &d.lt) && up(h, coef, &d.coef) && up(h, gsh, &d.gsh) &&
+            up(h, bsh, &d.bsh) && up(h, gb, &d.gen_bus) && up(h, P.bus_gen, &d.bus_gen) &&
+            up(h, cq, &d.c_quad) && up(h, cl, &d.c_lin) && up(h, pd, &d.p_d0) && up(h, qd, &d.q_d0) &&
+            up(h, P.x_th, &d.x_th) && up(h, P.x_v, &d.x_v) && up(h, P.u_v, &d.u_v) && up(h, P.u_p, &d.u_p) &&
+            up(h, P.bus_rP, &d.bus_rP) && up(h, P.bus_rQ, &d.bus_rQ) && up(h, P.line_hf, &d.line_hf) &&
+            up(h, P.line_ht, &d.line_ht) && up(h, P.inc_ptr, &d.inc_ptr) && up(h, P.inc_line, &d.inc_line) &&
+            up(h, P.inc_off_th, &d.inc_off_th) && up(h, P.inc_off_v, &d.inc_off_v) &&
+            up(h, P.jb_ptr, &d.jb_ptr) && up(h, P.jb_self_th, &d.jb_self_th) && up(h, P.jb_self_v, &d.jb_self_v) &&
+            up(h, P.gx_src, &d.gx_src) && up(h, P.gu_src, &d.gu_src) && up(h, P.a_ptr, &d.a_ptr) &&
+            up(h, P.a_src, &d.a_src) && up(h, P.ah_off, &d.ah_off) && up(h, P.h_line, &d.h_line) &&
+            up(h, P.h_end, &d.h_end) && up(h, P.blk_ptr, &d.blk_ptr) && up(h, P.lu_ptr, &d.lu_ptr) &&
+            up(h, P.lu_idx, &d.lu_idx) && up(h, P.lu_diag, &d.lu_diag) && up(h, P.lu_src, &d.lu_src) &&
+            up(h, P.lu_tpos, &d.lu_tpos) && up(h, P.upd_ptr, &d.upd_ptr) && up(h, P.upd_dst, &d.upd_dst) &&
+            up(h, P.levL_ptr, &d.levL_ptr) && up(h, P.levL_blk, &d.levL_blk) && up(h, P.levU_ptr, &d.levU_ptr) &&
+            up(h, P.levU_blk, &d.levU_blk) && up(h, P.guc_ptr, &d.guc_ptr) && up(h, P.guc_row, &d.guc_row) &&
+            up(h, P.guc_src, &d.guc_src) && up(h, P.gur_ptr, &d.gur_ptr) && up(h, P.gur_col, &d.gur_col) &&
+            up(h, P.gur_src, &d.gur_src) && up(h, P.bus_pth, &d.bus_pth) && up(h, P.bus_pv, &d.bus_pv) &&
+            up(h, gbus, &d.gbus);
+  Work& w = h->w;
+  const size_t S = max_scen;
+  w.max_tiles = max_scen * ((max_batch + h->C - 1) / h->C);
+  const size_t T = w.max_tiles, C = h->C;
+  ok = ok && alloc(h, S * d.nnz_jb, &w.jb) && alloc(h, S * d.nnz_gu, &w.gu) && alloc(h, S * d.nnz_lu, &w.lu) &&
+       alloc(h, S * d.nnz_lu, &w.luT) && alloc(h, S * d.n_x, &w.rowmax) && alloc(h, S * LS_N * d.n_l, &w.ls) &&
+       alloc(h, S * BS_N * d.n_b, &w.bs) && alloc(h, S * 4 * d.n_l, &w.sflow) && alloc(h, 2 * S, &w.info) &&
+       alloc(h, T * d.n_x * C, &w.slabZ) && alloc(h, T * d.n_x * C, &w.slabW) &&
+       alloc(h, T * d.n_u * C, &w.hu) && alloc(h, T * d.n_g * 2 * C, &w.mu);
+  if (!ok) {
+    g_build_err = std::string("device allocation/upload failed: ") + cudaGetErrorString(cudaGetLastError());
+    pf_destroy(h);
+    return PF_ERR_CUDA;
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    g_build_err = std::string("build sync: ") + cudaGetErrorString(cudaGetLastError());
+    pf_destroy(h);
+    return PF_ERR_CUDA;
+  }
+  *out = h;
+  return PF_OK;
+}
+
+void pf_destroy(pf_net* h) {
+  if (!h) return;
+  if (h->device >= 0) cudaSetDevice(h->device);
+  for (void* p : h->allocs) cudaFree(p);
+  delete h;
+}
+
+pf_status pf_query(const pf_net* h, pf_dims* o) {
+  if (!h || !o) return PF_ERR_ARG;
+  const Plan& P = h->P;
+  o->n_b = P.n_b; o->n_l = P.n_l; o->n_g = P.n_g; o->n_x = P.n_x; o->n_u = P.n_u; o->m = P.m;
+  o->n_r = P.n_r; o->n_h = P.n_h; o->ref_bus = P.r0; o->ref_gen = P.g_r;
+  o->nnz_gx = (int)P.gx_idx.size(); o->nnz_gu = (int)P.gu_idx.size(); o->nnz_a = (int)P.a_idx.size();
+  o->nnz_lu = (int)P.lu_idx.size(); o->n_blocks = (int)P.blk_bus.size();
+  o->n_levels_l = (int)P.levL_ptr.size() - 1; o->n_levels_u = (int)P.levU_ptr.size() - 1;
+  o->max_batch = h->max_batch; o->max_scen = h->max_scen; o->tile_cols = h->C;
+  return PF_OK;
+}
+
+pf_status pf_get_structure(const pf_net* h, int32_t which, int32_t* out) {
+  if (!h || !out) return PF_ERR_ARG;
+  const Plan& P = h->P;
+  const std::vector<int>* v = nullptr;
+  switch (which) {
+    case PF_X_THETA: v = &P.x_th; break;
+    case PF_X_V: v = &P.x_v; break;
+    case PF_U_V: v = &P.u_v; break;
+    case PF_U_P: v = &P.u_p; break;
+    case PF_GX_PTR: v = &P.gx_ptr; break;
+    case PF_GX_IDX: v = &P.gx_idx; break;
+    case PF_GU_PTR: v = &P.gu_ptr; break;
+    case PF_GU_IDX: v = &P.gu_idx; break;
+    case PF_A_PTR: v = &P.a_ptr; break;
+    case PF_A_IDX: v = &P.a_idx; break;
+    case PF_BUS_ORDER: v = &P.bus_order; break;
+    case PF_PERM: v = &P.perm; break;
+    case PF_BLOCK_PTR: v = &P.blk_ptr; break;
+    case PF_LU_PTR: v = &P.lu_ptr; break;
+    case PF_LU_IDX: v = &P.lu_idx; break;
+    case PF_LEVEL_L_PTR: v = &P.levL_ptr; break;
+    case PF_LEVEL_L_BLK: v = &P.levL_blk; break;
+    case PF_LEVEL_U_PTR: v = &P.levU_ptr; break;
+    case PF_LEVEL_U_BLK: v = &P.levU_blk; break;
+    default: return PF_ERR_ARG;
+  }
+  if (!v->empty()) std::memcpy(out, v->data(), v->size() * sizeof(int32_t));
+  return PF_OK;
+}
+
+const char* pf_last_error(const pf_net* h) { return h ? h->err.c_str() : g_build_err.c_str(); }
+
+int64_t pf_launch_count(const pf_net* h) { return h ? h->launches : 0; }
+
+pf_status pf_eval_constraints(pf_net* h, int32_t n_scen, const double* v, const double* theta,
+                              const double* p_g, const double* q_g, const double* p_d, const double* q_d,
+                              double* G, double* H, double* s_flow, void* stream) {
+  if (!h) return PF_ERR_ARG;
+  if (!v || !theta || !p_g || !q_g || !G || n_scen < 1) { h->err = "pf_eval_constraints: bad argument"; return PF_ERR_ARG; }
+  if (n_scen > h->max_scen) { h->err = "pf_eval_constraints: n_scen > max_scen"; return PF_ERR_CAPACITY; }
+  if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
+  h->launches += launch_eval(h->dn, h->w, n_scen, v, theta, p_g, q_g, p_d, q_d, G, H, s_flow, (cudaStream_t)stream);
+  return cuda_check(h, "pf_eval_constraints");
+}
+
+pf_status pf_jacobian(pf_net* h, int32_t n_scen, const double* v, const double* theta, double* Gx_val,
+                      double* Gu_val, double* A_val, int32_t* info, void* stream) {
+  if (!h) return PF_ERR_ARG;
+  if (!v || !theta || n_scen < 1) { h->err = "pf_jacobian: bad argument"; return PF_ERR_ARG; }
+  if (n_scen > h->max_scen) { h->err = "pf_jacobian: n_scen > max_scen"; return PF_ERR_CAPACITY; }
+  if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
+  h->launches += launch_jacobian(h->dn, h->w, n_scen, v, theta, Gx_val, Gu_val, A_val, info, (cudaStream_t)stream);
+  h->lu_scen = n_scen;
+  return cuda_check(h, "pf_jacobian");
+}
+
+pf_status pf_reduced_hessian_batch(pf_net* h, int32_t n_scen, const double* v, const double* theta,
+                                   const double* p_d, const double* lambda, const double* y,
+                                   const double* sigma_s, const double* sigma_x, const double* V,
+                                   int32_t col0, int32_t N, double* KV, void* stream) {
+  if (!h) return PF_ERR_ARG;
+  (void)v; (void)theta;  // the point's state was cached by pf_jacobian (same v, theta)
+  if (!lambda || !y || !KV || n_scen < 1 || N < 0) { h->err = "pf_reduced_hessian_batch: bad argument"; return PF_ERR_ARG; }
+  if (n_scen > h->max_scen || N > h->max_batch) { h->err = "pf_reduced_hessian_batch: capacity"; return PF_ERR_CAPACITY; }
+  if (!V && (col0 < 0 || col0 + N > h->P.n_u)) { h->err = "pf_reduced_hessian_batch: columns out of range"; return PF_ERR_ARG; }
+  if (h->lu_scen < n_scen) { h->err = "pf_reduced_hessian_batch: call pf_jacobian first"; return PF_ERR_STATE; }
+  if (N == 0) return PF_OK;
+  if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  h->launches += launch_prep(h->dn, h->w, n_scen, p_d, lambda, y, sigma_s, sigma_x, st);
+  h->launches += launch_reduce(h->dn, h->w, h->C, n_scen, V, col0, N, KV, st);
+  return cuda_check(h, "pf_reduced_hessian_batch");
+}
+
+pf_status pf_condensed_kkt_solve(pf_net* h, int32_t n_scen, double* K, const double* sigma_u, double delta_w,
+                                 double* rhs, int32_t nrhs, int32_t* info, void* stream) {
+  if (!h) return PF_ERR_ARG;
+  if (!K || n_scen < 1 || nrhs < 0 || (nrhs > 0 && !rhs)) { h->err = "pf_condensed_kkt_solve: bad argument"; return PF_ERR_ARG; }
+  if (n_scen > h->max_scen) { h->err = "pf_condensed_kkt_solve: n_scen > max_scen"; return PF_ERR_CAPACITY; }
+  if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
+  h->launches += launch_chol(h->dn, n_scen, K, sigma_u, delta_w, rhs, nrhs, info, h->w.info + h->max_scen,
+                             (cudaStream_t)stream);
+  return cuda_check(h, "pf_condensed_kkt_solve");
+}
+
+}  // extern "C"

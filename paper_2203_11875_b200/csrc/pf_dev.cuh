@@ -1,0 +1,52 @@
+// pf_dev.cuh — device-side views of the network plan and per-handle workspaces.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace pf {
+
+// Network-level device data (read-only, shared by all scenarios).
+struct DevNet {
+  int n_b, n_l, n_g, n_x, n_u, m, n_r, n_h, r0, g_r, n_gb, nblk;
+  int nnz_jb, nnz_gx, nnz_gu, nnz_a, nnz_lu;
+  int nlevL, nlevU;
+  const int *lf, *lt;           // [n_l] C_f, C_t
+  const double *coef;           // [8][n_l]: g_ff b_ff g_ft b_ft g_tf b_tf g_tt b_tt
+  const double *gsh, *bsh;      // [n_b] Y_sh
+  const int *gen_bus, *bus_gen; // [n_g], [n_b]
+  const double *c_quad, *c_lin; // [n_g]
+  const double *p_d0, *q_d0;    // [n_b] base loads
+  const int *x_th, *x_v, *u_v, *u_p, *bus_rP, *bus_rQ, *line_hf, *line_ht;
+  const int *inc_ptr, *inc_line, *inc_off_th, *inc_off_v;
+  const int *jb_ptr, *jb_self_th, *jb_self_v;
+  const int *gx_src, *gu_src, *a_ptr, *a_src, *ah_off, *h_line, *h_end;
+  const int *blk_ptr, *lu_ptr, *lu_idx, *lu_diag, *lu_src, *lu_tpos, *upd_ptr, *upd_dst;
+  const int *levL_ptr, *levL_blk, *levU_ptr, *levU_blk;
+  const int *guc_ptr, *guc_row, *guc_src, *gur_ptr, *gur_col, *gur_src;
+  const int *bus_pth, *bus_pv;
+  const int *gbus;              // [n_gb] generator buses ascending (the r buses)
+};
+
+// Per-scenario point state, SoA.  Line state (LS_*) and bus state (BS_*).
+enum { LS_VF, LS_VT, LS_C, LS_S, LS_SPF, LS_SQF, LS_SPT, LS_SQT,
+       LS_WC, LS_WS, LS_Y2F, LS_Y2T, LS_SGF, LS_SGT, LS_DF, LS_DT, LS_N };
+enum { BS_V, BS_MUP, BS_MUQ, BS_WD2, BS_SRP, BS_SRQ, BS_SXT, BS_SXV, BS_N };
+
+struct Work {
+  double* jb;      // [max_scen][nnz_jb]  J_bus values
+  double* gu;      // [max_scen][nnz_gu]  G_u values (internal copy)
+  double* lu;      // [max_scen][nnz_lu]  LU values (row-wise)
+  double* luT;     // [max_scen][nnz_lu]  transposed values: luT[e] = lu[tpos[e]]
+  double* rowmax;  // [max_scen][n_x]     pivot threshold scale (R18)
+  double* ls;      // [max_scen][LS_N][n_l]
+  double* bs;      // [max_scen][BS_N][n_b]
+  double* sflow;   // [max_scen][4][n_l]
+  int* info;       // [max_scen] internal pivot info
+  double* slabZ;   // [max_tiles][n_x][C]
+  double* slabW;   // [max_tiles][n_x][C]
+  double* hu;      // [max_tiles][n_u][C]
+  double* mu;      // [max_tiles][n_gb][2][C]
+  int max_tiles;
+};
+
+}  // namespace pf

@@ -1,0 +1,413 @@
+// pf_eval.cu — ψ-basis evaluation (A2/A3), ψ-chain Jacobians (A4), the
+// level-scheduled numeric LU refactorization of G_x (A5) and the per-scenario
+// ψ weights of the Hessian-vector product (A6).  sm_100a, FP64.
+//
+// Readings: R1 conj in s_f, R2/R3 L_line blocks, R4 M entries,
+// R5 ψ orientation Δ = θ_f − θ_t, R8 implicit p_ref, R18 static pivots.
+#include "pf_launch.h"
+
+#include <climits>
+
+namespace pf {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int blocks_for(long long n, int t = kThreads) {
+  long long b = (n + t - 1) / t;
+  if (b < 1) b = 1;
+  if (b > 148LL * 64) b = 148LL * 64;
+  return (int)b;
+}
+
+struct LineCoef { double gff, bff, gft, bft, gtf, btf, gtt, btt; };
+
+__device__ __forceinline__ LineCoef load_coef(const DevNet& n, int l) {
+  LineCoef c;
+  c.gff = __ldg(n.coef + 0 * n.n_l + l); c.bff = __ldg(n.coef + 1 * n.n_l + l);
+  c.gft = __ldg(n.coef + 2 * n.n_l + l); c.bft = __ldg(n.coef + 3 * n.n_l + l);
+  c.gtf = __ldg(n.coef + 4 * n.n_l + l); c.btf = __ldg(n.coef + 5 * n.n_l + l);
+  c.gtt = __ldg(n.coef + 6 * n.n_l + l); c.btt = __ldg(n.coef + 7 * n.n_l + l);
+  return c;
+}
+
+// ψ^c = v_f v_t cos Δ, ψ^s = v_f v_t sin Δ (R5), and the line-local
+// L_line products (eq. base:powerlines P:L128–154 with R1–R3).
+struct Flows { double c, s, pc, ps, spf, sqf, spt, sqt; };
+
+__device__ __forceinline__ Flows line_flows(const LineCoef& k, double vf, double vt, double thf, double tht) {
+  Flows o;
+  sincos(thf - tht, &o.s, &o.c);
+  const double vv = vf * vt;
+  o.pc = vv * o.c;
+  o.ps = vv * o.s;
+  o.spf = k.gft * o.pc + k.bft * o.ps + k.gff * vf * vf;
+  o.sqf = -k.bft * o.pc + k.gft * o.ps - k.bff * vf * vf;
+  o.spt = k.gtf * o.pc - k.btf * o.ps + k.gtt * vt * vt;
+  o.sqt = -k.btf * o.pc - k.gtf * o.ps - k.btt * vt * vt;
+  return o;
+}
+
+// ---------------------------------------------------------------- A2/A3
+__global__ void k_line_eval(DevNet n, Work w, int n_scen, const double* __restrict__ v,
+                            const double* __restrict__ th, double* __restrict__ H,
+                            double* __restrict__ s_out) {
+  const long long total = (long long)n_scen * n.n_l;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / n.n_l), l = (int)(t % n.n_l);
+    const int f = __ldg(n.lf + l), to = __ldg(n.lt + l);
+    const double* vs = v + (size_t)s * n.n_b;
+    const double* ts = th + (size_t)s * n.n_b;
+    Flows o = line_flows(load_coef(n, l), vs[f], vs[to], ts[f], ts[to]);
+    double* sf = w.sflow + (size_t)s * 4 * n.n_l;
+    sf[l] = o.spf; sf[n.n_l + l] = o.sqf; sf[2 * n.n_l + l] = o.spt; sf[3 * n.n_l + l] = o.sqt;
+    if (s_out) {
+      double* so = s_out + (size_t)s * 4 * n.n_l;
+      so[l] = o.spf; so[n.n_l + l] = o.sqf; so[2 * n.n_l + l] = o.spt; so[3 * n.n_l + l] = o.sqt;
+    }
+    if (H) {  // eq. linelimitsvec
+      double* hs = H + (size_t)s * 2 * n.n_l;
+      hs[l] = o.spf * o.spf + o.sqf * o.sqf;
+      hs[n.n_l + l] = o.spt * o.spt + o.sqt * o.sqt;
+    }
+  }
+}
+
+// G = Mψ + [p_d − C_g p_g ; q_d − C_g q_g] (eq. base:powerflow P:L109–125).
+// Row P_i of M gathers the line ends incident to i (R4) plus G_ii ψ^d_i;
+// G_ii's Y_ff / Y_tt parts already sit in s_p^f / s_p^t, the shunt remains.
+__global__ void k_bus_eval(DevNet n, Work w, int n_scen, const double* __restrict__ v,
+                           const double* __restrict__ p_g, const double* __restrict__ q_g,
+                           const double* __restrict__ p_d, const double* __restrict__ q_d,
+                           double* __restrict__ G) {
+  const long long total = (long long)n_scen * n.n_b;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / n.n_b), i = (int)(t % n.n_b);
+    const double* sf = w.sflow + (size_t)s * 4 * n.n_l;
+    double P = 0.0, Q = 0.0;
+    for (int e = __ldg(n.inc_ptr + i); e < __ldg(n.inc_ptr + i + 1); ++e) {
+      const int l = __ldg(n.inc_line + e);
+      const bool from = __ldg(n.lf + l) == i;
+      P += from ? sf[l] : sf[2 * n.n_l + l];
+      Q += from ? sf[n.n_l + l] : sf[3 * n.n_l + l];
+    }
+    const double vi = v[(size_t)s * n.n_b + i];
+    P += __ldg(n.gsh + i) * vi * vi;
+    Q -= __ldg(n.bsh + i) * vi * vi;
+    const int g = __ldg(n.bus_gen + i);
+    if (g >= 0) { P -= p_g[(size_t)s * n.n_g + g]; Q -= q_g[(size_t)s * n.n_g + g]; }
+    P += p_d ? p_d[(size_t)s * n.n_b + i] : __ldg(n.p_d0 + i);
+    Q += q_d ? q_d[(size_t)s * n.n_b + i] : __ldg(n.q_d0 + i);
+    G[(size_t)s * 2 * n.n_b + i] = P;
+    G[(size_t)s * 2 * n.n_b + n.n_b + i] = Q;
+  }
+}
+
+// ---------------------------------------------------------------- A4
+__global__ void k_line_state(DevNet n, Work w, int n_scen, const double* __restrict__ v,
+                             const double* __restrict__ th) {
+  const long long total = (long long)n_scen * n.n_l;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / n.n_l), l = (int)(t % n.n_l);
+    const int f = __ldg(n.lf + l), to = __ldg(n.lt + l);
+    const double vf = v[(size_t)s * n.n_b + f], vt = v[(size_t)s * n.n_b + to];
+    Flows o = line_flows(load_coef(n, l), vf, vt, th[(size_t)s * n.n_b + f], th[(size_t)s * n.n_b + to]);
+    double* ls = w.ls + (size_t)s * LS_N * n.n_l;
+    ls[LS_VF * n.n_l + l] = vf; ls[LS_VT * n.n_l + l] = vt;
+    ls[LS_C * n.n_l + l] = o.c; ls[LS_S * n.n_l + l] = o.s;
+    ls[LS_SPF * n.n_l + l] = o.spf; ls[LS_SQF * n.n_l + l] = o.sqf;
+    ls[LS_SPT * n.n_l + l] = o.spt; ls[LS_SQT * n.n_l + l] = o.sqt;
+  }
+}
+
+// ∂(s_p, s_q) of one line end w.r.t. the local variables (v_f, v_t, θ_f, θ_t):
+// J_ψ rows ∂ψ^c = (v_t c, v_f c, −ψ^s, ψ^s), ∂ψ^s = (v_t s, v_f s, ψ^c, −ψ^c),
+// composed with the L_line coefficients.
+struct EndGrad { double p[4], q[4]; };
+
+__device__ __forceinline__ EndGrad end_grad(const LineCoef& k, double vf, double vt, double c, double s, bool from) {
+  const double pc = vf * vt * c, ps = vf * vt * s;
+  const double dc[4] = {vt * c, vf * c, -ps, ps};
+  const double ds[4] = {vt * s, vf * s, pc, -pc};
+  EndGrad g;
+  if (from) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) { g.p[a] = k.gft * dc[a] + k.bft * ds[a]; g.q[a] = -k.bft * dc[a] + k.gft * ds[a]; }
+    g.p[0] += 2.0 * k.gff * vf; g.q[0] -= 2.0 * k.bff * vf;
+  } else {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) { g.p[a] = k.gtf * dc[a] - k.btf * ds[a]; g.q[a] = -k.btf * dc[a] - k.gtf * ds[a]; }
+    g.p[1] += 2.0 * k.gtt * vt; g.q[1] -= 2.0 * k.btt * vt;
+  }
+  return g;
+}
+
+// J_bus rows P_i, Q_i: one thread per (scenario, bus), ascending incident
+// lines (parallel lines accumulate into the same entries, deterministically).
+__global__ void k_jbus(DevNet n, Work w, int n_scen) {
+  const long long total = (long long)n_scen * n.n_b;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / n.n_b), i = (int)(t % n.n_b);
+    double* jb = w.jb + (size_t)s * n.nnz_jb;
+    const double* ls = w.ls + (size_t)s * LS_N * n.n_l;
+    double* rp = jb + __ldg(n.jb_ptr + i);
+    double* rq = jb + __ldg(n.jb_ptr + n.n_b + i);
+    const int len = __ldg(n.jb_ptr + i + 1) - __ldg(n.jb_ptr + i);
+    for (int a = 0; a < len; ++a) { rp[a] = 0.0; rq[a] = 0.0; }
+    double pv = 0, pth = 0, qv = 0, qth = 0;
+    for (int e = __ldg(n.inc_ptr + i); e < __ldg(n.inc_ptr + i + 1); ++e) {
+      const int l = __ldg(n.inc_line + e);
+      const bool from = __ldg(n.lf + l) == i;
+      EndGrad g = end_grad(load_coef(n, l), ls[LS_VF * n.n_l + l], ls[LS_VT * n.n_l + l],
+                           ls[LS_C * n.n_l + l], ls[LS_S * n.n_l + l], from);
+      const int own_v = from ? 0 : 1, oth_v = from ? 1 : 0, own_t = from ? 2 : 3, oth_t = from ? 3 : 2;
+      pv += g.p[own_v]; qv += g.q[own_v]; pth += g.p[own_t]; qth += g.q[own_t];
+      const int ov = __ldg(n.inc_off_v + e), ot = __ldg(n.inc_off_th + e);
+      rp[ov] += g.p[oth_v]; rq[ov] += g.q[oth_v];
+      if (ot >= 0) { rp[ot] += g.p[oth_t]; rq[ot] += g.q[oth_t]; }
+    }
+    const int sv = __ldg(n.jb_self_v + i), st = __ldg(n.jb_self_th + i);
+    // shunt part of G_ii ψ^d_i (R4): ∂/∂v_i of g_sh v_i², −b_sh v_i²
+    const double vb = w.bs[(size_t)s * BS_N * n.n_b + BS_V * n.n_b + i];
+    pv += 2.0 * __ldg(n.gsh + i) * vb;
+    qv -= 2.0 * __ldg(n.bsh + i) * vb;
+    rp[sv] += pv; rq[sv] += qv;
+    if (st >= 0) { rp[st] += pth; rq[st] += qth; }
+  }
+}
+
+__global__ void k_bus_v(DevNet n, Work w, int n_scen, const double* __restrict__ v) {
+  const long long total = (long long)n_scen * n.n_b;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / n.n_b), i = (int)(t % n.n_b);
+    w.bs[(size_t)s * BS_N * n.n_b + BS_V * n.n_b + i] = v[(size_t)s * n.n_b + i];
+  }
+}
+
+// Gathers J_bus values into the G_x / G_u / A patterns; h rows of A from the
+// line ends: ∇H = 2(s_p ∇s_p + s_q ∇s_q).
+__global__ void k_gather(DevNet n, Work w, int n_scen, double* __restrict__ Gx,
+                         double* __restrict__ Gu, double* __restrict__ A) {
+  const int per = n.nnz_gx + n.nnz_gu + n.nnz_a;
+  const long long total = (long long)n_scen * per;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / per);
+    int k = (int)(t % per);
+    const double* jb = w.jb + (size_t)s * n.nnz_jb;
+    if (k < n.nnz_gx) {
+      if (Gx) Gx[(size_t)s * n.nnz_gx + k] = jb[__ldg(n.gx_src + k)];
+      continue;
+    }
+    k -= n.nnz_gx;
+    if (k < n.nnz_gu) {
+      const int src = __ldg(n.gu_src + k);
+      const double val = src >= 0 ? jb[src] : -1.0;  // −C_g p_g entry (eq. powerflowvec)
+      w.gu[(size_t)s * n.nnz_gu + k] = val;
+      if (Gu) Gu[(size_t)s * n.nnz_gu + k] = val;
+      continue;
+    }
+    k -= n.nnz_gu;
+    if (!A) continue;
+    const int src = __ldg(n.a_src + k);
+    if (src >= 0) { A[(size_t)s * n.nnz_a + k] = jb[src]; continue; }
+    // h row owning position k: binary search in a_ptr over rows [n_r, m)
+    int lo = n.n_r, hi = n.m - 1;
+    while (lo < hi) { int mid = (lo + hi + 1) >> 1; if (__ldg(n.a_ptr + mid) <= k) lo = mid; else hi = mid - 1; }
+    const int h = lo - n.n_r, base = __ldg(n.a_ptr + lo);
+    const int l = __ldg(n.h_line + h), e = __ldg(n.h_end + h);
+    const double* ls = w.ls + (size_t)s * LS_N * n.n_l;
+    EndGrad g = end_grad(load_coef(n, l), ls[LS_VF * n.n_l + l], ls[LS_VT * n.n_l + l],
+                         ls[LS_C * n.n_l + l], ls[LS_S * n.n_l + l], e == 0);
+    const double sp = e == 0 ? ls[LS_SPF * n.n_l + l] : ls[LS_SPT * n.n_l + l];
+    const double sq = e == 0 ? ls[LS_SQF * n.n_l + l] : ls[LS_SQT * n.n_l + l];
+    for (int a = 0; a < 4; ++a)
+      if (__ldg(n.ah_off + 4 * h + a) == k - base) A[(size_t)s * n.nnz_a + k] = 2.0 * (sp * g.p[a] + sq * g.q[a]);
+  }
+}
+
+// ---------------------------------------------------------------- A5
+// Numeric LU of P G_x Pᵀ with the fixed symbolic pattern and static pivots
+// (R18): up-looking IKJ rows, one warp per bus block, blocks of one level in
+// parallel, __syncthreads between levels.  One CTA per scenario.
+constexpr int kLuThreads = 512;
+
+__global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int* __restrict__ info_out) {
+  const int s = blockIdx.x;
+  double* lu = w.lu + (size_t)s * n.nnz_lu;
+  double* luT = w.luT + (size_t)s * n.nnz_lu;
+  double* rowmax = w.rowmax + (size_t)s * n.n_x;
+  const double* jb = w.jb + (size_t)s * n.nnz_jb;
+  __shared__ int s_info;
+  if (threadIdx.x == 0) s_info = INT_MAX;
+  for (int r = threadIdx.x; r < n.n_x; r += blockDim.x) {
+    double mx = 0.0;
+    for (int e = __ldg(n.lu_ptr + r); e < __ldg(n.lu_ptr + r + 1); ++e) {
+      const int src = __ldg(n.lu_src + e);
+      const double val = src >= 0 ? jb[src] : 0.0;
+      lu[e] = val;
+      mx = fmax(mx, fabs(val));
+    }
+    rowmax[r] = mx;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  for (int lev = 0; lev < n.nlevL; ++lev) {
+    const int b0 = __ldg(n.levL_ptr + lev), b1 = __ldg(n.levL_ptr + lev + 1);
+    for (int bi = b0 + warp; bi < b1; bi += nwarp) {
+      const int p = __ldg(n.levL_blk + bi);
+      for (int r = __ldg(n.blk_ptr + p); r < __ldg(n.blk_ptr + p + 1); ++r) {
+        const int dr = __ldg(n.lu_diag + r);
+        for (int e = __ldg(n.lu_ptr + r); e < dr; ++e) {
+          const int k = __ldg(n.lu_idx + e);
+          const double l = lu[e] / lu[__ldg(n.lu_diag + k)];
+          __syncwarp();
+          if (lane == 0) lu[e] = l;
+          const int u0 = __ldg(n.lu_diag + k) + 1;
+          const int q0 = __ldg(n.upd_ptr + e), cnt = __ldg(n.upd_ptr + e + 1) - q0;
+          for (int t = lane; t < cnt; t += 32) lu[__ldg(n.upd_dst + q0 + t)] -= l * lu[u0 + t];
+          __syncwarp();
+        }
+        if (lane == 0) {
+          const double d = lu[dr];
+          if (!(fabs(d) >= 1e-12 * rowmax[r]) || !isfinite(d) || d == 0.0) atomicMin(&s_info, r + 1);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < n.nnz_lu; e += blockDim.x) luT[e] = lu[__ldg(n.lu_tpos + e)];
+  if (threadIdx.x == 0) {
+    const int v = s_info == INT_MAX ? 0 : s_info;
+    w.info[s] = v;
+    if (info_out) info_out[s] = v;
+  }
+}
+
+// ---------------------------------------------------------------- A6
+// μ̃ (bus multipliers of ∇²p_i, ∇²q_i): λ on g rows, y_r on r rows and
+// (2c1 p_ref + c2)_{g_r} on P_r0 (R8); Σ of the r rows (with the p_ref
+// curvature 2c1_{g_r} folded into P_r0) and Σ_x of each bus variable.
+__global__ void k_prep_bus1(DevNet n, Work w, int n_scen, const double* __restrict__ p_d,
+                            const double* __restrict__ lam, const double* __restrict__ y,
+                            const double* __restrict__ sig_s, const double* __restrict__ sig_x) {
+  const long long total = (long long)n_scen * n.n_b;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / n.n_b), i = (int)(t % n.n_b);
+    const double* L = lam + (size_t)s * n.n_x;
+    const double* Y = y + (size_t)s * n.m;
+    double* bs = w.bs + (size_t)s * BS_N * n.n_b;
+    const int xt = __ldg(n.x_th + i), xv = __ldg(n.x_v + i), rp = __ldg(n.bus_rP + i), rq = __ldg(n.bus_rQ + i);
+    double muP = (xt >= 0 ? L[xt] : 0.0) + (rp >= 0 ? Y[rp] : 0.0);
+    double muQ = (xv >= 0 ? L[xv] : 0.0) + (rq >= 0 ? Y[rq] : 0.0);
+    double srp = (rp >= 0 && sig_s) ? sig_s[(size_t)s * n.m + rp] : 0.0;
+    if (i == n.r0) {
+      const double* ls = w.ls + (size_t)s * LS_N * n.n_l;
+      double P = 0.0;
+      for (int e = __ldg(n.inc_ptr + i); e < __ldg(n.inc_ptr + i + 1); ++e) {
+        const int l = __ldg(n.inc_line + e);
+        P += __ldg(n.lf + l) == i ? ls[LS_SPF * n.n_l + l] : ls[LS_SPT * n.n_l + l];
+      }
+      const double vi = bs[BS_V * n.n_b + i];
+      P += __ldg(n.gsh + i) * vi * vi;
+      const double pref = P + (p_d ? p_d[(size_t)s * n.n_b + i] : __ldg(n.p_d0 + i));
+      const double c1 = __ldg(n.c_quad + n.g_r), c2 = __ldg(n.c_lin + n.g_r);
+      muP += 2.0 * c1 * pref + c2;
+      srp += 2.0 * c1;
+    }
+    bs[BS_MUP * n.n_b + i] = muP;
+    bs[BS_MUQ * n.n_b + i] = muQ;
+    bs[BS_SRP * n.n_b + i] = srp;
+    bs[BS_SRQ * n.n_b + i] = (rq >= 0 && sig_s) ? sig_s[(size_t)s * n.m + rq] : 0.0;
+    bs[BS_SXT * n.n_b + i] = (xt >= 0 && sig_x) ? sig_x[(size_t)s * n.n_x + xt] : 0.0;
+    bs[BS_SXV * n.n_b + i] = (xv >= 0 && sig_x) ? sig_x[(size_t)s * n.n_x + xv] : 0.0;
+  }
+}
+
+// w̄ = Mᵀμ̃ + L_lineᵀ(2ŷ ⊙ s) per line (A6): with the end "efforts"
+// E = μ̃ + 2ŷ s, w̄^c = g_ft E_fp − b_ft E_fq + g_tf E_tp − b_tf E_tq,
+// w̄^s = b_ft E_fp + g_ft E_fq − b_tf E_tp − g_tf E_tq; the v² columns give
+// the per-end diagonal parts d_f, d_t of w̄^d.
+__global__ void k_prep_line(DevNet n, Work w, int n_scen, const double* __restrict__ y,
+                            const double* __restrict__ sig_s) {
+  const long long total = (long long)n_scen * n.n_l;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / n.n_l), l = (int)(t % n.n_l);
+    double* ls = w.ls + (size_t)s * LS_N * n.n_l;
+    const double* bs = w.bs + (size_t)s * BS_N * n.n_b;
+    const int f = __ldg(n.lf + l), to = __ldg(n.lt + l);
+    const int hf = __ldg(n.line_hf + l), ht = __ldg(n.line_ht + l);
+    const double* Y = y + (size_t)s * n.m;
+    const double y2f = hf >= 0 ? 2.0 * Y[n.n_r + hf] : 0.0;
+    const double y2t = ht >= 0 ? 2.0 * Y[n.n_r + ht] : 0.0;
+    const double sgf = (hf >= 0 && sig_s) ? sig_s[(size_t)s * n.m + n.n_r + hf] : 0.0;
+    const double sgt = (ht >= 0 && sig_s) ? sig_s[(size_t)s * n.m + n.n_r + ht] : 0.0;
+    const LineCoef k = load_coef(n, l);
+    const double Efp = bs[BS_MUP * n.n_b + f] + y2f * ls[LS_SPF * n.n_l + l];
+    const double Efq = bs[BS_MUQ * n.n_b + f] + y2f * ls[LS_SQF * n.n_l + l];
+    const double Etp = bs[BS_MUP * n.n_b + to] + y2t * ls[LS_SPT * n.n_l + l];
+    const double Etq = bs[BS_MUQ * n.n_b + to] + y2t * ls[LS_SQT * n.n_l + l];
+    ls[LS_WC * n.n_l + l] = k.gft * Efp - k.bft * Efq + k.gtf * Etp - k.btf * Etq;
+    ls[LS_WS * n.n_l + l] = k.bft * Efp + k.gft * Efq - k.btf * Etp - k.gtf * Etq;
+    ls[LS_DF * n.n_l + l] = k.gff * Efp - k.bff * Efq;
+    ls[LS_DT * n.n_l + l] = k.gtt * Etp - k.btt * Etq;
+    ls[LS_Y2F * n.n_l + l] = y2f; ls[LS_Y2T * n.n_l + l] = y2t;
+    ls[LS_SGF * n.n_l + l] = sgf; ls[LS_SGT * n.n_l + l] = sgt;
+  }
+}
+
+// w̄^d_i = Σ_{ends at i} d_end + g_sh μ̃^P_i − b_sh μ̃^Q_i (R4 diagonal); stores 2 w̄^d.
+__global__ void k_prep_bus2(DevNet n, Work w, int n_scen) {
+  const long long total = (long long)n_scen * n.n_b;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / n.n_b), i = (int)(t % n.n_b);
+    const double* ls = w.ls + (size_t)s * LS_N * n.n_l;
+    double* bs = w.bs + (size_t)s * BS_N * n.n_b;
+    double wd = __ldg(n.gsh + i) * bs[BS_MUP * n.n_b + i] - __ldg(n.bsh + i) * bs[BS_MUQ * n.n_b + i];
+    for (int e = __ldg(n.inc_ptr + i); e < __ldg(n.inc_ptr + i + 1); ++e) {
+      const int l = __ldg(n.inc_line + e);
+      wd += __ldg(n.lf + l) == i ? ls[LS_DF * n.n_l + l] : ls[LS_DT * n.n_l + l];
+    }
+    bs[BS_WD2 * n.n_b + i] = 2.0 * wd;
+  }
+}
+
+}  // namespace
+
+int launch_eval(const DevNet& n, const Work& w, int n_scen, const double* v, const double* th,
+                const double* p_g, const double* q_g, const double* p_d, const double* q_d,
+                double* G, double* H, double* s_flow, cudaStream_t st) {
+  k_line_eval<<<blocks_for((long long)n_scen * n.n_l), kThreads, 0, st>>>(n, w, n_scen, v, th, H, s_flow);
+  k_bus_eval<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen, v, p_g, q_g, p_d, q_d, G);
+  return 2;
+}
+
+int launch_jacobian(const DevNet& n, const Work& w, int n_scen, const double* v, const double* th,
+                    double* Gx, double* Gu, double* A, int* info, cudaStream_t st) {
+  k_line_state<<<blocks_for((long long)n_scen * n.n_l), kThreads, 0, st>>>(n, w, n_scen, v, th);
+  k_bus_v<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen, v);
+  k_jbus<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen);
+  k_gather<<<blocks_for((long long)n_scen * (n.nnz_gx + n.nnz_gu + n.nnz_a)), kThreads, 0, st>>>(n, w, n_scen, Gx, Gu, A);
+  k_lu<<<n_scen, kLuThreads, 0, st>>>(n, w, info);
+  return 5;
+}
+
+int launch_prep(const DevNet& n, const Work& w, int n_scen, const double* p_d, const double* lam,
+                const double* y, const double* sigma_s, const double* sigma_x, cudaStream_t st) {
+  k_prep_bus1<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen, p_d, lam, y, sigma_s, sigma_x);
+  k_prep_line<<<blocks_for((long long)n_scen * n.n_l), kThreads, 0, st>>>(n, w, n_scen, y, sigma_s);
+  k_prep_bus2<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen);
+  return 3;
+}
+
+}  // namespace pf

@@ -1,0 +1,30 @@
+// pf_launch.h — host launchers of the sm_100a kernels (one per hot-path step).
+#pragma once
+#include "pf_dev.cuh"
+
+namespace pf {
+
+// A2/A3: line kernel (ψ, flows, H) then bus gather (G).  Returns launches.
+int launch_eval(const DevNet& n, const Work& w, int n_scen, const double* v, const double* th,
+                const double* p_g, const double* q_g, const double* p_d, const double* q_d,
+                double* G, double* H, double* s_flow, cudaStream_t st);
+
+// A4/A5: line state, J_bus values, gathers into G_x/G_u/A, numeric LU + transposed values.
+int launch_jacobian(const DevNet& n, const Work& w, int n_scen, const double* v, const double* th,
+                    double* Gx, double* Gu, double* A, int* info, cudaStream_t st);
+
+// A6: per-scenario ψ weights w̄ and bus/line state for the HVP.
+int launch_prep(const DevNet& n, const Work& w, int n_scen, const double* p_d, const double* lam,
+                const double* y, const double* sigma_s, const double* sigma_x, cudaStream_t st);
+
+// A7.1–A7.5 fused: RHS, L/U sweeps, matrix-free K·[V;Z], Uᵀ/Lᵀ sweeps, projection.
+int launch_reduce(const DevNet& n, const Work& w, int C, int n_scen, const double* V, int col0,
+                  int N, double* KV, cudaStream_t st);
+
+// A9: symmetrize + shift, blocked FP64 Cholesky (DMMA trailing update), solves.
+int launch_chol(const DevNet& n, int n_scen, double* K, const double* sigma_u, double delta_w,
+                double* rhs, int nrhs, int* info, int* info_ws, cudaStream_t st);
+
+int pick_tile_cols(int n_x, int n_scen_x_N);
+
+}  // namespace pf
