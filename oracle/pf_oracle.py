@@ -321,13 +321,16 @@ def jacobians(net, part, point):
     n_l = int(net["n_l"])
     JL = line_jacobian(net, part, v, th)
     sf, st = line_flows(net, v, th)
-    Ah_rows = []
-    for (l, e) in part["h_rows"]:
-        s = sf[l] if e == 0 else st[l]
-        rp = l + 2 * n_l * e
-        rq = l + n_l + 2 * n_l * e
-        Ah_rows.append(2.0 * (s.real * JL[rp, :] + s.imag * JL[rq, :]))
-    Ah = sp.vstack(Ah_rows) if Ah_rows else sp.csr_matrix((0, n_u + n_x))
+    # one row per h row (l, e): 2 (s_p ∇s_p + s_q ∇s_q) of that line end
+    hl = np.array([l for (l, e) in part["h_rows"]], dtype=np.int64)
+    he = np.array([e for (l, e) in part["h_rows"]], dtype=np.int64)
+    if len(hl):
+        s_h = np.where(he == 0, sf[hl], st[hl])
+        rp = hl + 2 * n_l * he
+        rq = hl + n_l + 2 * n_l * he
+        Ah = 2.0 * (sp.diags(s_h.real) @ JL[rp, :] + sp.diags(s_h.imag) @ JL[rq, :])
+    else:
+        Ah = sp.csr_matrix((0, n_u + n_x))
     A = sp.vstack([Ar, Ah]).tocsr()
     return Gx.tocsr(), Gu.tocsr(), A
 

@@ -245,7 +245,7 @@ pf_status pf_reduced_hessian_batch(pf_net* h, int32_t n_scen, const double* v, c
                                    int32_t col0, int32_t N, double* KV, void* stream) {
   if (!h) return PF_ERR_ARG;
   (void)v; (void)theta;  // the point's state was cached by pf_jacobian (same v, theta)
-  if (!lambda || !y || !KV || n_scen < 1 || N < 0) { h->err = "pf_reduced_hessian_batch: bad argument"; return PF_ERR_ARG; }
+  if (!lambda || !y || (!KV && N > 0) || n_scen < 1 || N < 0) { h->err = "pf_reduced_hessian_batch: bad argument"; return PF_ERR_ARG; }
   if (n_scen > h->max_scen || N > h->max_batch) { h->err = "pf_reduced_hessian_batch: capacity"; return PF_ERR_CAPACITY; }
   if (!V && (col0 < 0 || col0 + N > h->P.n_u)) { h->err = "pf_reduced_hessian_batch: columns out of range"; return PF_ERR_ARG; }
   if (h->lu_scen < n_scen) { h->err = "pf_reduced_hessian_batch: call pf_jacobian first"; return PF_ERR_STATE; }
