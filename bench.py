@@ -213,6 +213,7 @@ def main():
     tmp.close()
     col0, ncols, cpad = column_partition(n_u, world, rank) if directions else (0, n_u, n_u)
     h = Network(net, max_batch=max(cpad, 1), max_scen=S, device=local)
+    h.profile(True)
     d = h.dims
 
     def stack(key):
@@ -274,6 +275,7 @@ def main():
     # ------------------------------------------------------------ timed loop (device-resident inputs)
     launches0 = h.launch_count()
     step_ms, red_ms, chol_ms = [], [], []
+    kern = {k: [] for k in h.KERNELS}
     with ClockSampler(local) as clk:
         if world > 1:
             dist.barrier()
@@ -289,6 +291,8 @@ def main():
             step_ms.append(e0.elapsed_time(e1))
             red_ms.append(re[0].elapsed_time(re[1]))
             chol_ms.append(ce[0].elapsed_time(ce[1]))
+            for k, v in h.kernel_times().items():
+                kern[k].append(v)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -341,23 +345,37 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ------------------------------------------------------------ roofline of the dominant kernel (k_reduce)
+    # ------------------------------------------------------------ roofline of the dominant kernel
     peaks = read_peaks()
     hbm = peaks.get("hbm_gbs")
-    bytes_per_dir = 8.0 * (12 * n_x + 5 * n_u)      # SURVEY §8(d) fused-streaming bytes per direction
-    dirs_per_launch = S * ncols
-    achieved = bytes_per_dir * dirs_per_launch / (red_avg / 1e3) / 1e9
+    dirs = S * ncols
+    # algorithmic DRAM bytes per direction of each kernel: slab rows
+    # written/read once per pass; factors, network and line state are per-launch
+    # constants (L2-resident) and are not counted.
+    per_dir = {"k_fwd": 8.0 * 5 * n_x,                    # zero-fill + L sweep (r+w) + U sweep (r+w)
+               "k_mu": 8.0 * 2 * n_g,                     # μ_A rows written (Z reads hit L2)
+               "k_hvp": 8.0 * (2 * n_x + n_u),            # Z read, H_x write, H_u write
+               "k_adj": 8.0 * (5 * n_x + 2 * n_u),        # Uᵀ, Lᵀ sweeps (r+w), Ψ read, H_u read, K̂V write
+               "k_lu": None}
+    kstats = {}
+    for k, v in kern.items():
+        if not v:
+            continue
+        ms = statistics.mean(v)
+        ach = per_dir[k] * dirs / (ms / 1e3) / 1e9 if per_dir.get(k) else None
+        kstats[k] = {"ms": ms, "GBps": ach, "frac": (ach / hbm) if (ach and hbm) else None}
+    dom = max((k for k in kstats if k != "k_lu"), key=lambda k: kstats[k]["ms"])
     traffic = None
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        traffic = tj.get(args.config)
+        traffic = tj.get(args.config, {}).get(dom)
     except Exception:
         pass
-    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": (achieved / hbm) if hbm else None, "traffic": traffic,
-            "kernel": "k_reduce (pf_reduced_hessian_batch; events also span its 3 tiny prep kernels)",
-            "algorithmic_bytes_per_direction": bytes_per_dir, "directions_per_launch": dirs_per_launch,
-            "kernel_ms": red_avg, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}
+    roof = {"bound": "hbm", "achieved": kstats[dom]["GBps"], "peak": hbm, "unit": "GB/s",
+            "frac": kstats[dom]["frac"], "traffic": traffic, "kernel": dom,
+            "algorithmic_bytes_per_direction": per_dir[dom], "directions_per_launch": dirs,
+            "kernel_ms": kstats[dom]["ms"], "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
+            "per_kernel": kstats}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:

@@ -202,6 +202,17 @@ pf_status pf_condensed_kkt_solve(pf_net *net, int32_t n_scen, double *K,
 /* Number of kernels this handle has launched so far (bench evidence). */
 int64_t pf_launch_count(const pf_net *net);
 
+/*
+ * Instrumentation (bench / profiling only).  pf_profile(net, 1) makes the
+ * compute calls record CUDA events on their stream around the hot kernels;
+ * pf_kernel_times writes the last calls' per-kernel milliseconds, in the
+ * order k_fwd, k_mu, k_hvp, k_adj (pf_reduced_hessian_batch) and k_lu
+ * (pf_jacobian), synchronizing on the events; returns how many were written
+ * (0 when profiling is off).
+ */
+pf_status pf_profile(pf_net *net, int32_t enable);
+int32_t pf_kernel_times(pf_net *net, float *ms /* [host] cap */, int32_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,6 +22,8 @@ struct pf_net {
   std::vector<void*> allocs;
   std::string err;
   long long launches = 0;
+  bool prof = false;         // instrumentation: events around the hot kernels
+  cudaEvent_t ev[8] = {};    // [0..4] reduction kernels, [5..6] k_lu
 };
 
 static std::string g_build_err;
@@ -122,6 +124,9 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
   std::vector<int> lf(line_from, line_from + n_l), lt(line_to, line_to + n_l), gb(gen_bus, gen_bus + n_g);
   std::vector<int> gbus;
   for (int i = 0; i < n_b; ++i) if (P.bus_gen[i] >= 0) gbus.push_back(i);
+  std::vector<int4> rowmeta(P.n_x);
+  for (int r = 0; r < P.n_x; ++r) rowmeta[r] = make_int4(P.lu_ptr[r], P.lu_diag[r], P.lu_ptr[r + 1], P.row_blk[r]);
+  d.C = h->C;
 
   bool ok = up(h, lf, &d.lf) && up(h, lt, &d.lt) && up(h, coef, &d.coef) && up(h, gsh, &d.gsh) &&
             up(h, bsh, &d.bsh) && up(h, gb, &d.gen_bus) && up(h, P.bus_gen, &d.bus_gen) &&
@@ -140,13 +145,13 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
             up(h, P.levU_blk, &d.levU_blk) && up(h, P.guc_ptr, &d.guc_ptr) && up(h, P.guc_row, &d.guc_row) &&
             up(h, P.guc_src, &d.guc_src) && up(h, P.gur_ptr, &d.gur_ptr) && up(h, P.gur_col, &d.gur_col) &&
             up(h, P.gur_src, &d.gur_src) && up(h, P.bus_pth, &d.bus_pth) && up(h, P.bus_pv, &d.bus_pv) &&
-            up(h, gbus, &d.gbus);
+            up(h, gbus, &d.gbus) && up(h, rowmeta, &d.rowmeta) && up(h, P.hvp_bus, &d.hvp_bus);
   Work& w = h->w;
   const size_t S = max_scen;
   w.max_tiles = max_scen * ((max_batch + h->C - 1) / h->C);
   const size_t T = w.max_tiles, C = h->C;
   ok = ok && alloc(h, S * d.nnz_jb, &w.jb) && alloc(h, S * d.nnz_gu, &w.gu) && alloc(h, S * d.nnz_lu, &w.lu) &&
-       alloc(h, S * d.nnz_lu, &w.luT) && alloc(h, S * d.n_x, &w.rowmax) && alloc(h, S * LS_N * d.n_l, &w.ls) &&
+       alloc(h, S * d.nnz_lu, &w.luT) && alloc(h, S * d.nnz_lu, &w.pkA) && alloc(h, S * d.nnz_lu, &w.pkT) && alloc(h, S * d.n_x, &w.rowmax) && alloc(h, S * LS_N * d.n_l, &w.ls) &&
        alloc(h, S * BS_N * d.n_b, &w.bs) && alloc(h, S * 4 * d.n_l, &w.sflow) && alloc(h, 2 * S, &w.info) &&
        alloc(h, T * d.n_x * C, &w.slabZ) && alloc(h, T * d.n_x * C, &w.slabW) &&
        alloc(h, T * d.n_u * C, &w.hu) && alloc(h, T * d.n_g * 2 * C, &w.mu);
@@ -167,6 +172,7 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
 void pf_destroy(pf_net* h) {
   if (!h) return;
   if (h->device >= 0) cudaSetDevice(h->device);
+  for (auto& e : h->ev) if (e) cudaEventDestroy(e);
   for (void* p : h->allocs) cudaFree(p);
   delete h;
 }
@@ -234,7 +240,8 @@ pf_status pf_jacobian(pf_net* h, int32_t n_scen, const double* v, const double* 
   if (!v || !theta || n_scen < 1) { h->err = "pf_jacobian: bad argument"; return PF_ERR_ARG; }
   if (n_scen > h->max_scen) { h->err = "pf_jacobian: n_scen > max_scen"; return PF_ERR_CAPACITY; }
   if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
-  h->launches += launch_jacobian(h->dn, h->w, n_scen, v, theta, Gx_val, Gu_val, A_val, info, (cudaStream_t)stream);
+  h->launches += launch_jacobian(h->dn, h->w, n_scen, v, theta, Gx_val, Gu_val, A_val, info, (cudaStream_t)stream,
+                                 h->prof ? h->ev + 5 : nullptr);
   h->lu_scen = n_scen;
   return cuda_check(h, "pf_jacobian");
 }
@@ -253,7 +260,7 @@ pf_status pf_reduced_hessian_batch(pf_net* h, int32_t n_scen, const double* v, c
   if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
   cudaStream_t st = (cudaStream_t)stream;
   h->launches += launch_prep(h->dn, h->w, n_scen, p_d, lambda, y, sigma_s, sigma_x, st);
-  h->launches += launch_reduce(h->dn, h->w, h->C, n_scen, V, col0, N, KV, st);
+  h->launches += launch_reduce(h->dn, h->w, h->C, n_scen, V, col0, N, KV, st, h->prof ? h->ev : nullptr);
   return cuda_check(h, "pf_reduced_hessian_batch");
 }
 
@@ -266,6 +273,31 @@ pf_status pf_condensed_kkt_solve(pf_net* h, int32_t n_scen, double* K, const dou
   h->launches += launch_chol(h->dn, n_scen, K, sigma_u, delta_w, rhs, nrhs, info, h->w.info + h->max_scen,
                              (cudaStream_t)stream);
   return cuda_check(h, "pf_condensed_kkt_solve");
+}
+
+pf_status pf_profile(pf_net* h, int32_t enable) {
+  if (!h) return PF_ERR_ARG;
+  if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
+  if (enable && !h->ev[0])
+    for (auto& e : h->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) return cuda_check(h, "pf_profile");
+  h->prof = enable != 0;
+  return PF_OK;
+}
+
+int32_t pf_kernel_times(pf_net* h, float* ms, int32_t cap) {
+  if (!h || !h->prof || !ms) return 0;
+  const int pairs[5][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {5, 6}};
+  int k = 0;
+  for (; k < 5 && k < cap; ++k) {
+    float t = -1.0f;
+    if (cudaEventSynchronize(h->ev[pairs[k][1]]) == cudaSuccess &&
+        cudaEventElapsedTime(&t, h->ev[pairs[k][0]], h->ev[pairs[k][1]]) != cudaSuccess)
+      t = -1.0f;
+    ms[k] = t;
+  }
+  cudaGetLastError();
+  return k;
 }
 
 }  // extern "C"

@@ -40,66 +40,68 @@ __global__ void k_chol_init(int n, int n_scen, double* __restrict__ K, const dou
   }
 }
 
-// Unblocked Cholesky of the diagonal block in SMEM; first failing column → info.
-__global__ void __launch_bounds__(256) k_chol_diag(int n, int k0, double* __restrict__ K, int* __restrict__ info) {
-  const int s = blockIdx.x;
+// Panel step of the right-looking factorization, one launch per 64-column
+// panel: every CTA factors the 64×64 diagonal block in SMEM (unblocked, 256
+// threads; CTA 0 writes L_kk back and reports the first failing column in
+// info), then solves its 64-row block of the panel, X L_kkᵀ = A (4 lanes per
+// row, shuffle-reduced dot products).
+__global__ void __launch_bounds__(256) k_chol_panel(int n, int k0, double* __restrict__ K, int* __restrict__ info) {
+  const int s = blockIdx.y;
   if (info[s] != 0) return;
-  __shared__ double a[NB][NB + 1];
+  extern __shared__ double smem_panel[];
+  double (*L)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(smem_panel);
+  double (*X)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(smem_panel + NB * (NB + 1));
   __shared__ int fail;
   double* A = K + (size_t)s * n * n;
   const int nb = min(NB, n - k0);
   for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
     const int c = idx / nb, r = idx % nb;
-    a[r][c] = r >= c ? A[(size_t)(k0 + c) * n + k0 + r] : 0.0;
+    L[r][c] = r >= c ? A[(size_t)(k0 + c) * n + k0 + r] : 0.0;
   }
   if (threadIdx.x == 0) fail = 0;
   __syncthreads();
   for (int jj = 0; jj < nb; ++jj) {
     if (threadIdx.x == 0) {
-      const double d = a[jj][jj];
+      const double d = L[jj][jj];
       if (!(d > 0.0) || !isfinite(d)) fail = k0 + jj + 1;
-      else a[jj][jj] = sqrt(d);
+      else L[jj][jj] = sqrt(d);
     }
     __syncthreads();
     if (fail) break;
-    const double piv = a[jj][jj];
-    for (int r = jj + 1 + threadIdx.x; r < nb; r += blockDim.x) a[r][jj] /= piv;
+    const double piv = L[jj][jj];
+    for (int r = jj + 1 + threadIdx.x; r < nb; r += blockDim.x) L[r][jj] /= piv;
     __syncthreads();
     const int m = nb - jj - 1;
     for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
       const int r = jj + 1 + idx / m, c = jj + 1 + idx % m;
-      if (c <= r) a[r][c] -= a[r][jj] * a[c][jj];
+      if (c <= r) L[r][c] -= L[r][jj] * L[c][jj];
     }
     __syncthreads();
   }
-  if (fail) { if (threadIdx.x == 0) info[s] = fail; return; }
-  for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
-    const int c = idx / nb, r = idx % nb;
-    if (r >= c) A[(size_t)(k0 + c) * n + k0 + r] = a[r][c];
+  if (fail) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) info[s] = fail;
+    return;
   }
-}
-
-// Panel: X L_kkᵀ = A[i-block, k-block] (one thread per row, DFMA, rows in SMEM).
-__global__ void __launch_bounds__(NB) k_chol_trsm(int n, int k0, double* __restrict__ K, const int* __restrict__ info) {
-  const int s = blockIdx.y;
-  if (info[s] != 0) return;
-  extern __shared__ double smem_trsm[];
-  double (*L)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(smem_trsm);
-  double (*X)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(smem_trsm + NB * (NB + 1));
-  double* A = K + (size_t)s * n * n;
-  const int nb = min(NB, n - k0);
+  if (blockIdx.x == 0)
+    for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
+      const int c = idx / nb, r = idx % nb;
+      if (r >= c) A[(size_t)(k0 + c) * n + k0 + r] = L[r][c];
+    }
   const int i0 = k0 + nb + blockIdx.x * NB;
+  if (i0 >= n) return;
   for (int idx = threadIdx.x; idx < nb * NB; idx += blockDim.x) {
     const int c = idx / NB, r = idx % NB;
-    if (r < nb) L[r][c] = r >= c ? A[(size_t)(k0 + c) * n + k0 + r] : 0.0;
     X[r][c] = (i0 + r < n) ? A[(size_t)(k0 + c) * n + i0 + r] : 0.0;
   }
   __syncthreads();
-  const int r = threadIdx.x;
+  const int r = threadIdx.x >> 2, q = threadIdx.x & 3;
   for (int c = 0; c < nb; ++c) {
-    double acc = X[r][c];
-    for (int m = 0; m < c; ++m) acc -= X[r][m] * L[c][m];
-    X[r][c] = acc / L[c][c];
+    double part = 0.0;
+    for (int mm = q; mm < c; mm += 4) part += X[r][mm] * L[c][mm];
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    if (q == 0) X[r][c] = (X[r][c] - part) / L[c][c];
+    __syncwarp();
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < nb * NB; idx += blockDim.x) {
@@ -171,26 +173,37 @@ __global__ void __launch_bounds__(128) k_chol_syrk(int n, int k0, double* __rest
 }
 
 // L Lᵀ p = b for one (scenario, right-hand side): blocked forward / backward
-// substitution, b staged in SMEM, off-diagonal updates as coalesced column sweeps.
+// substitution; b and each 64×64 diagonal block staged in SMEM, the
+// off-diagonal updates as coalesced column sweeps over L.
 __global__ void __launch_bounds__(256) k_chol_solve(int n, const double* __restrict__ K, double* __restrict__ rhs,
                                                     int nrhs, const int* __restrict__ info) {
-  extern __shared__ double b[];
+  extern __shared__ double sm_solve[];
+  double (*D)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(sm_solve);
+  double* b = sm_solve + NB * (NB + 1);
   const int s = blockIdx.y, rr = blockIdx.x;
   if (info[s] != 0) return;
   const double* L = K + (size_t)s * n * n;
   double* bg = rhs + ((size_t)s * nrhs + rr) * n;
   for (int i = threadIdx.x; i < n; i += blockDim.x) b[i] = bg[i];
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  auto stage = [&](int j0, int nb) {
+    for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
+      const int c = idx / nb, r = idx % nb;
+      D[r][c] = r >= c ? L[(size_t)(j0 + c) * n + j0 + r] : 0.0;
+    }
+  };
+  __syncthreads();
   // forward: L y = b
   for (int j0 = 0; j0 < n; j0 += NB) {
-    const int j1 = min(n, j0 + NB);
+    const int j1 = min(n, j0 + NB), nb = j1 - j0;
+    stage(j0, nb);
+    __syncthreads();
     if (warp == 0) {
-      for (int j = j0; j < j1; ++j) {
-        const double yj = b[j] / L[(size_t)j * n + j];
+      for (int j = 0; j < nb; ++j) {
+        const double yj = b[j0 + j] / D[j][j];
         __syncwarp();
-        if (lane == 0) b[j] = yj;
-        for (int i = j + 1 + lane; i < j1; i += 32) b[i] -= L[(size_t)j * n + i] * yj;
+        if (lane == 0) b[j0 + j] = yj;
+        for (int i = j + 1 + lane; i < nb; i += 32) b[j0 + i] -= D[i][j] * yj;
         __syncwarp();
       }
     }
@@ -205,7 +218,7 @@ __global__ void __launch_bounds__(256) k_chol_solve(int n, const double* __restr
   // backward: Lᵀ p = y
   const int nblk = (n + NB - 1) / NB;
   for (int bk = nblk - 1; bk >= 0; --bk) {
-    const int j0 = bk * NB, j1 = min(n, j0 + NB);
+    const int j0 = bk * NB, j1 = min(n, j0 + NB), nb = j1 - j0;
     for (int j = j0 + warp; j < j1; j += nwarp) {
       double acc = 0.0;
       for (int i = j1 + lane; i < n; i += 32) acc += L[(size_t)j * n + i] * b[i];
@@ -213,14 +226,15 @@ __global__ void __launch_bounds__(256) k_chol_solve(int n, const double* __restr
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0) b[j] -= acc;
     }
+    stage(j0, nb);
     __syncthreads();
     if (warp == 0) {
-      for (int j = j1 - 1; j >= j0; --j) {
+      for (int j = nb - 1; j >= 0; --j) {
         double acc = 0.0;
-        for (int i = j + 1 + lane; i < j1; i += 32) acc += L[(size_t)j * n + i] * b[i];
+        for (int i = j + 1 + lane; i < nb; i += 32) acc += D[i][j] * b[j0 + i];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) b[j] = (b[j] - acc) / L[(size_t)j * n + j];
+        if (lane == 0) b[j0 + j] = (b[j0 + j] - acc) / D[j][j];
         __syncwarp();
       }
     }
@@ -242,7 +256,7 @@ int launch_chol(const DevNet& net, int n_scen, double* K, const double* sigma_u,
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_chol_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, kSyrkSmem);
-    cudaFuncSetAttribute(k_chol_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem);
+    cudaFuncSetAttribute(k_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem);
     attr = true;
   }
   long long tot = (long long)n_scen * n * n;
@@ -251,20 +265,19 @@ int launch_chol(const DevNet& net, int n_scen, double* K, const double* sigma_u,
   ++launches;
   for (int k0 = 0; k0 < n; k0 += NB) {
     const int nb = std::min(NB, n - k0);
-    k_chol_diag<<<n_scen, 256, 0, st>>>(n, k0, K, info_ws);
-    ++launches;
     const int rest = n - k0 - nb;
+    const int T = (rest + NB - 1) / NB;
+    k_chol_panel<<<dim3(std::max(T, 1), n_scen), 256, kTrsmSmem, st>>>(n, k0, K, info_ws);
+    ++launches;
     if (rest > 0) {
-      const int T = (rest + NB - 1) / NB;
-      k_chol_trsm<<<dim3(T, n_scen), NB, kTrsmSmem, st>>>(n, k0, K, info_ws);
       k_chol_syrk<<<dim3(T * (T + 1) / 2, n_scen), 128, kSyrkSmem, st>>>(n, k0, K, info_ws);
-      launches += 2;
+      ++launches;
     }
   }
   if (nrhs > 0) {
-    const size_t smem = (size_t)n * sizeof(double);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_chol_solve<<<dim3(nrhs, n_scen), 256, (size_t)n * sizeof(double), st>>>(n, K, rhs, nrhs, info_ws);
+    const size_t smem = (size_t)(n + NB * (NB + 1)) * sizeof(double);
+    cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_chol_solve<<<dim3(nrhs, n_scen), 256, smem, st>>>(n, K, rhs, nrhs, info_ws);
     ++launches;
   }
   if (info) { k_info_out<<<1, 256, 0, st>>>(n_scen, info_ws, info); ++launches; }

@@ -25,6 +25,9 @@ struct DevNet {
   const int *guc_ptr, *guc_row, *guc_src, *gur_ptr, *gur_col, *gur_src;
   const int *bus_pth, *bus_pv;
   const int *gbus;              // [n_gb] generator buses ascending (the r buses)
+  const int4 *rowmeta;          // [n_x] {lu_ptr[r], lu_diag[r], lu_ptr[r+1], block of r}
+  const int *hvp_bus;           // [n_b] buses in elimination order, the reference bus last
+  int C;                        // directions per tile (slab row width)
 };
 
 // Per-scenario point state, SoA.  Line state (LS_*) and bus state (BS_*).
@@ -37,6 +40,8 @@ struct Work {
   double* gu;      // [max_scen][nnz_gu]  G_u values (internal copy)
   double* lu;      // [max_scen][nnz_lu]  LU values (row-wise)
   double* luT;     // [max_scen][nnz_lu]  transposed values: luT[e] = lu[tpos[e]]
+  double2* pkA;    // [max_scen][nnz_lu]  packed {lu[e], bits(idx[e]*C)} for the L / U sweeps
+  double2* pkT;    // [max_scen][nnz_lu]  packed {luT[e], bits(idx[e]*C)} for the Uᵀ / Lᵀ sweeps
   double* rowmax;  // [max_scen][n_x]     pivot threshold scale (R18)
   double* ls;      // [max_scen][LS_N][n_l]
   double* bs;      // [max_scen][BS_N][n_b]

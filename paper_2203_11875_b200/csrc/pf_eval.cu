@@ -6,7 +6,11 @@
 // R5 ψ orientation Δ = θ_f − θ_t, R8 implicit p_ref, R18 static pivots.
 #include "pf_launch.h"
 
+#include <algorithm>
 #include <climits>
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
 
 namespace pf {
 
@@ -234,59 +238,84 @@ __global__ void k_gather(DevNet n, Work w, int n_scen, double* __restrict__ Gx,
 
 // ---------------------------------------------------------------- A5
 // Numeric LU of P G_x Pᵀ with the fixed symbolic pattern and static pivots
-// (R18): up-looking IKJ rows, one warp per bus block, blocks of one level in
-// parallel, __syncthreads between levels.  One CTA per scenario.
-constexpr int kLuThreads = 512;
+// (R18): up-looking IKJ rows, one warp per bus block, the blocks of one level
+// spread over all warps of the scenario's CTA group; a grid-wide barrier
+// (cooperative launch, all CTAs co-resident) separates levels.  Values
+// written by other SMs are read with ld.global.cg (L2), never a stale L1 line.
+constexpr int kLuThreads = 256;
 
-__global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int* __restrict__ info_out) {
-  const int s = blockIdx.x;
-  double* lu = w.lu + (size_t)s * n.nnz_lu;
-  double* luT = w.luT + (size_t)s * n.nnz_lu;
-  double* rowmax = w.rowmax + (size_t)s * n.n_x;
-  const double* jb = w.jb + (size_t)s * n.nnz_jb;
-  __shared__ int s_info;
-  if (threadIdx.x == 0) s_info = INT_MAX;
-  for (int r = threadIdx.x; r < n.n_x; r += blockDim.x) {
-    double mx = 0.0;
-    for (int e = __ldg(n.lu_ptr + r); e < __ldg(n.lu_ptr + r + 1); ++e) {
-      const int src = __ldg(n.lu_src + e);
-      const double val = src >= 0 ? jb[src] : 0.0;
-      lu[e] = val;
-      mx = fmax(mx, fabs(val));
-    }
-    rowmax[r] = mx;
-  }
-  __syncthreads();
+__global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int n_scen, int P, int* __restrict__ info_out) {
+  cg::grid_group grid = cg::this_grid();
+  const int s = blockIdx.x / P, sub = blockIdx.x % P;
+  const bool active = s < n_scen;
+  double* lu = w.lu + (size_t)(active ? s : 0) * n.nnz_lu;
+  double* rowmax = w.rowmax + (size_t)(active ? s : 0) * n.n_x;
+  const double* jb = w.jb + (size_t)(active ? s : 0) * n.nnz_jb;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int gthread = sub * blockDim.x + threadIdx.x, nthread = P * blockDim.x;
+  const int gwarp = sub * nwarp + warp, ngwarp = P * nwarp;
+  if (active) {
+    if (gthread == 0) w.info[s] = INT_MAX;
+    for (int r = gthread; r < n.n_x; r += nthread) {
+      double mx = 0.0;
+      for (int e = __ldg(n.lu_ptr + r); e < __ldg(n.lu_ptr + r + 1); ++e) {
+        const int src = __ldg(n.lu_src + e);
+        const double val = src >= 0 ? jb[src] : 0.0;
+        __stcg(lu + e, val);
+        mx = fmax(mx, fabs(val));
+      }
+      rowmax[r] = mx;
+    }
+  }
+  grid.sync();
   for (int lev = 0; lev < n.nlevL; ++lev) {
-    const int b0 = __ldg(n.levL_ptr + lev), b1 = __ldg(n.levL_ptr + lev + 1);
-    for (int bi = b0 + warp; bi < b1; bi += nwarp) {
-      const int p = __ldg(n.levL_blk + bi);
-      for (int r = __ldg(n.blk_ptr + p); r < __ldg(n.blk_ptr + p + 1); ++r) {
-        const int dr = __ldg(n.lu_diag + r);
-        for (int e = __ldg(n.lu_ptr + r); e < dr; ++e) {
-          const int k = __ldg(n.lu_idx + e);
-          const double l = lu[e] / lu[__ldg(n.lu_diag + k)];
-          __syncwarp();
-          if (lane == 0) lu[e] = l;
-          const int u0 = __ldg(n.lu_diag + k) + 1;
-          const int q0 = __ldg(n.upd_ptr + e), cnt = __ldg(n.upd_ptr + e + 1) - q0;
-          for (int t = lane; t < cnt; t += 32) lu[__ldg(n.upd_dst + q0 + t)] -= l * lu[u0 + t];
+    if (active) {
+      const int b0 = __ldg(n.levL_ptr + lev), b1 = __ldg(n.levL_ptr + lev + 1);
+      for (int bi = b0 + gwarp; bi < b1; bi += ngwarp) {
+        const int p = __ldg(n.levL_blk + bi);
+        for (int r = __ldg(n.blk_ptr + p); r < __ldg(n.blk_ptr + p + 1); ++r) {
+          const int dr = __ldg(n.lu_diag + r);
+          for (int e = __ldg(n.lu_ptr + r); e < dr; ++e) {
+            const int k = __ldg(n.lu_idx + e);
+            const double l = __ldcg(lu + e) / __ldcg(lu + __ldg(n.lu_diag + k));
+            __syncwarp();
+            if (lane == 0) __stcg(lu + e, l);
+            const int u0 = __ldg(n.lu_diag + k) + 1;
+            const int q0 = __ldg(n.upd_ptr + e), cnt = __ldg(n.upd_ptr + e + 1) - q0;
+            for (int t = lane; t < cnt; t += 32) {
+              double* dst = lu + __ldg(n.upd_dst + q0 + t);
+              __stcg(dst, __ldcg(dst) - l * __ldcg(lu + u0 + t));
+            }
+            __syncwarp();
+          }
+          if (lane == 0) {
+            const double d = __ldcg(lu + dr);
+            if (!(fabs(d) >= 1e-12 * rowmax[r]) || !isfinite(d) || d == 0.0) atomicMin(w.info + s, r + 1);
+          }
           __syncwarp();
         }
-        if (lane == 0) {
-          const double d = lu[dr];
-          if (!(fabs(d) >= 1e-12 * rowmax[r]) || !isfinite(d) || d == 0.0) atomicMin(&s_info, r + 1);
-        }
-        __syncwarp();
       }
     }
-    __syncthreads();
+    grid.sync();
   }
-  for (int e = threadIdx.x; e < n.nnz_lu; e += blockDim.x) luT[e] = lu[__ldg(n.lu_tpos + e)];
-  if (threadIdx.x == 0) {
-    const int v = s_info == INT_MAX ? 0 : s_info;
-    w.info[s] = v;
+  if (active) {
+    double* luT = w.luT + (size_t)s * n.nnz_lu;
+    double2* pkA = w.pkA + (size_t)s * n.nnz_lu;
+    double2* pkT = w.pkT + (size_t)s * n.nnz_lu;
+    for (int e = gthread; e < n.nnz_lu; e += nthread) {
+      const double t = __ldcg(lu + __ldg(n.lu_tpos + e));
+      const double c = __longlong_as_double((long long)__ldg(n.lu_idx + e) * n.C);
+      luT[e] = t;
+      pkA[e] = make_double2(__ldcg(lu + e), c);
+      pkT[e] = make_double2(t, c);
+    }
+  }
+}
+
+__global__ void k_lu_info(int n_scen, int* __restrict__ info, int* __restrict__ info_out) {
+  for (int s = threadIdx.x; s < n_scen; s += blockDim.x) {
+    const int v = info[s] == INT_MAX ? 0 : info[s];
+    info[s] = v;
     if (info_out) info_out[s] = v;
   }
 }
@@ -393,13 +422,28 @@ int launch_eval(const DevNet& n, const Work& w, int n_scen, const double* v, con
 }
 
 int launch_jacobian(const DevNet& n, const Work& w, int n_scen, const double* v, const double* th,
-                    double* Gx, double* Gu, double* A, int* info, cudaStream_t st) {
+                    double* Gx, double* Gu, double* A, int* info, cudaStream_t st, cudaEvent_t* ev) {
   k_line_state<<<blocks_for((long long)n_scen * n.n_l), kThreads, 0, st>>>(n, w, n_scen, v, th);
   k_bus_v<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen, v);
   k_jbus<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen);
   k_gather<<<blocks_for((long long)n_scen * (n.nnz_gx + n.nnz_gu + n.nnz_a)), kThreads, 0, st>>>(n, w, n_scen, Gx, Gu, A);
-  k_lu<<<n_scen, kLuThreads, 0, st>>>(n, w, info);
-  return 5;
+  static int lu_grid = 0;
+  if (lu_grid == 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lu, kLuThreads, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    lu_grid = std::max(1, per_sm) * sms;
+  }
+  int P = std::max(1, lu_grid / n_scen);
+  int grid = P * n_scen;
+  if (grid > lu_grid) { P = 1; grid = n_scen; }  // more scenarios than co-resident CTAs: not supported cooperatively
+  void* args[] = {(void*)&n, (void*)&w, (void*)&n_scen, (void*)&P, (void*)&info};
+  if (ev) cudaEventRecord(ev[0], st);
+  cudaLaunchCooperativeKernel((void*)k_lu, dim3(grid), dim3(kLuThreads), args, 0, st);
+  if (ev) cudaEventRecord(ev[1], st);
+  k_lu_info<<<1, 256, 0, st>>>(n_scen, w.info, info);
+  return 6;
 }
 
 int launch_prep(const DevNet& n, const Work& w, int n_scen, const double* p_d, const double* lam,

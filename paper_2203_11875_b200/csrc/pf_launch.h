@@ -11,7 +11,8 @@ int launch_eval(const DevNet& n, const Work& w, int n_scen, const double* v, con
 
 // A4/A5: line state, J_bus values, gathers into G_x/G_u/A, numeric LU + transposed values.
 int launch_jacobian(const DevNet& n, const Work& w, int n_scen, const double* v, const double* th,
-                    double* Gx, double* Gu, double* A, int* info, cudaStream_t st);
+                    double* Gx, double* Gu, double* A, int* info, cudaStream_t st,
+                    cudaEvent_t* ev = nullptr /* optional: [2] around k_lu */);
 
 // A6: per-scenario ψ weights w̄ and bus/line state for the HVP.
 int launch_prep(const DevNet& n, const Work& w, int n_scen, const double* p_d, const double* lam,
@@ -19,7 +20,8 @@ int launch_prep(const DevNet& n, const Work& w, int n_scen, const double* p_d, c
 
 // A7.1–A7.5 fused: RHS, L/U sweeps, matrix-free K·[V;Z], Uᵀ/Lᵀ sweeps, projection.
 int launch_reduce(const DevNet& n, const Work& w, int C, int n_scen, const double* V, int col0,
-                  int N, double* KV, cudaStream_t st);
+                  int N, double* KV, cudaStream_t st,
+                  cudaEvent_t* ev = nullptr /* optional: [5] around k_fwd, k_mu, k_hvp, k_adj */);
 
 // A9: symmetrize + shift, blocked FP64 Cholesky (DMMA trailing update), solves.
 int launch_chol(const DevNet& n, int n_scen, double* K, const double* sigma_u, double delta_w,

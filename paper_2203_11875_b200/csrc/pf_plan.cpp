@@ -311,6 +311,8 @@ std::string build_plan(int n_b, int n_l, int n_g, const int32_t* lf, const int32
         P.guc_row[fill[c]] = r; P.guc_src[fill[c]] = P.gur_src[e]; fill[c]++;
       }
   }
+  P.hvp_bus = P.bus_order;
+  P.hvp_bus.push_back(ref_bus);
   P.bus_pth.assign(n_b, -1); P.bus_pv.assign(n_b, -1);
   for (int i = 0; i < n_b; ++i) {
     if (P.x_th[i] >= 0) P.bus_pth[i] = P.iperm[P.x_th[i]];

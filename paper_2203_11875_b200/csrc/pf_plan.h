@@ -47,6 +47,7 @@ struct Plan {
 
   // bus -> permuted slab rows
   std::vector<int> bus_pth, bus_pv;
+  std::vector<int> hvp_bus;   // elimination order, reference bus last
 };
 
 // Returns "" on success, else an error message; *topology is set when the

@@ -1,107 +1,145 @@
-// pf_reduce.cu — the batched reduced-Hessian kernel (A7.1–A7.5 of SURVEY §8(a)).
+// pf_reduce.cu — the batched reduced-Hessian kernels (A7.1–A7.5 of SURVEY §8(a)).
 //
-// One CTA owns a tile of C Hessian-vector directions of one scenario and runs
-// the paper's three steps (with R11) end to end, without
-// leaving the kernel:
-//   a. B = −P G_u V            (unit V: a column scatter; dense V: a row SpMM)
-//   b. Z̃ = U^{-1} L^{-1} B     (level-scheduled sweeps, bus blocks of 1–2 rows)
-//   c. [H_u; H_x] = K [V; Z]   (matrix-free through ψ: line-local J_ψ, L_line,
-//                              ∇²ψ with w̄, plus the r-row / p_ref terms,
-//                              AᵀΣ_sA, Σ_x; deterministic bus gathers)
-//   d. Ψ̃ = L^{-T} U^{-T} H̃_x  (transposed sweeps on the same level sets)
-//   e. K̂V = H_u − (P G_u)ᵀ Ψ̃  (column gathers, transposed through SMEM so the
-//                              [N][n_u] output is written coalesced)
-// Slabs are [n_x][C] (direction fastest): a team of C lanes handles one row,
-// lane j = direction j, so every slab access is one contiguous C×8-byte run.
-// Columns are independent: each column's arithmetic is the same for any N,
-// any tile, any GPU count (bit-identical K̂ across batch sizes).
+// The paper's three steps for K̂V (with R11) over tiles of C
+// directions of one scenario:
+//   k_fwd  a. B = −P G_u V       (unit V: a column scatter; dense V: a row SpMM)
+//          b. Z̃ = U^{-1} L^{-1} B (level-scheduled sweeps over bus blocks)
+//   k_mu   c1. μ_A = Σ_r ⊙ R_r M dψ at the r buses (generator buses)
+//   k_hvp  c2. [H_u; H_x] = K [V; Z] matrix-free through ψ (line-local J_ψ,
+//              L_line, ∇²ψ with w̄, the r-row / p_ref terms, AᵀΣ_sA, Σ_x),
+//              one team per bus gathering its incident lines (no atomics)
+//   k_adj  d. Ψ̃ = L^{-T} U^{-T} H̃_x  (transposed sweeps, same level sets)
+//          e. K̂V = H_u − (P G_u)ᵀ Ψ̃  (column gathers, SMEM-transposed store)
+// Slabs are [n_x][C] per tile, direction fastest: a team of C lanes handles
+// one row, lane j = direction j, so every slab access is one contiguous C×8 B
+// run.  Sweep nonzeros are packed {value, column·C} (one 16-byte load each)
+// and summed with four independent accumulators for memory-level parallelism.
+// Every column's arithmetic is independent of N, the tile and the GPU count,
+// so K̂ is bit-identical across batch sizes.
 #include "pf_launch.h"
 
 namespace pf {
 
 namespace {
 
-constexpr int kRedThreads = 256;
-constexpr int kCH = 64;  // u-columns per transposed output chunk
+constexpr int kThreads = 256;
+constexpr int kCH = 64;        // u-columns per transposed output chunk
+constexpr int kBusPerCta = 64; // buses per k_hvp CTA
 
+__device__ __forceinline__ double2 ldpk(const double2* p) { return __ldg(p); }
+__device__ __forceinline__ long long col_of(double2 q) { return __double_as_longlong(q.y); }
+
+// One row of a triangular sweep: acc = X[r] − Σ_{e∈[s,t)} v_e X[c_e], optionally
+// divided by the pivot.  Four independent accumulators keep ≥4 slab loads in flight.
 template <int C>
-__device__ __forceinline__ void sweep_L(const DevNet& n, const double* __restrict__ lu, double* X, int lane, int team, int nteam) {
-  for (int lev = 0; lev < n.nlevL; ++lev) {
-    const int b1 = __ldg(n.levL_ptr + lev + 1);
-    for (int bi = __ldg(n.levL_ptr + lev) + team; bi < b1; bi += nteam) {
-      const int p = __ldg(n.levL_blk + bi);
-      const int r1 = __ldg(n.blk_ptr + p + 1);
-      for (int r = __ldg(n.blk_ptr + p); r < r1; ++r) {
-        double acc = X[r * C + lane];
-        const int e1 = __ldg(n.lu_diag + r);
-        for (int e = __ldg(n.lu_ptr + r); e < e1; ++e) acc -= __ldg(lu + e) * X[__ldg(n.lu_idx + e) * C + lane];
-        X[r * C + lane] = acc;
+__device__ __forceinline__ void sweep_row(const double2* __restrict__ pk, double* X, int r, int s, int t,
+                                          bool divide, int d, int lane) {
+  double a0 = X[r * C + lane], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (; s + 3 < t; s += 4) {
+    const double2 p0 = ldpk(pk + s), p1 = ldpk(pk + s + 1), p2 = ldpk(pk + s + 2), p3 = ldpk(pk + s + 3);
+    a0 -= p0.x * X[col_of(p0) + lane];
+    a1 -= p1.x * X[col_of(p1) + lane];
+    a2 -= p2.x * X[col_of(p2) + lane];
+    a3 -= p3.x * X[col_of(p3) + lane];
+  }
+  for (; s < t; ++s) {
+    const double2 p = ldpk(pk + s);
+    a0 -= p.x * X[col_of(p) + lane];
+  }
+  double acc = (a0 + a1) + (a2 + a3);
+  if (divide) acc /= ldpk(pk + d).x;
+  X[r * C + lane] = acc;
+}
+
+// LOWER: use row r's strict-lower part [ptr, diag) and walk the block's rows
+// forward (L, Uᵀ); otherwise the strict-upper part (diag, end), rows backward (U, Lᵀ).
+template <int C, bool LOWER>
+__device__ __forceinline__ void sweep(const DevNet& n, const double2* __restrict__ pk, double* X, bool divide,
+                                      int lane, int team, int nteam) {
+  const int nlev = LOWER ? n.nlevL : n.nlevU;
+  const int* lptr = LOWER ? n.levL_ptr : n.levU_ptr;
+  const int* lblk = LOWER ? n.levL_blk : n.levU_blk;
+  for (int lev = 0; lev < nlev; ++lev) {
+    const int b1 = __ldg(lptr + lev + 1);
+    for (int bi = __ldg(lptr + lev) + team; bi < b1; bi += nteam) {
+      const int p = __ldg(lblk + bi);
+      const int r0 = __ldg(n.blk_ptr + p), r1 = __ldg(n.blk_ptr + p + 1);
+      if (LOWER) {
+        for (int r = r0; r < r1; ++r) {
+          const int4 m = __ldg(n.rowmeta + r);
+          sweep_row<C>(pk, X, r, m.x, m.y, divide, m.y, lane);
+        }
+      } else {
+        for (int r = r1 - 1; r >= r0; --r) {
+          const int4 m = __ldg(n.rowmeta + r);
+          sweep_row<C>(pk, X, r, m.y + 1, m.z, divide, m.y, lane);
+        }
       }
     }
     __syncthreads();
   }
 }
 
+// ---------------------------------------------------------------- a, b
 template <int C>
-__device__ __forceinline__ void sweep_U(const DevNet& n, const double* __restrict__ lu, double* X, int lane, int team, int nteam) {
-  for (int lev = 0; lev < n.nlevU; ++lev) {
-    const int b1 = __ldg(n.levU_ptr + lev + 1);
-    for (int bi = __ldg(n.levU_ptr + lev) + team; bi < b1; bi += nteam) {
-      const int p = __ldg(n.levU_blk + bi);
-      const int r0 = __ldg(n.blk_ptr + p);
-      for (int r = __ldg(n.blk_ptr + p + 1) - 1; r >= r0; --r) {
-        double acc = X[r * C + lane];
-        const int d = __ldg(n.lu_diag + r), e1 = __ldg(n.lu_ptr + r + 1);
-        for (int e = d + 1; e < e1; ++e) acc -= __ldg(lu + e) * X[__ldg(n.lu_idx + e) * C + lane];
-        X[r * C + lane] = acc / __ldg(lu + d);
-      }
-    }
+__global__ void __launch_bounds__(kThreads, 4) k_fwd(DevNet n, Work w, const double* __restrict__ V, int col0, int N) {
+  const int ntile = (N + C - 1) / C;
+  const int tile = blockIdx.x, s = blockIdx.y;
+  const size_t cta = (size_t)s * ntile + tile;
+  const int lane = threadIdx.x % C, team = threadIdx.x / C, nteam = blockDim.x / C;
+  const int j = tile * C + lane;
+  const bool valid = j < N;
+  const int n_x = n.n_x, n_u = n.n_u;
+  double* X = w.slabZ + cta * n_x * C;
+  const double* gu = w.gu + (size_t)s * n.nnz_gu;
+  const double2* pk = w.pkA + (size_t)s * n.nnz_lu;
+  if (V == nullptr) {  // A7.1 for unit directions: a scatter of G_u's column col0 + j
+    for (int idx = threadIdx.x; idx < n_x * C; idx += blockDim.x) X[idx] = 0.0;
     __syncthreads();
+    if (team == 0 && valid) {
+      const int c = col0 + j;
+      for (int e = __ldg(n.guc_ptr + c); e < __ldg(n.guc_ptr + c + 1); ++e)
+        X[__ldg(n.guc_row + e) * C + lane] = -gu[__ldg(n.guc_src + e)];
+    }
+  } else {             // A7.1 for dense directions: B = −P G_u V (row SpMM)
+    const double* Vs = V + ((size_t)s * N + (valid ? j : 0)) * n_u;
+    for (int r = team; r < n_x; r += nteam) {
+      double acc = 0.0;
+      if (valid)
+        for (int e = __ldg(n.gur_ptr + r); e < __ldg(n.gur_ptr + r + 1); ++e)
+          acc += gu[__ldg(n.gur_src + e)] * Vs[__ldg(n.gur_col + e)];
+      X[r * C + lane] = -acc;
+    }
   }
+  __syncthreads();
+  sweep<C, true>(n, pk, X, false, lane, team, nteam);   // L^{-1}
+  sweep<C, false>(n, pk, X, true, lane, team, nteam);   // U^{-1}
 }
 
-// Uᵀ z = h (forward, L level sets): z_r = (h_r − Σ_{k<r} u_kr z_k) / u_rr,
-// the u_kr read through the transposed copy luT at row r's L positions.
-template <int C>
-__device__ __forceinline__ void sweep_UT(const DevNet& n, const double* __restrict__ lu, const double* __restrict__ luT,
-                                         double* X, int lane, int team, int nteam) {
-  for (int lev = 0; lev < n.nlevL; ++lev) {
-    const int b1 = __ldg(n.levL_ptr + lev + 1);
-    for (int bi = __ldg(n.levL_ptr + lev) + team; bi < b1; bi += nteam) {
-      const int p = __ldg(n.levL_blk + bi);
-      const int r1 = __ldg(n.blk_ptr + p + 1);
-      for (int r = __ldg(n.blk_ptr + p); r < r1; ++r) {
-        double acc = X[r * C + lane];
-        const int d = __ldg(n.lu_diag + r);
-        for (int e = __ldg(n.lu_ptr + r); e < d; ++e) acc -= __ldg(luT + e) * X[__ldg(n.lu_idx + e) * C + lane];
-        X[r * C + lane] = acc / __ldg(lu + d);
-      }
-    }
-    __syncthreads();
+// ---------------------------------------------------------------- directions in bus space
+struct Dir {
+  const double* X;
+  const double* Vs;
+  int lane, col;  // col = col0 + j for unit directions
+  bool valid;
+  __device__ __forceinline__ double vdir(int c) const {
+    if (!valid) return 0.0;
+    return Vs ? Vs[c] : (c == col ? 1.0 : 0.0);
   }
-}
+};
 
-// Lᵀ w = z (backward, U level sets): w_r = z_r − Σ_{j>r} l_jr w_j.
 template <int C>
-__device__ __forceinline__ void sweep_LT(const DevNet& n, const double* __restrict__ luT, double* X, int lane, int team, int nteam) {
-  for (int lev = 0; lev < n.nlevU; ++lev) {
-    const int b1 = __ldg(n.levU_ptr + lev + 1);
-    for (int bi = __ldg(n.levU_ptr + lev) + team; bi < b1; bi += nteam) {
-      const int p = __ldg(n.levU_blk + bi);
-      const int r0 = __ldg(n.blk_ptr + p);
-      for (int r = __ldg(n.blk_ptr + p + 1) - 1; r >= r0; --r) {
-        double acc = X[r * C + lane];
-        const int e1 = __ldg(n.lu_ptr + r + 1);
-        for (int e = __ldg(n.lu_diag + r) + 1; e < e1; ++e) acc -= __ldg(luT + e) * X[__ldg(n.lu_idx + e) * C + lane];
-        X[r * C + lane] = acc;
-      }
-    }
-    __syncthreads();
-  }
+__device__ __forceinline__ double dth_of(const DevNet& n, const Dir& d, int i) {
+  const int p = __ldg(n.bus_pth + i);
+  return p >= 0 ? d.X[p * C + d.lane] : 0.0;
+}
+template <int C>
+__device__ __forceinline__ double dv_of(const DevNet& n, const Dir& d, int i) {
+  const int p = __ldg(n.bus_pv + i);
+  return p >= 0 ? d.X[p * C + d.lane] : d.vdir(__ldg(n.u_v + i));
 }
 
 struct Coef { double gff, bff, gft, bft, gtf, btf, gtt, btt; };
-
 __device__ __forceinline__ Coef coef(const DevNet& n, int l) {
   Coef c;
   c.gff = __ldg(n.coef + 0 * n.n_l + l); c.bff = __ldg(n.coef + 1 * n.n_l + l);
@@ -112,104 +150,94 @@ __device__ __forceinline__ Coef coef(const DevNet& n, int l) {
 }
 
 template <int C>
-__global__ void __launch_bounds__(kRedThreads) k_reduce(DevNet n, Work w, int n_scen, const double* __restrict__ V,
-                                                        int col0, int N, double* __restrict__ KV) {
-  __shared__ double T[C][kCH + 1];
+__device__ __forceinline__ Dir make_dir(const DevNet& n, const Work& w, const double* V, int col0, int N, int s,
+                                        int tile, size_t cta, int lane) {
+  Dir d;
+  d.lane = lane;
+  const int j = tile * C + lane;
+  d.valid = j < N;
+  d.col = col0 + j;
+  d.X = w.slabZ + cta * n.n_x * C;
+  d.Vs = (V && d.valid) ? V + ((size_t)s * N + j) * n.n_u : nullptr;
+  return d;
+}
+
+// ---------------------------------------------------------------- c1
+// μ_A at the generator buses: dG = R_r M dψ (the bus's line ends plus the
+// shunt part of G_ii ψ^d), μ_A = Σ_r dG (+ 2c1 dG on P_r0, folded into Σ_rP).
+template <int C>
+__global__ void __launch_bounds__(kThreads) k_mu(DevNet n, Work w, const double* __restrict__ V, int col0, int N) {
   const int ntile = (N + C - 1) / C;
-  const int tile = blockIdx.x, s = blockIdx.y;
+  const int tile = blockIdx.y, s = blockIdx.z;
   const size_t cta = (size_t)s * ntile + tile;
   const int lane = threadIdx.x % C, team = threadIdx.x / C, nteam = blockDim.x / C;
-  const int j = tile * C + lane;
-  const bool valid = j < N;
-  const int n_x = n.n_x, n_u = n.n_u, n_l = n.n_l, n_b = n.n_b;
-  double* X = w.slabZ + cta * n_x * C;
-  double* Y = w.slabW + cta * n_x * C;
-  double* Hs = w.hu + cta * n_u * C;
-  double* MU = w.mu + cta * n.n_g * 2 * C;
-  const double* lu = w.lu + (size_t)s * n.nnz_lu;
-  const double* luT = w.luT + (size_t)s * n.nnz_lu;
-  const double* gu = w.gu + (size_t)s * n.nnz_gu;
+  const int gi = blockIdx.x * nteam + team;
+  if (gi >= n.n_gb) return;
+  const Dir d = make_dir<C>(n, w, V, col0, N, s, tile, cta, lane);
+  const int n_l = n.n_l, n_b = n.n_b;
   const double* ls = w.ls + (size_t)s * LS_N * n_l;
   const double* bs = w.bs + (size_t)s * BS_N * n_b;
-  const double* Vs = (V && valid) ? V + ((size_t)s * N + j) * n_u : nullptr;
-  auto vdir = [&](int c) -> double {
-    if (!valid) return 0.0;
-    return Vs ? Vs[c] : (c == col0 + j ? 1.0 : 0.0);
-  };
-
-  // ---- a. tangent right-hand side B = −P G_u V (A7.1)
-  if (V == nullptr) {
-    for (int idx = threadIdx.x; idx < n_x * C; idx += blockDim.x) X[idx] = 0.0;
-    __syncthreads();
-    if (team == 0 && valid) {
-      const int c = col0 + j;
-      for (int e = __ldg(n.guc_ptr + c); e < __ldg(n.guc_ptr + c + 1); ++e)
-        X[__ldg(n.guc_row + e) * C + lane] = -gu[__ldg(n.guc_src + e)];
-    }
-  } else {
-    for (int r = team; r < n_x; r += nteam) {
-      double acc = 0.0;
-      for (int e = __ldg(n.gur_ptr + r); e < __ldg(n.gur_ptr + r + 1); ++e)
-        acc += gu[__ldg(n.gur_src + e)] * vdir(__ldg(n.gur_col + e));
-      X[r * C + lane] = -acc;
+  const int i = __ldg(n.gbus + gi);
+  const double dvi = dv_of<C>(n, d, i), dthi = dth_of<C>(n, d, i);
+  double dP = 0.0, dQ = 0.0;
+  for (int e = __ldg(n.inc_ptr + i); e < __ldg(n.inc_ptr + i + 1); ++e) {
+    const int l = __ldg(n.inc_line + e);
+    const bool from = __ldg(n.lf + l) == i;
+    const int o = from ? __ldg(n.lt + l) : __ldg(n.lf + l);
+    const double dvo = dv_of<C>(n, d, o), dtho = dth_of<C>(n, d, o);
+    const Coef k = coef(n, l);
+    const double vf = ls[LS_VF * n_l + l], vt = ls[LS_VT * n_l + l];
+    const double c = ls[LS_C * n_l + l], sn = ls[LS_S * n_l + l];
+    const double dvf = from ? dvi : dvo, dvt = from ? dvo : dvi;
+    const double dD = from ? dthi - dtho : dtho - dthi;
+    const double pc = vf * vt * c, ps = vf * vt * sn;
+    const double dpc = vt * c * dvf + vf * c * dvt - ps * dD;
+    const double dps = vt * sn * dvf + vf * sn * dvt + pc * dD;
+    if (from) {
+      dP += k.gft * dpc + k.bft * dps + 2.0 * k.gff * vf * dvf;
+      dQ += -k.bft * dpc + k.gft * dps - 2.0 * k.bff * vf * dvf;
+    } else {
+      dP += k.gtf * dpc - k.btf * dps + 2.0 * k.gtt * vt * dvt;
+      dQ += -k.btf * dpc - k.gtf * dps - 2.0 * k.btt * vt * dvt;
     }
   }
-  __syncthreads();
+  const double vi = bs[BS_V * n_b + i];
+  dP += 2.0 * __ldg(n.gsh + i) * vi * dvi;
+  dQ -= 2.0 * __ldg(n.bsh + i) * vi * dvi;
+  double* MU = w.mu + cta * n.n_g * 2 * C;
+  const int g = __ldg(n.bus_gen + i);
+  MU[(2 * g) * C + lane] = bs[BS_SRP * n_b + i] * dP;
+  MU[(2 * g + 1) * C + lane] = bs[BS_SRQ * n_b + i] * dQ;
+}
 
-  // ---- b. forward tangent solve Z̃ = U^{-1} L^{-1} B (A7.2)
-  sweep_L<C>(n, lu, X, lane, team, nteam);
-  sweep_U<C>(n, lu, X, lane, team, nteam);
-
-  auto dth = [&](int i) -> double { const int p = __ldg(n.bus_pth + i); return p >= 0 ? X[p * C + lane] : 0.0; };
-  auto dv = [&](int i) -> double { const int p = __ldg(n.bus_pv + i); return p >= 0 ? X[p * C + lane] : vdir(__ldg(n.u_v + i)); };
-
-  // ---- c1. μ_A = Σ_r ⊙ dG_r at the r buses (generator buses), dG_r = R_r M dψ
-  for (int gi = team; gi < n.n_gb; gi += nteam) {
-    const int i = __ldg(n.gbus + gi);
-    const double dvi = dv(i), dthi = dth(i);
-    double dP = 0.0, dQ = 0.0;
-    for (int e = __ldg(n.inc_ptr + i); e < __ldg(n.inc_ptr + i + 1); ++e) {
-      const int l = __ldg(n.inc_line + e);
-      const bool from = __ldg(n.lf + l) == i;
-      const int o = from ? __ldg(n.lt + l) : __ldg(n.lf + l);
-      const double dvo = dv(o), dtho = dth(o);
-      const Coef k = coef(n, l);
-      const double vf = ls[LS_VF * n_l + l], vt = ls[LS_VT * n_l + l];
-      const double c = ls[LS_C * n_l + l], sn = ls[LS_S * n_l + l];
-      const double dvf = from ? dvi : dvo, dvt = from ? dvo : dvi;
-      const double dD = from ? dthi - dtho : dtho - dthi;
-      const double pc = vf * vt * c, ps = vf * vt * sn;
-      const double dpc = vt * c * dvf + vf * c * dvt - ps * dD;
-      const double dps = vt * sn * dvf + vf * sn * dvt + pc * dD;
-      if (from) {
-        dP += k.gft * dpc + k.bft * dps + 2.0 * k.gff * vf * dvf;
-        dQ += -k.bft * dpc + k.gft * dps - 2.0 * k.bff * vf * dvf;
-      } else {
-        dP += k.gtf * dpc - k.btf * dps + 2.0 * k.gtt * vt * dvt;
-        dQ += -k.btf * dpc - k.gtf * dps - 2.0 * k.btt * vt * dvt;
-      }
-    }
-    const double vi = bs[BS_V * n_b + i];
-    dP += 2.0 * __ldg(n.gsh + i) * vi * dvi;
-    dQ -= 2.0 * __ldg(n.bsh + i) * vi * dvi;
-    const int g = __ldg(n.bus_gen + i);
-    MU[(2 * g) * C + lane] = bs[BS_SRP * n_b + i] * dP;
-    MU[(2 * g + 1) * C + lane] = bs[BS_SRQ * n_b + i] * dQ;
-  }
-  __syncthreads();
-
-  // ---- c2. [H_u; H_x] = K [V; Z] per bus (A7.3), gathering the incident lines
+// ---------------------------------------------------------------- c2
+template <int C>
+__global__ void __launch_bounds__(kThreads) k_hvp(DevNet n, Work w, const double* __restrict__ V, int col0, int N) {
+  const int ntile = (N + C - 1) / C;
+  const int tile = blockIdx.y, s = blockIdx.z;
+  const size_t cta = (size_t)s * ntile + tile;
+  const int lane = threadIdx.x % C, team = threadIdx.x / C, nteam = blockDim.x / C;
+  const Dir d = make_dir<C>(n, w, V, col0, N, s, tile, cta, lane);
+  const int n_l = n.n_l, n_b = n.n_b;
+  const double* ls = w.ls + (size_t)s * LS_N * n_l;
+  const double* bs = w.bs + (size_t)s * BS_N * n_b;
+  const double* MU = w.mu + cta * n.n_g * 2 * C;
+  double* Y = w.slabW + cta * n.n_x * C;
+  double* Hs = w.hu + cta * n.n_u * C;
   auto muP = [&](int b) -> double { const int g = __ldg(n.bus_gen + b); return g >= 0 ? MU[(2 * g) * C + lane] : 0.0; };
   auto muQ = [&](int b) -> double { const int g = __ldg(n.bus_gen + b); return g >= 0 ? MU[(2 * g + 1) * C + lane] : 0.0; };
-  for (int i = team; i < n_b; i += nteam) {
-    const double dvi = dv(i), dthi = dth(i);
+  const int k1 = min(n_b, (int)(blockIdx.x + 1) * kBusPerCta);
+  // buses in elimination order: a chunk's own θ/v rows are contiguous slab rows
+  for (int kb = blockIdx.x * kBusPerCta + team; kb < k1; kb += nteam) {
+    const int i = __ldg(n.hvp_bus + kb);
+    const double dvi = dv_of<C>(n, d, i), dthi = dth_of<C>(n, d, i);
     double hv = 0.0, hth = 0.0;
     for (int e = __ldg(n.inc_ptr + i); e < __ldg(n.inc_ptr + i + 1); ++e) {
       const int l = __ldg(n.inc_line + e);
       const int f = __ldg(n.lf + l), t = __ldg(n.lt + l);
       const bool from = f == i;
       const int o = from ? t : f;
-      const double dvo = dv(o), dtho = dth(o);
+      const double dvo = dv_of<C>(n, d, o), dtho = dth_of<C>(n, d, o);
       const Coef k = coef(n, l);
       const double vf = ls[LS_VF * n_l + l], vt = ls[LS_VT * n_l + l];
       const double c = ls[LS_C * n_l + l], sn = ls[LS_S * n_l + l];
@@ -226,7 +254,7 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce(DevNet n, Work w, int n_
       const double dsqt = -k.btf * dpc - k.gtf * dps - 2.0 * k.btt * vt * dvt;
       const double spf = ls[LS_SPF * n_l + l], sqf = ls[LS_SQF * n_l + l];
       const double spt = ls[LS_SPT * n_l + l], sqt = ls[LS_SQT * n_l + l];
-      // dH = 2(s_p ds_p + s_q ds_q);  ḡ_s = 2ŷ⊙ds + 2 s ⊙ (Σ_h dH)
+      // Σ_h dH with dH = 2(s_p ds_p + s_q ds_q);  ḡ_s = 2ŷ⊙ds + 2 s ⊙ (Σ_h dH)
       const double sgf = ls[LS_SGF * n_l + l] * 2.0 * (spf * dspf + sqf * dsqf);
       const double sgt = ls[LS_SGT * n_l + l] * 2.0 * (spt * dspt + sqt * dsqt);
       const double y2f = ls[LS_Y2F * n_l + l], y2t = ls[LS_Y2T * n_l + l];
@@ -261,17 +289,28 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce(DevNet n, Work w, int n_
     if (pv >= 0) Y[pv * C + lane] = hv;
     else Hs[__ldg(n.u_v + i) * C + lane] = hv;
   }
-  for (int g = team; g < n.n_g; g += nteam) {  // objective curvature on explicit p_g
-    const int up = __ldg(n.u_p + g);
-    if (up >= 0) Hs[up * C + lane] = 2.0 * __ldg(n.c_quad + g) * vdir(up);
-  }
-  __syncthreads();
+  if (blockIdx.x == 0)  // objective curvature on explicit p_g
+    for (int g = team; g < n.n_g; g += nteam) {
+      const int up = __ldg(n.u_p + g);
+      if (up >= 0) Hs[up * C + lane] = 2.0 * __ldg(n.c_quad + g) * d.vdir(up);
+    }
+}
 
-  // ---- d. adjoint solve Ψ̃ = L^{-T} U^{-T} H̃_x (A7.4)
-  sweep_UT<C>(n, lu, luT, Y, lane, team, nteam);
-  sweep_LT<C>(n, luT, Y, lane, team, nteam);
-
-  // ---- e. K̂V = H_u − (P G_u)ᵀ Ψ̃ (A7.5, R11)
+// ---------------------------------------------------------------- d, e
+template <int C>
+__global__ void __launch_bounds__(kThreads, 4) k_adj(DevNet n, Work w, int N, double* __restrict__ KV) {
+  __shared__ double T[C][kCH + 1];
+  const int ntile = (N + C - 1) / C;
+  const int tile = blockIdx.x, s = blockIdx.y;
+  const size_t cta = (size_t)s * ntile + tile;
+  const int lane = threadIdx.x % C, team = threadIdx.x / C, nteam = blockDim.x / C;
+  const int n_x = n.n_x, n_u = n.n_u;
+  double* Y = w.slabW + cta * n_x * C;
+  const double* Hs = w.hu + cta * n_u * C;
+  const double* gu = w.gu + (size_t)s * n.nnz_gu;
+  const double2* pk = w.pkT + (size_t)s * n.nnz_lu;
+  sweep<C, true>(n, pk, Y, true, lane, team, nteam);    // U^{-T}
+  sweep<C, false>(n, pk, Y, false, lane, team, nteam);  // L^{-T}
   for (int c0 = 0; c0 < n_u; c0 += kCH) {
     for (int cc = team; cc < kCH && c0 + cc < n_u; cc += nteam) {
       const int c = c0 + cc;
@@ -291,6 +330,22 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce(DevNet n, Work w, int n_
   }
 }
 
+template <int C>
+void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int col0, int N, double* KV,
+                cudaStream_t st, cudaEvent_t* ev) {
+  const int ntile = (N + C - 1) / C;
+  const int teams = kThreads / C;
+  if (ev) cudaEventRecord(ev[0], st);
+  k_fwd<C><<<dim3(ntile, n_scen), kThreads, 0, st>>>(n, w, V, col0, N);
+  if (ev) cudaEventRecord(ev[1], st);
+  k_mu<C><<<dim3((n.n_gb + teams - 1) / teams, ntile, n_scen), kThreads, 0, st>>>(n, w, V, col0, N);
+  if (ev) cudaEventRecord(ev[2], st);
+  k_hvp<C><<<dim3((n.n_b + kBusPerCta - 1) / kBusPerCta, ntile, n_scen), kThreads, 0, st>>>(n, w, V, col0, N);
+  if (ev) cudaEventRecord(ev[3], st);
+  k_adj<C><<<dim3(ntile, n_scen), kThreads, 0, st>>>(n, w, N, KV);
+  if (ev) cudaEventRecord(ev[4], st);
+}
+
 }  // namespace
 
 int pick_tile_cols(int n_x, int total_cols) {
@@ -301,14 +356,13 @@ int pick_tile_cols(int n_x, int total_cols) {
 }
 
 int launch_reduce(const DevNet& n, const Work& w, int C, int n_scen, const double* V, int col0,
-                  int N, double* KV, cudaStream_t st) {
-  dim3 grid((N + C - 1) / C, n_scen);
+                  int N, double* KV, cudaStream_t st, cudaEvent_t* ev) {
   switch (C) {
-    case 32: k_reduce<32><<<grid, kRedThreads, 0, st>>>(n, w, n_scen, V, col0, N, KV); break;
-    case 16: k_reduce<16><<<grid, kRedThreads, 0, st>>>(n, w, n_scen, V, col0, N, KV); break;
-    default: k_reduce<8><<<grid, kRedThreads, 0, st>>>(n, w, n_scen, V, col0, N, KV); break;
+    case 32: launch_all<32>(n, w, n_scen, V, col0, N, KV, st, ev); break;
+    case 16: launch_all<16>(n, w, n_scen, V, col0, N, KV, st, ev); break;
+    default: launch_all<8>(n, w, n_scen, V, col0, N, KV, st, ev); break;
   }
-  return 1;
+  return 4;
 }
 
 }  // namespace pf

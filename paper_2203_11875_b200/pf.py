@@ -25,7 +25,7 @@ STRUCTURE = dict(x_theta=0, x_v=1, u_v=2, u_p=3, gx_ptr=4, gx_idx=5, gu_ptr=6, g
 # exported symbols declared in include/pf.h
 SYMBOLS = ["pf_build_network", "pf_destroy", "pf_query", "pf_get_structure", "pf_last_error", "pf_build_error",
            "pf_eval_constraints", "pf_jacobian", "pf_reduced_hessian_batch", "pf_condensed_kkt_solve",
-           "pf_launch_count"]
+           "pf_launch_count", "pf_profile", "pf_kernel_times"]
 
 
 class PFError(RuntimeError):
@@ -75,6 +75,10 @@ def load_library():
     lib.pf_condensed_kkt_solve.restype = ctypes.c_int
     lib.pf_launch_count.argtypes = [P]
     lib.pf_launch_count.restype = ctypes.c_int64
+    lib.pf_profile.argtypes = [P, I32]
+    lib.pf_profile.restype = ctypes.c_int
+    lib.pf_kernel_times.argtypes = [P, P, I32]
+    lib.pf_kernel_times.restype = ctypes.c_int32
     _lib = lib
     return lib
 
@@ -176,6 +180,17 @@ class Network:
 
     def launch_count(self):
         return int(self._lib.pf_launch_count(self._h))
+
+    KERNELS = ("k_fwd", "k_mu", "k_hvp", "k_adj", "k_lu")
+
+    def profile(self, enable=True):
+        self._check(self._lib.pf_profile(self._h, int(enable)), "pf_profile")
+
+    def kernel_times(self):
+        """Per-kernel ms of the last reduction / jacobian calls (profiling on)."""
+        ms = (ctypes.c_float * 5)()
+        k = self._lib.pf_kernel_times(self._h, ctypes.cast(ms, ctypes.c_void_p), 5)
+        return {self.KERNELS[i]: float(ms[i]) for i in range(k)}
 
     # ---------------------------------------------------------------- compute
     def pf_eval_constraints(self, n_scen, v, theta, p_g, q_g, p_d=None, q_d=None, G=None, H=None, s_flow=None,

@@ -1,12 +1,11 @@
 #!/bin/bash
-# One GPU round-trip: parity tests (incl. full-size sampled), bench, ncu launch list + full capture of k_reduce.
-set -x
+# One GPU round-trip: parity tests (incl. full-size sampled), bench, ncu launch list + full capture of the hot kernels.
 mkdir -p gpurun_out
 python -m paper_2203_11875_b200._build
 timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 600 python bench.py --steps ${STEPS:-5} --warmup 3 ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-    python bench.py --profile-steps 1 --delta-w 1e5 > gpurun_out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_reduce -c 1 -f -o gpurun_out/prof_reduce \
-    python bench.py --profile-steps 1 --delta-w 1e5 > gpurun_out/ncu_full.log 2>&1
+    python bench.py --profile-steps 1 --delta-w 1e6 ${BENCH_ARGS} > gpurun_out/ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${NCU_K:-k_fwd|k_hvp|k_adj}" -c ${NCU_C:-3} -f \
+    -o gpurun_out/prof_reduce python bench.py --profile-steps 1 --delta-w 1e6 ${BENCH_ARGS} > gpurun_out/ncu_full.log 2>&1
 tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
