@@ -127,6 +127,7 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
   std::vector<int4> rowmeta(P.n_x);
   for (int r = 0; r < P.n_x; ++r) rowmeta[r] = make_int4(P.lu_ptr[r], P.lu_diag[r], P.lu_ptr[r + 1], P.row_blk[r]);
   d.C = h->C;
+  d.lu_maxlen = P.lu_maxlen;
 
   bool ok = up(h, lf, &d.lf) && up(h, lt, &d.lt) && up(h, coef, &d.coef) && up(h, gsh, &d.gsh) &&
             up(h, bsh, &d.bsh) && up(h, gb, &d.gen_bus) && up(h, P.bus_gen, &d.bus_gen) &&
@@ -151,8 +152,8 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
   w.max_tiles = max_scen * ((max_batch + h->C - 1) / h->C);
   const size_t T = w.max_tiles, C = h->C;
   ok = ok && alloc(h, S * d.nnz_jb, &w.jb) && alloc(h, S * d.nnz_gu, &w.gu) && alloc(h, S * d.nnz_lu, &w.lu) &&
-       alloc(h, S * d.nnz_lu, &w.luT) && alloc(h, S * d.nnz_lu, &w.pkA) && alloc(h, S * d.nnz_lu, &w.pkT) && alloc(h, S * d.n_x, &w.rowmax) && alloc(h, S * LS_N * d.n_l, &w.ls) &&
-       alloc(h, S * BS_N * d.n_b, &w.bs) && alloc(h, S * 4 * d.n_l, &w.sflow) && alloc(h, 2 * S, &w.info) &&
+       alloc(h, S * d.nnz_lu, &w.luT) && alloc(h, S * d.nnz_lu, &w.pkA) && alloc(h, S * d.nnz_lu, &w.pkT) && alloc(h, S * d.n_x, &w.rowmax) && alloc(h, S * d.n_x, &w.invd) && alloc(h, S * LS_N * d.n_l, &w.ls) &&
+       alloc(h, S * BS_N * d.n_b, &w.bs) && alloc(h, S * LB_N * d.n_l, &w.lblk) && alloc(h, S * 4 * d.n_l, &w.sflow) && alloc(h, 2 * S, &w.info) &&
        alloc(h, T * d.n_x * C, &w.slabZ) && alloc(h, T * d.n_x * C, &w.slabW) &&
        alloc(h, T * d.n_u * C, &w.hu) && alloc(h, T * d.n_g * 2 * C, &w.mu);
   if (!ok) {

@@ -28,12 +28,16 @@ struct DevNet {
   const int4 *rowmeta;          // [n_x] {lu_ptr[r], lu_diag[r], lu_ptr[r+1], block of r}
   const int *hvp_bus;           // [n_b] buses in elimination order, the reference bus last
   int C;                        // directions per tile (slab row width)
+  int lu_maxlen;                // longest row of the filled LU pattern
 };
 
 // Per-scenario point state, SoA.  Line state (LS_*) and bus state (BS_*).
 enum { LS_VF, LS_VT, LS_C, LS_S, LS_SPF, LS_SQF, LS_SPT, LS_SQT,
        LS_WC, LS_WS, LS_Y2F, LS_Y2T, LS_SGF, LS_SGT, LS_DF, LS_DT, LS_N };
 enum { BS_V, BS_MUP, BS_MUQ, BS_WD2, BS_SRP, BS_SRQ, BS_SXT, BS_SXV, BS_N };
+// Per-line K blocks (AoS, 18 doubles = 9 × 16 B): symmetric H (3×3) on
+// (v_f, v_t, Δ) and J (4×3) = ∂(s_p^f, s_q^f, s_p^t, s_q^t)/∂(v_f, v_t, Δ).
+enum { LB_H00, LB_H01, LB_H02, LB_H11, LB_H12, LB_H22, LB_J, LB_N = LB_J + 12 };
 
 struct Work {
   double* jb;      // [max_scen][nnz_jb]  J_bus values
@@ -43,8 +47,10 @@ struct Work {
   double2* pkA;    // [max_scen][nnz_lu]  packed {lu[e], bits(idx[e]*C)} for the L / U sweeps
   double2* pkT;    // [max_scen][nnz_lu]  packed {luT[e], bits(idx[e]*C)} for the Uᵀ / Lᵀ sweeps
   double* rowmax;  // [max_scen][n_x]     pivot threshold scale (R18)
+  double* invd;    // [max_scen][n_x]     1 / u_rr of the factorized rows
   double* ls;      // [max_scen][LS_N][n_l]
   double* bs;      // [max_scen][BS_N][n_b]
+  double* lblk;    // [max_scen][n_l][LB_N]  line-local K blocks
   double* sflow;   // [max_scen][4][n_l]
   int* info;       // [max_scen] internal pivot info
   double* slabZ;   // [max_tiles][n_x][C]

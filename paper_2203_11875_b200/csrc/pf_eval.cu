@@ -268,28 +268,56 @@ __global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int n_scen,
     }
   }
   grid.sync();
+  extern __shared__ double lu_ws[];
+  double* ws = lu_ws + warp * n.lu_maxlen;  // the warp's dense row workspace
+  double* invd = w.invd + (size_t)(active ? s : 0) * n.n_x;
   for (int lev = 0; lev < n.nlevL; ++lev) {
     if (active) {
       const int b0 = __ldg(n.levL_ptr + lev), b1 = __ldg(n.levL_ptr + lev + 1);
       for (int bi = b0 + gwarp; bi < b1; bi += ngwarp) {
         const int p = __ldg(n.levL_blk + bi);
         for (int r = __ldg(n.blk_ptr + p); r < __ldg(n.blk_ptr + p + 1); ++r) {
-          const int dr = __ldg(n.lu_diag + r);
-          for (int e = __ldg(n.lu_ptr + r); e < dr; ++e) {
-            const int k = __ldg(n.lu_idx + e);
-            const double l = __ldcg(lu + e) / __ldcg(lu + __ldg(n.lu_diag + k));
-            __syncwarp();
-            if (lane == 0) __stcg(lu + e, l);
-            const int u0 = __ldg(n.lu_diag + k) + 1;
-            const int q0 = __ldg(n.upd_ptr + e), cnt = __ldg(n.upd_ptr + e + 1) - q0;
-            for (int t = lane; t < cnt; t += 32) {
-              double* dst = lu + __ldg(n.upd_dst + q0 + t);
-              __stcg(dst, __ldcg(dst) - l * __ldcg(lu + u0 + t));
+          const int base = __ldg(n.lu_ptr + r), len = __ldg(n.lu_ptr + r + 1) - base;
+          const int dl = __ldg(n.lu_diag + r) - base;
+          for (int a = lane; a < len; a += 32) ws[a] = __ldcg(lu + base + a);
+          __syncwarp();
+          // IKJ over the row's L entries; the U row of the next pivot is
+          // prefetched into registers while the current update runs.
+          double pu[4], pin = 0.0;
+          int pq0 = 0, pcnt = 0, pu0 = 0;
+          auto fetch = [&](int a) {
+            const int e = base + a, k = __ldg(n.lu_idx + e);
+            pu0 = __ldg(n.lu_diag + k) + 1;
+            pq0 = __ldg(n.upd_ptr + e);
+            pcnt = __ldg(n.upd_ptr + e + 1) - pq0;
+            pin = __ldcg(invd + k);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int t = lane + 32 * j;
+              pu[j] = t < pcnt ? __ldcg(lu + pu0 + t) : 0.0;
             }
+          };
+          if (dl > 0) fetch(0);
+          for (int a = 0; a < dl; ++a) {
+            double cu[4] = {pu[0], pu[1], pu[2], pu[3]};
+            const double cin = pin;
+            const int q0 = pq0, cnt = pcnt, u0 = pu0;
+            if (a + 1 < dl) fetch(a + 1);
+            const double l = ws[a] * cin;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int t = lane + 32 * j;
+              if (t < cnt) ws[__ldg(n.upd_dst + q0 + t)] -= l * cu[j];
+            }
+            for (int t = lane + 128; t < cnt; t += 32) ws[__ldg(n.upd_dst + q0 + t)] -= l * __ldcg(lu + u0 + t);
             __syncwarp();
+            if (lane == 0) ws[a] = l;
           }
+          __syncwarp();
+          for (int a = lane; a < len; a += 32) __stcg(lu + base + a, ws[a]);
           if (lane == 0) {
-            const double d = __ldcg(lu + dr);
+            const double d = ws[dl];
+            __stcg(invd + r, 1.0 / d);
             if (!(fabs(d) >= 1e-12 * rowmax[r]) || !isfinite(d) || d == 0.0) atomicMin(w.info + s, r + 1);
           }
           __syncwarp();
@@ -391,6 +419,51 @@ __global__ void k_prep_line(DevNet n, Work w, int n_scen, const double* __restri
     ls[LS_DT * n.n_l + l] = k.gtt * Etp - k.btt * Etq;
     ls[LS_Y2F * n.n_l + l] = y2f; ls[LS_Y2T * n.n_l + l] = y2t;
     ls[LS_SGF * n.n_l + l] = sgf; ls[LS_SGT * n.n_l + l] = sgt;
+
+    // Line-local blocks of K in the coordinates (v_f, v_t, Δ = θ_f − θ_t):
+    //   J (4×3) = ∂(s_p^f, s_q^f, s_p^t, s_q^t) = L_line J_ψ (+ the v² columns),
+    //   H (3×3) = w̄^c ∇²ψ^c + w̄^s ∇²ψ^s                       (second order, A6)
+    //           + Σ_ends 2ŷ (∇s_p∇s_pᵀ + ∇s_q∇s_qᵀ)            (y_h Gauss–Newton)
+    //           + Σ_ends Σ_h ∇H ∇Hᵀ, ∇H = 2(s_p∇s_p + s_q∇s_q)   (AᵀΣ_sA on h rows).
+    // K·d restricted to the line is then H d_loc + Jᵀ μ_A(ends): linear in d,
+    // so it is precomputed once per scenario instead of once per direction.
+    {
+      const double vf = ls[LS_VF * n.n_l + l], vt = ls[LS_VT * n.n_l + l];
+      const double c = ls[LS_C * n.n_l + l], sn = ls[LS_S * n.n_l + l];
+      const double pc = vf * vt * c, ps = vf * vt * sn;
+      const double dc[3] = {vt * c, vf * c, -ps}, ds[3] = {vt * sn, vf * sn, pc};
+      double J[4][3];
+      for (int a = 0; a < 3; ++a) {
+        J[0][a] = k.gft * dc[a] + k.bft * ds[a];
+        J[1][a] = -k.bft * dc[a] + k.gft * ds[a];
+        J[2][a] = k.gtf * dc[a] - k.btf * ds[a];
+        J[3][a] = -k.btf * dc[a] - k.gtf * ds[a];
+      }
+      J[0][0] += 2.0 * k.gff * vf; J[1][0] -= 2.0 * k.bff * vf;
+      J[2][1] += 2.0 * k.gtt * vt; J[3][1] -= 2.0 * k.btt * vt;
+      const double wc = ls[LS_WC * n.n_l + l], ws = ls[LS_WS * n.n_l + l];
+      // ∇²ψ^c = [[0, c, −v_t s], [c, 0, −v_f s], [−v_t s, −v_f s, −ψ^c]],
+      // ∇²ψ^s = [[0, s, v_t c], [s, 0, v_f c], [v_t c, v_f c, −ψ^s]]
+      double H[3][3] = {{0.0, wc * c + ws * sn, -wc * vt * sn + ws * vt * c},
+                        {0.0, 0.0, -wc * vf * sn + ws * vf * c},
+                        {0.0, 0.0, -wc * pc - ws * ps}};
+      const double spv[2] = {ls[LS_SPF * n.n_l + l], ls[LS_SPT * n.n_l + l]};
+      const double sqv[2] = {ls[LS_SQF * n.n_l + l], ls[LS_SQT * n.n_l + l]};
+      const double y2[2] = {y2f, y2t}, sg[2] = {sgf, sgt};
+      for (int e = 0; e < 2; ++e) {
+        const double* Jp = J[2 * e];
+        const double* Jq = J[2 * e + 1];
+        double gH[3];
+        for (int a = 0; a < 3; ++a) gH[a] = 2.0 * (spv[e] * Jp[a] + sqv[e] * Jq[a]);
+        for (int a = 0; a < 3; ++a)
+          for (int b = a; b < 3; ++b) H[a][b] += y2[e] * (Jp[a] * Jp[b] + Jq[a] * Jq[b]) + sg[e] * gH[a] * gH[b];
+      }
+      double* o = w.lblk + ((size_t)s * n.n_l + l) * LB_N;
+      o[LB_H00] = H[0][0]; o[LB_H01] = H[0][1]; o[LB_H02] = H[0][2];
+      o[LB_H11] = H[1][1]; o[LB_H12] = H[1][2]; o[LB_H22] = H[2][2];
+      for (int r = 0; r < 4; ++r)
+        for (int a = 0; a < 3; ++a) o[LB_J + 3 * r + a] = J[r][a];
+    }
   }
 }
 
@@ -427,20 +500,19 @@ int launch_jacobian(const DevNet& n, const Work& w, int n_scen, const double* v,
   k_bus_v<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen, v);
   k_jbus<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen);
   k_gather<<<blocks_for((long long)n_scen * (n.nnz_gx + n.nnz_gu + n.nnz_a)), kThreads, 0, st>>>(n, w, n_scen, Gx, Gu, A);
-  static int lu_grid = 0;
-  if (lu_grid == 0) {
-    int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lu, kLuThreads, 0);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    lu_grid = std::max(1, per_sm) * sms;
-  }
+  const size_t smem = (size_t)(kLuThreads / 32) * n.lu_maxlen * sizeof(double);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lu, kLuThreads, smem);
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int lu_grid = std::max(1, per_sm) * sms;
   int P = std::max(1, lu_grid / n_scen);
   int grid = P * n_scen;
   if (grid > lu_grid) { P = 1; grid = n_scen; }  // more scenarios than co-resident CTAs: not supported cooperatively
   void* args[] = {(void*)&n, (void*)&w, (void*)&n_scen, (void*)&P, (void*)&info};
   if (ev) cudaEventRecord(ev[0], st);
-  cudaLaunchCooperativeKernel((void*)k_lu, dim3(grid), dim3(kLuThreads), args, 0, st);
+  cudaLaunchCooperativeKernel((void*)k_lu, dim3(grid), dim3(kLuThreads), args, smem, st);
   if (ev) cudaEventRecord(ev[1], st);
   k_lu_info<<<1, 256, 0, st>>>(n_scen, w.info, info);
   return 6;

@@ -264,10 +264,11 @@ std::string build_plan(int n_b, int n_l, int n_g, const int32_t* lf, const int32
       int kk = P.lu_idx[e];
       if (kk < r)
         for (int s = P.lu_diag[kk] + 1; s < P.lu_ptr[kk + 1]; ++s)
-          P.upd_dst.push_back(find_in_row(P.lu_ptr, P.lu_idx, r, P.lu_idx[s]));
+          P.upd_dst.push_back(find_in_row(P.lu_ptr, P.lu_idx, r, P.lu_idx[s]) - P.lu_ptr[r]);  // offset in row r
       P.upd_ptr[e + 1] = (int)P.upd_dst.size();
     }
   for (int d : P.upd_dst) if (d < 0) return "internal error: fill pattern not closed";
+  for (int r = 0; r < n_x; ++r) P.lu_maxlen = std::max(P.lu_maxlen, P.lu_ptr[r + 1] - P.lu_ptr[r]);
 
   // level sets (longest path in the block DAGs)
   std::vector<int> levL(nblk, 0), levU(nblk, 0);

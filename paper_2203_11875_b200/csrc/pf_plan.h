@@ -37,7 +37,8 @@ struct Plan {
   // ordering and symbolic LU of P G_x Pᵀ (R18)
   std::vector<int> bus_order, perm, iperm, blk_ptr, blk_bus, row_blk;
   std::vector<int> lu_ptr, lu_idx, lu_diag, lu_src, lu_tpos;
-  std::vector<int> upd_ptr, upd_dst;       // per LU entry: range in upd_dst (L entries only)
+  std::vector<int> upd_ptr, upd_dst;       // per LU entry: range in upd_dst (L entries only); dst = offset in the row
+  int lu_maxlen = 0;                       // longest row of the filled pattern
   std::vector<int> levL_ptr, levL_blk, levU_ptr, levU_blk;
   std::vector<double> row_scale_dummy;
 

@@ -139,16 +139,6 @@ __device__ __forceinline__ double dv_of(const DevNet& n, const Dir& d, int i) {
   return p >= 0 ? d.X[p * C + d.lane] : d.vdir(__ldg(n.u_v + i));
 }
 
-struct Coef { double gff, bff, gft, bft, gtf, btf, gtt, btt; };
-__device__ __forceinline__ Coef coef(const DevNet& n, int l) {
-  Coef c;
-  c.gff = __ldg(n.coef + 0 * n.n_l + l); c.bff = __ldg(n.coef + 1 * n.n_l + l);
-  c.gft = __ldg(n.coef + 2 * n.n_l + l); c.bft = __ldg(n.coef + 3 * n.n_l + l);
-  c.gtf = __ldg(n.coef + 4 * n.n_l + l); c.btf = __ldg(n.coef + 5 * n.n_l + l);
-  c.gtt = __ldg(n.coef + 6 * n.n_l + l); c.btt = __ldg(n.coef + 7 * n.n_l + l);
-  return c;
-}
-
 template <int C>
 __device__ __forceinline__ Dir make_dir(const DevNet& n, const Work& w, const double* V, int col0, int N, int s,
                                         int tile, size_t cta, int lane) {
@@ -162,9 +152,23 @@ __device__ __forceinline__ Dir make_dir(const DevNet& n, const Work& w, const do
   return d;
 }
 
+// Line block of K (pf_eval.cu k_prep_line): H (3×3 sym) and J (4×3) on the
+// local coordinates (v_f, v_t, Δ), 9 × 16-byte loads.
+struct LBlk { double h[6], j[12]; };
+__device__ __forceinline__ void load_h(const double* p, double* h) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+  h[0] = a.x; h[1] = a.y; h[2] = b.x; h[3] = b.y; h[4] = c.x; h[5] = c.y;
+}
+__device__ __forceinline__ void load_j(const double* p, double* j) {
+  const double2* q = reinterpret_cast<const double2*>(p + LB_J);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) { const double2 v = __ldg(q + k); j[2 * k] = v.x; j[2 * k + 1] = v.y; }
+}
+
 // ---------------------------------------------------------------- c1
-// μ_A at the generator buses: dG = R_r M dψ (the bus's line ends plus the
-// shunt part of G_ii ψ^d), μ_A = Σ_r dG (+ 2c1 dG on P_r0, folded into Σ_rP).
+// μ_A at the generator buses: dG = R_r M dψ = Σ_{ends at i} J_end · d_loc plus
+// the shunt part of G_ii ψ^d; μ_A = Σ_r dG (+ 2c1 dG on P_r0, folded into Σ_rP).
 template <int C>
 __global__ void __launch_bounds__(kThreads) k_mu(DevNet n, Work w, const double* __restrict__ V, int col0, int N) {
   const int ntile = (N + C - 1) / C;
@@ -174,8 +178,8 @@ __global__ void __launch_bounds__(kThreads) k_mu(DevNet n, Work w, const double*
   const int gi = blockIdx.x * nteam + team;
   if (gi >= n.n_gb) return;
   const Dir d = make_dir<C>(n, w, V, col0, N, s, tile, cta, lane);
-  const int n_l = n.n_l, n_b = n.n_b;
-  const double* ls = w.ls + (size_t)s * LS_N * n_l;
+  const int n_b = n.n_b;
+  const double* lb = w.lblk + (size_t)s * n.n_l * LB_N;
   const double* bs = w.bs + (size_t)s * BS_N * n_b;
   const int i = __ldg(n.gbus + gi);
   const double dvi = dv_of<C>(n, d, i), dthi = dth_of<C>(n, d, i);
@@ -185,21 +189,13 @@ __global__ void __launch_bounds__(kThreads) k_mu(DevNet n, Work w, const double*
     const bool from = __ldg(n.lf + l) == i;
     const int o = from ? __ldg(n.lt + l) : __ldg(n.lf + l);
     const double dvo = dv_of<C>(n, d, o), dtho = dth_of<C>(n, d, o);
-    const Coef k = coef(n, l);
-    const double vf = ls[LS_VF * n_l + l], vt = ls[LS_VT * n_l + l];
-    const double c = ls[LS_C * n_l + l], sn = ls[LS_S * n_l + l];
     const double dvf = from ? dvi : dvo, dvt = from ? dvo : dvi;
     const double dD = from ? dthi - dtho : dtho - dthi;
-    const double pc = vf * vt * c, ps = vf * vt * sn;
-    const double dpc = vt * c * dvf + vf * c * dvt - ps * dD;
-    const double dps = vt * sn * dvf + vf * sn * dvt + pc * dD;
-    if (from) {
-      dP += k.gft * dpc + k.bft * dps + 2.0 * k.gff * vf * dvf;
-      dQ += -k.bft * dpc + k.gft * dps - 2.0 * k.bff * vf * dvf;
-    } else {
-      dP += k.gtf * dpc - k.btf * dps + 2.0 * k.gtt * vt * dvt;
-      dQ += -k.btf * dpc - k.gtf * dps - 2.0 * k.btt * vt * dvt;
-    }
+    double J[12];
+    load_j(lb + (size_t)l * LB_N, J);
+    // rows (s_p, s_q) of this end
+    dP += from ? J[0] * dvf + J[1] * dvt + J[2] * dD : J[6] * dvf + J[7] * dvt + J[8] * dD;
+    dQ += from ? J[3] * dvf + J[4] * dvt + J[5] * dD : J[9] * dvf + J[10] * dvt + J[11] * dD;
   }
   const double vi = bs[BS_V * n_b + i];
   dP += 2.0 * __ldg(n.gsh + i) * vi * dvi;
@@ -211,6 +207,9 @@ __global__ void __launch_bounds__(kThreads) k_mu(DevNet n, Work w, const double*
 }
 
 // ---------------------------------------------------------------- c2
+// [H_u; H_x] = K [V; Z]: per bus, Σ over incident lines of the line block
+// (H d_loc + Jᵀ μ_A(ends)) restricted to the bus's own (v, θ), plus the bus
+// terms 2w̄^d dv (ψ^d curvature), the shunt part of Mᵀμ_A, and Σ_x.
 template <int C>
 __global__ void __launch_bounds__(kThreads) k_hvp(DevNet n, Work w, const double* __restrict__ V, int col0, int N) {
   const int ntile = (N + C - 1) / C;
@@ -218,19 +217,20 @@ __global__ void __launch_bounds__(kThreads) k_hvp(DevNet n, Work w, const double
   const size_t cta = (size_t)s * ntile + tile;
   const int lane = threadIdx.x % C, team = threadIdx.x / C, nteam = blockDim.x / C;
   const Dir d = make_dir<C>(n, w, V, col0, N, s, tile, cta, lane);
-  const int n_l = n.n_l, n_b = n.n_b;
-  const double* ls = w.ls + (size_t)s * LS_N * n_l;
+  const int n_b = n.n_b;
+  const double* lb = w.lblk + (size_t)s * n.n_l * LB_N;
   const double* bs = w.bs + (size_t)s * BS_N * n_b;
   const double* MU = w.mu + cta * n.n_g * 2 * C;
   double* Y = w.slabW + cta * n.n_x * C;
   double* Hs = w.hu + cta * n.n_u * C;
-  auto muP = [&](int b) -> double { const int g = __ldg(n.bus_gen + b); return g >= 0 ? MU[(2 * g) * C + lane] : 0.0; };
-  auto muQ = [&](int b) -> double { const int g = __ldg(n.bus_gen + b); return g >= 0 ? MU[(2 * g + 1) * C + lane] : 0.0; };
   const int k1 = min(n_b, (int)(blockIdx.x + 1) * kBusPerCta);
   // buses in elimination order: a chunk's own θ/v rows are contiguous slab rows
   for (int kb = blockIdx.x * kBusPerCta + team; kb < k1; kb += nteam) {
     const int i = __ldg(n.hvp_bus + kb);
     const double dvi = dv_of<C>(n, d, i), dthi = dth_of<C>(n, d, i);
+    const int gi_own = __ldg(n.bus_gen + i);
+    const double mPi = gi_own >= 0 ? MU[(2 * gi_own) * C + lane] : 0.0;
+    const double mQi = gi_own >= 0 ? MU[(2 * gi_own + 1) * C + lane] : 0.0;
     double hv = 0.0, hth = 0.0;
     for (int e = __ldg(n.inc_ptr + i); e < __ldg(n.inc_ptr + i + 1); ++e) {
       const int l = __ldg(n.inc_line + e);
@@ -238,50 +238,31 @@ __global__ void __launch_bounds__(kThreads) k_hvp(DevNet n, Work w, const double
       const bool from = f == i;
       const int o = from ? t : f;
       const double dvo = dv_of<C>(n, d, o), dtho = dth_of<C>(n, d, o);
-      const Coef k = coef(n, l);
-      const double vf = ls[LS_VF * n_l + l], vt = ls[LS_VT * n_l + l];
-      const double c = ls[LS_C * n_l + l], sn = ls[LS_S * n_l + l];
       const double dvf = from ? dvi : dvo, dvt = from ? dvo : dvi;
       const double dD = from ? dthi - dtho : dtho - dthi;
-      const double pc = vf * vt * c, ps = vf * vt * sn;
-      // dψ = J_ψ d
-      const double dpc = vt * c * dvf + vf * c * dvt - ps * dD;
-      const double dps = vt * sn * dvf + vf * sn * dvt + pc * dD;
-      // ds = L_line dψ
-      const double dspf = k.gft * dpc + k.bft * dps + 2.0 * k.gff * vf * dvf;
-      const double dsqf = -k.bft * dpc + k.gft * dps - 2.0 * k.bff * vf * dvf;
-      const double dspt = k.gtf * dpc - k.btf * dps + 2.0 * k.gtt * vt * dvt;
-      const double dsqt = -k.btf * dpc - k.gtf * dps - 2.0 * k.btt * vt * dvt;
-      const double spf = ls[LS_SPF * n_l + l], sqf = ls[LS_SQF * n_l + l];
-      const double spt = ls[LS_SPT * n_l + l], sqt = ls[LS_SQT * n_l + l];
-      // Σ_h dH with dH = 2(s_p ds_p + s_q ds_q);  ḡ_s = 2ŷ⊙ds + 2 s ⊙ (Σ_h dH)
-      const double sgf = ls[LS_SGF * n_l + l] * 2.0 * (spf * dspf + sqf * dsqf);
-      const double sgt = ls[LS_SGT * n_l + l] * 2.0 * (spt * dspt + sqt * dsqt);
-      const double y2f = ls[LS_Y2F * n_l + l], y2t = ls[LS_Y2T * n_l + l];
-      // end efforts e = ḡ_s + μ_A (M's line columns equal L_line's, R4)
-      const double efp = y2f * dspf + 2.0 * spf * sgf + muP(f);
-      const double efq = y2f * dsqf + 2.0 * sqf * sgf + muQ(f);
-      const double etp = y2t * dspt + 2.0 * spt * sgt + muP(t);
-      const double etq = y2t * dsqt + 2.0 * sqt * sgt + muQ(t);
-      // ḡ_ψ = L_lineᵀ ḡ_s + Mᵀ μ_A
-      const double gc = k.gft * efp - k.bft * efq + k.gtf * etp - k.btf * etq;
-      const double gs = k.bft * efp + k.gft * efq - k.btf * etp - k.gtf * etq;
-      // Σ_k w̄_k ∇²ψ_k d (line-local 4×4)
-      const double wc = ls[LS_WC * n_l + l], ws = ls[LS_WS * n_l + l];
-      const double hD = wc * (-vt * sn * dvf - vf * sn * dvt - pc * dD) + ws * (vt * c * dvf + vf * c * dvt - ps * dD);
-      const double jth = -ps * gc + pc * gs;
-      if (from) {
-        hv += vt * c * gc + vt * sn * gs + 2.0 * vf * (k.gff * efp - k.bff * efq)
-            + wc * (c * dvt - vt * sn * dD) + ws * (sn * dvt + vt * c * dD);
-        hth += jth + hD;
-      } else {
-        hv += vf * c * gc + vf * sn * gs + 2.0 * vt * (k.gtt * etp - k.btt * etq)
-            + wc * (c * dvf - vf * sn * dD) + ws * (sn * dvf + vf * c * dD);
-        hth -= jth + hD;
+      const double* p = lb + (size_t)l * LB_N;
+      double h[6];
+      load_h(p, h);
+      const double hvv = from ? h[0] * dvf + h[1] * dvt + h[2] * dD : h[1] * dvf + h[3] * dvt + h[4] * dD;
+      double hD = h[2] * dvf + h[4] * dvt + h[5] * dD;
+      double hvo = hvv;
+      const int go = __ldg(n.bus_gen + o);
+      if (gi_own >= 0 || go >= 0) {  // Jᵀ μ_A: only lines touching an r bus
+        double J[12];
+        load_j(p, J);
+        const double mPo = go >= 0 ? MU[(2 * go) * C + lane] : 0.0;
+        const double mQo = go >= 0 ? MU[(2 * go + 1) * C + lane] : 0.0;
+        const double mpf = from ? mPi : mPo, mqf = from ? mQi : mQo;
+        const double mpt = from ? mPo : mPi, mqt = from ? mQo : mQi;
+        hvo += from ? J[0] * mpf + J[3] * mqf + J[6] * mpt + J[9] * mqt
+                    : J[1] * mpf + J[4] * mqf + J[7] * mpt + J[10] * mqt;
+        hD += J[2] * mpf + J[5] * mqf + J[8] * mpt + J[11] * mqt;
       }
+      hv += hvo;
+      hth += from ? hD : -hD;
     }
     const double vi = bs[BS_V * n_b + i];
-    hv += bs[BS_WD2 * n_b + i] * dvi + 2.0 * vi * (__ldg(n.gsh + i) * muP(i) - __ldg(n.bsh + i) * muQ(i));
+    hv += bs[BS_WD2 * n_b + i] * dvi + 2.0 * vi * (__ldg(n.gsh + i) * mPi - __ldg(n.bsh + i) * mQi);
     hv += bs[BS_SXV * n_b + i] * dvi;
     hth += bs[BS_SXT * n_b + i] * dthi;
     const int pt = __ldg(n.bus_pth + i), pv = __ldg(n.bus_pv + i);
