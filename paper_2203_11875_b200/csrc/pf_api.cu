@@ -155,7 +155,9 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
        alloc(h, S * d.nnz_lu, &w.luT) && alloc(h, S * d.nnz_lu, &w.pkA) && alloc(h, S * d.nnz_lu, &w.pkT) && alloc(h, S * d.n_x, &w.rowmax) && alloc(h, S * d.n_x, &w.invd) && alloc(h, S * LS_N * d.n_l, &w.ls) &&
        alloc(h, S * BS_N * d.n_b, &w.bs) && alloc(h, S * LB_N * d.n_l, &w.lblk) && alloc(h, S * 4 * d.n_l, &w.sflow) && alloc(h, 2 * S, &w.info) &&
        alloc(h, T * d.n_x * C, &w.slabZ) && alloc(h, T * d.n_x * C, &w.slabW) &&
-       alloc(h, T * d.n_u * C, &w.hu) && alloc(h, T * d.n_g * 2 * C, &w.mu);
+       alloc(h, T * d.n_u * C, &w.hu) && alloc(h, T * d.n_g * 2 * C, &w.mu) &&
+       alloc(h, S * (size_t)chol_part_slots(d.n_u) * 64 * 64, &w.cpart);
+  w.cpart_slots = chol_part_slots(d.n_u);
   if (!ok) {
     g_build_err = std::string("device allocation/upload failed: ") + cudaGetErrorString(cudaGetLastError());
     pf_destroy(h);
@@ -271,7 +273,7 @@ pf_status pf_condensed_kkt_solve(pf_net* h, int32_t n_scen, double* K, const dou
   if (!K || n_scen < 1 || nrhs < 0 || (nrhs > 0 && !rhs)) { h->err = "pf_condensed_kkt_solve: bad argument"; return PF_ERR_ARG; }
   if (n_scen > h->max_scen) { h->err = "pf_condensed_kkt_solve: n_scen > max_scen"; return PF_ERR_CAPACITY; }
   if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
-  h->launches += launch_chol(h->dn, n_scen, K, sigma_u, delta_w, rhs, nrhs, info, h->w.info + h->max_scen,
+  h->launches += launch_chol(h->dn, h->w, n_scen, K, sigma_u, delta_w, rhs, nrhs, info, h->w.info + h->max_scen,
                              (cudaStream_t)stream);
   return cuda_check(h, "pf_condensed_kkt_solve");
 }

@@ -65,15 +65,22 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N_>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N_)); }
 
-// A[I-tile, j-panel] −= L[I-tile, 0:j0] · L[j-panel, 0:j0]ᵀ for one 64×64 tile.
-// 4 warps × 32×32 outputs; K streamed in 32-wide chunks, 2 SMEM stages.
-__global__ void __launch_bounds__(128) k_chol_update(int n, int j0, double* __restrict__ K, const int* __restrict__ info) {
+// Split-K partial Gram products of the left-looking update:
+//   P[ks][t] = Σ_{k ∈ chunk range ks} L[j0 + 64t : +64, k] · L[j0 : j0+64, k]ᵀ
+// for the 64×64 tiles t of panel j (tile 0 is the diagonal block).  4 warps ×
+// 32×32 outputs, K streamed in 32-wide chunks through 2 cp.async SMEM stages.
+// The panel kernel subtracts Σ_ks P[ks][t] (fixed order: deterministic).
+__global__ void __launch_bounds__(128) k_chol_update(int n, int j0, int T, int KS, const double* __restrict__ K,
+                                                     double* __restrict__ part, int slots, const int* __restrict__ info) {
   const int s = blockIdx.y;
   if (info[s] != 0) return;
   extern __shared__ double sm_upd[];
-  double* A = K + (size_t)s * n * n;
+  const double* A = K + (size_t)s * n * n;
   const int nb = min(NB, n - j0);
-  const int I0 = j0 + blockIdx.x * NB;
+  const int tile = blockIdx.x % T, ks = blockIdx.x / T;
+  const int I0 = j0 + tile * NB;
+  const int nchunk = j0 / KC, per = (nchunk + KS - 1) / KS;
+  const int c0 = ks * per, c1 = min(nchunk, c0 + per);
   auto As = [&](int st) { return sm_upd + st * 2 * KC * LDT; };
   auto Bs = [&](int st) { return sm_upd + st * 2 * KC * LDT + KC * LDT; };
   auto load = [&](int st, int k0) {
@@ -95,14 +102,13 @@ __global__ void __launch_bounds__(128) k_chol_update(int n, int j0, double* __re
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) { acc[a][b][0] = 0.0; acc[a][b][1] = 0.0; }
-  const int nchunk = j0 / KC;
-  load(0, 0);
-  for (int c = 0; c < nchunk; ++c) {
-    if (c + 1 < nchunk) { load((c + 1) & 1, (c + 1) * KC); cp_wait<1>(); }
+  if (c0 < c1) load(0, c0 * KC);
+  for (int c = c0; c < c1; ++c) {
+    if (c + 1 < c1) { load((c + 1 - c0) & 1, (c + 1) * KC); cp_wait<1>(); }
     else cp_wait<0>();
     __syncthreads();
-    const double* a = As(c & 1);
-    const double* b = Bs(c & 1);
+    const double* a = As((c - c0) & 1);
+    const double* b = Bs((c - c0) & 1);
 #pragma unroll
     for (int kk = 0; kk < KC; kk += 4) {
       double af[4], bf[4];
@@ -117,53 +123,92 @@ __global__ void __launch_bounds__(128) k_chol_update(int n, int j0, double* __re
     }
     __syncthreads();
   }
+  double* P = part + ((size_t)s * slots + (size_t)ks * T + tile) * (NB * NB);
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int r = I0 + wr * 32 + mt * 8 + g;
+        const int r = wr * 32 + mt * 8 + g;
         const int c = wc * 32 + nt * 8 + 2 * q + h;
-        if (r < n && c < nb && r >= j0 + c) A[(size_t)(j0 + c) * n + r] -= acc[mt][nt][h];
+        P[c * NB + r] = acc[mt][nt][h];
       }
 }
 
-// Panel step: every CTA factors the 64×64 diagonal block in SMEM (CTA 0 writes
-// L_jj back and reports the first failing column in info), then solves its
-// 64-row block of the panel, X L_jjᵀ = A (4 lanes per row, shuffle-reduced).
-__global__ void __launch_bounds__(256) k_chol_panel(int n, int k0, double* __restrict__ K, int* __restrict__ info) {
+// Panel step.  Every CTA (a) loads the diagonal block minus its split-K
+// partials and factors it in SMEM as a 4×4 grid of 16×16 tiles (warp-level
+// 16×16 Cholesky, tile TRSM, tile SYRK: 12 CTA barriers instead of 3 per
+// column); CTA 0 writes L_jj back and reports the first failing column in
+// info; (b) loads its 64-row block of the panel minus partials and solves
+// X L_jjᵀ = A (4 lanes per row, shuffle-reduced dot products).
+__global__ void __launch_bounds__(256) k_chol_panel(int n, int k0, int T, int KS, double* __restrict__ K,
+                                                    const double* __restrict__ part, int slots, int* __restrict__ info) {
   const int s = blockIdx.y;
   if (info[s] != 0) return;
   extern __shared__ double smem_panel[];
   double (*L)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(smem_panel);
   double (*X)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(smem_panel + NB * (NB + 1));
+  __shared__ double invL[NB];
   __shared__ int fail;
-  __shared__ double inv_piv;
   double* A = K + (size_t)s * n * n;
   const int nb = min(NB, n - k0);
-  for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
-    const int c = idx / nb, r = idx % nb;
-    L[r][c] = r >= c ? A[(size_t)(k0 + c) * n + k0 + r] : 0.0;
+  const double* Ps = part + (size_t)s * slots * (NB * NB);
+  for (int idx = threadIdx.x; idx < NB * NB; idx += blockDim.x) {
+    const int c = idx / NB, r = idx % NB;
+    double v;
+    if (r < nb && c < nb) {
+      if (r >= c) {
+        v = A[(size_t)(k0 + c) * n + k0 + r];
+        for (int ks = 0; ks < KS; ++ks) v -= Ps[(size_t)(ks * T) * (NB * NB) + c * NB + r];
+      } else v = 0.0;
+    } else v = (r == c) ? 1.0 : 0.0;  // identity padding past the matrix edge
+    L[r][c] = v;
   }
   if (threadIdx.x == 0) fail = 0;
   __syncthreads();
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  for (int jj = 0; jj < nb; ++jj) {
-    if (threadIdx.x == 0) {
-      const double d = L[jj][jj];
-      if (!(d > 0.0) || !isfinite(d)) fail = k0 + jj + 1;
-      else { const double sq = sqrt(d); L[jj][jj] = sq; inv_piv = 1.0 / sq; }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = 0; t < 4; ++t) {
+    const int t0 = 16 * t;
+    if (warp == 0) {  // 16×16 diagonal tile, lane i < 16 owns row t0 + i
+      for (int j = 0; j < 16; ++j) {
+        const int J = t0 + j;
+        const double d = L[J][J];
+        if (!(d > 0.0) || !isfinite(d)) { if (lane == 0) fail = k0 + J + 1; break; }
+        const double piv = sqrt(d), inv = 1.0 / piv;
+        __syncwarp();
+        if (lane == j) { L[J][J] = piv; invL[J] = inv; }
+        if (lane > j && lane < 16) L[t0 + lane][J] *= inv;
+        __syncwarp();
+        if (lane > j && lane < 16) {
+          const int r = t0 + lane;
+          const double lr = L[r][J];
+          for (int c = J + 1; c <= r; ++c) L[r][c] -= lr * L[c][J];
+        }
+        __syncwarp();
+      }
     }
     __syncthreads();
     if (fail) break;
-    const double ip = inv_piv;
-    for (int r = jj + 1 + threadIdx.x; r < nb; r += blockDim.x) L[r][jj] *= ip;
-    __syncthreads();
-    for (int r = jj + 1 + ty; r < nb; r += 16) {
-      const double lr = L[r][jj];
-      for (int c = jj + 1 + tx; c <= r; c += 16) L[r][c] -= lr * L[c][jj];
+    // tile TRSM: rows below the tile, X L_ttᵀ = A
+    for (int r = t0 + 16 + threadIdx.x; r < NB; r += blockDim.x) {
+      for (int c = 0; c < 16; ++c) {
+        const int C = t0 + c;
+        double v = L[r][C];
+        for (int m = 0; m < c; ++m) v -= L[r][t0 + m] * L[C][t0 + m];
+        L[r][C] = v * invL[C];
+      }
     }
+    __syncthreads();
+    // tile SYRK on the trailing lower triangle
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    for (int r = t0 + 16 + ty; r < NB; r += 16)
+      for (int c = t0 + 16 + tx; c <= r; c += 16) {
+        double v = L[r][c];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) v -= L[r][t0 + m] * L[c][t0 + m];
+        L[r][c] = v;
+      }
     __syncthreads();
   }
   if (fail) {
@@ -179,16 +224,21 @@ __global__ void __launch_bounds__(256) k_chol_panel(int n, int k0, double* __res
   if (i0 >= n) return;
   for (int idx = threadIdx.x; idx < nb * NB; idx += blockDim.x) {
     const int c = idx / NB, r = idx % NB;
-    X[r][c] = (i0 + r < n) ? A[(size_t)(k0 + c) * n + i0 + r] : 0.0;
+    double v = 0.0;
+    if (i0 + r < n) {
+      v = A[(size_t)(k0 + c) * n + i0 + r];
+      for (int ks = 0; ks < KS; ++ks) v -= Ps[(size_t)(ks * T + blockIdx.x + 1) * (NB * NB) + c * NB + r];
+    }
+    X[r][c] = v;
   }
   __syncthreads();
   const int r = threadIdx.x >> 2, q = threadIdx.x & 3;
   for (int c = 0; c < nb; ++c) {
-    double part = 0.0;
-    for (int mm = q; mm < c; mm += 4) part += X[r][mm] * L[c][mm];
-    part += __shfl_xor_sync(0xffffffffu, part, 1);
-    part += __shfl_xor_sync(0xffffffffu, part, 2);
-    if (q == 0) X[r][c] = (X[r][c] - part) / L[c][c];
+    double p = 0.0;
+    for (int mm = q; mm < c; mm += 4) p += X[r][mm] * L[c][mm];
+    p += __shfl_xor_sync(0xffffffffu, p, 1);
+    p += __shfl_xor_sync(0xffffffffu, p, 2);
+    if (q == 0) X[r][c] = (X[r][c] - p) * invL[c];
     __syncwarp();
   }
   __syncthreads();
@@ -229,16 +279,19 @@ __global__ void __launch_bounds__(kSolveThreads) k_chol_solve(int n, const doubl
     for (int J = 0; J < nblk; ++J) {
       const int j0 = J * NB, nb = min(NB, n - j0);
       if (active && sub == J % P) {
+        for (int t = threadIdx.x; t < nb; t += blockDim.x) yb[t] = __ldcg(b + j0 + t);
         stage(j0, nb);
         if (warp == 0) {
           for (int j = 0; j < nb; ++j) {
-            const double yj = __ldcg(b + j0 + j) / D[j][j];
+            const double yj = yb[j] / D[j][j];
             __syncwarp();
-            if (lane == 0) __stcg(b + j0 + j, yj);
-            for (int i = j + 1 + lane; i < nb; i += 32) __stcg(b + j0 + i, __ldcg(b + j0 + i) - D[i][j] * yj);
+            if (lane == 0) yb[j] = yj;
+            for (int i = j + 1 + lane; i < nb; i += 32) yb[i] -= D[i][j] * yj;
             __syncwarp();
           }
         }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nb; t += blockDim.x) __stcg(b + j0 + t, yb[t]);
       }
       grid.sync();
       if (active) {
@@ -267,17 +320,20 @@ __global__ void __launch_bounds__(kSolveThreads) k_chol_solve(int n, const doubl
     for (int J = nblk - 1; J >= 0; --J) {
       const int j0 = J * NB, nb = min(NB, n - j0);
       if (active && sub == J % P) {
+        for (int t = threadIdx.x; t < nb; t += blockDim.x) yb[t] = __ldcg(b + j0 + t);
         stage(j0, nb);
         if (warp == 0) {
           for (int j = nb - 1; j >= 0; --j) {
             double acc = 0.0;
-            for (int i = j + 1 + lane; i < nb; i += 32) acc += D[i][j] * __ldcg(b + j0 + i);
+            for (int i = j + 1 + lane; i < nb; i += 32) acc += D[i][j] * yb[i];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) __stcg(b + j0 + j, (__ldcg(b + j0 + j) - acc) / D[j][j]);
+            if (lane == 0) yb[j] = (yb[j] - acc) / D[j][j];
             __syncwarp();
           }
         }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nb; t += blockDim.x) __stcg(b + j0 + t, yb[t]);
       }
       grid.sync();
       if (active) {
@@ -307,7 +363,9 @@ __global__ void k_info_out(int n_scen, const int* __restrict__ ws, int* __restri
 
 }  // namespace
 
-int launch_chol(const DevNet& net, int n_scen, double* K, const double* sigma_u, double delta_w,
+int chol_part_slots(int n_u) { return (n_u + NB - 1) / NB + 296; }
+
+int launch_chol(const DevNet& net, const Work& w, int n_scen, double* K, const double* sigma_u, double delta_w,
                 double* rhs, int nrhs, int* info, int* info_ws, cudaStream_t st) {
   const int n = net.n_u;
   int launches = 0;
@@ -327,14 +385,17 @@ int launch_chol(const DevNet& net, int n_scen, double* K, const double* sigma_u,
   ++launches;
   for (int j0 = 0; j0 < n; j0 += NB) {
     const int rows = n - j0;
-    const int T = (rows + NB - 1) / NB;
-    if (j0 > 0) {
-      k_chol_update<<<dim3(T, n_scen), 128, kUpdSmem, st>>>(n, j0, K, info_ws);
+    const int T = (rows + NB - 1) / NB;   // tiles of the panel, tile 0 = diagonal block
+    int KS = 0;
+    if (j0 > 0) {  // split K so that ~2 CTAs per SM work on every panel
+      const int nchunk = j0 / KC;
+      KS = std::max(1, std::min({(296 + T * n_scen - 1) / (T * n_scen), nchunk, 16}));
+      KS = std::min(KS, std::max(1, w.cpart_slots / T));
+      k_chol_update<<<dim3(T * KS, n_scen), 128, kUpdSmem, st>>>(n, j0, T, KS, K, w.cpart, w.cpart_slots, info_ws);
       ++launches;
     }
-    const int nb = std::min(NB, rows);
-    const int Tb = (rows - nb + NB - 1) / NB;
-    k_chol_panel<<<dim3(std::max(Tb, 1), n_scen), 256, kPanelSmem, st>>>(n, j0, K, info_ws);
+    k_chol_panel<<<dim3(std::max(T - 1, 1), n_scen), 256, kPanelSmem, st>>>(n, j0, T, KS, K, w.cpart,
+                                                                               w.cpart_slots, info_ws);
     ++launches;
   }
   if (nrhs > 0) {

@@ -57,6 +57,8 @@ struct Work {
   double* slabW;   // [max_tiles][n_x][C]
   double* hu;      // [max_tiles][n_u][C]
   double* mu;      // [max_tiles][n_gb][2][C]
+  double* cpart;   // Cholesky split-K partial sums: [max_scen][kCholSlots][64*64]
+  int cpart_slots; // tiles × K-splits per scenario that fit cpart
   int max_tiles;
 };
 

@@ -24,9 +24,10 @@ int launch_reduce(const DevNet& n, const Work& w, int C, int n_scen, const doubl
                   cudaEvent_t* ev = nullptr /* optional: [5] around k_fwd, k_mu, k_hvp, k_adj */);
 
 // A9: symmetrize + shift, blocked FP64 Cholesky (DMMA trailing update), solves.
-int launch_chol(const DevNet& n, int n_scen, double* K, const double* sigma_u, double delta_w,
+int launch_chol(const DevNet& n, const Work& w, int n_scen, double* K, const double* sigma_u, double delta_w,
                 double* rhs, int nrhs, int* info, int* info_ws, cudaStream_t st);
 
 int pick_tile_cols(int n_x, int n_scen_x_N);
+int chol_part_slots(int n_u);   // split-K partial tiles per scenario the Cholesky may use
 
 }  // namespace pf

@@ -18,6 +18,8 @@
 // so K̂ is bit-identical across batch sizes.
 #include "pf_launch.h"
 
+#include <cstdlib>
+
 namespace pf {
 
 namespace {
@@ -29,30 +31,77 @@ constexpr int kBusPerCta = 64; // buses per k_hvp CTA
 __device__ __forceinline__ double2 ldpk(const double2* p) { return __ldg(p); }
 __device__ __forceinline__ long long col_of(double2 q) { return __double_as_longlong(q.y); }
 
-// One row of a triangular sweep: acc = X[r] − Σ_{e∈[s,t)} v_e X[c_e], optionally
-// divided by the pivot.  Four independent accumulators keep ≥4 slab loads in flight.
-template <int C>
-__device__ __forceinline__ void sweep_row(const double2* __restrict__ pk, double* X, int r, int s, int t,
-                                          bool divide, int d, int lane) {
-  double a0 = X[r * C + lane], a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  for (; s + 3 < t; s += 4) {
-    const double2 p0 = ldpk(pk + s), p1 = ldpk(pk + s + 1), p2 = ldpk(pk + s + 2), p3 = ldpk(pk + s + 3);
-    a0 -= p0.x * X[col_of(p0) + lane];
-    a1 -= p1.x * X[col_of(p1) + lane];
-    a2 -= p2.x * X[col_of(p2) + lane];
-    a3 -= p3.x * X[col_of(p3) + lane];
+// One bus block of a triangular sweep, its one or two rows as independent
+// dot-product chains.  LOWER (L, Uᵀ: strict-lower part, forward): row r0 = θ,
+// row r0+1 = v depends on r0 only through its LAST lower entry (column r0),
+// which is applied after the other chain finishes.  Otherwise (U, Lᵀ:
+// strict-upper part, backward): row r0+1 first, row r0 depends on it through
+// its FIRST upper entry (column r0+1).
+struct Chain {
+  int s, t;       // remaining packed entries [s, t)
+  int row, d;     // row and its diagonal entry
+  double acc;
+};
+
+template <int C, bool LOWER>
+__device__ __forceinline__ void block_chains(const DevNet& n, const double2* __restrict__ pk, const double* X, int p,
+                                             int lane, Chain& c0, Chain& c1, bool& two) {
+  const int r0 = __ldg(n.blk_ptr + p);
+  two = __ldg(n.blk_ptr + p + 1) - r0 == 2;
+  const int4 m0 = __ldg(n.rowmeta + r0);
+  if (LOWER) {
+    c0.s = m0.x; c0.t = m0.y;
+  } else {
+    c0.s = m0.y + 1 + (two ? 1 : 0); c0.t = m0.z;  // θ row: skip its (θ, v) entry
   }
-  for (; s < t; ++s) {
-    const double2 p = ldpk(pk + s);
-    a0 -= p.x * X[col_of(p) + lane];
+  c0.row = r0; c0.d = m0.y; c0.acc = X[r0 * C + lane];
+  if (two) {
+    const int4 m1 = __ldg(n.rowmeta + r0 + 1);
+    if (LOWER) { c1.s = m1.x; c1.t = m1.y - 1; }   // v row: skip its (v, θ) entry
+    else { c1.s = m1.y + 1; c1.t = m1.z; }
+    c1.row = r0 + 1; c1.d = m1.y; c1.acc = X[(r0 + 1) * C + lane];
+  } else {
+    c1.s = c1.t = 0; c1.row = -1; c1.d = 0; c1.acc = 0.0;
   }
-  double acc = (a0 + a1) + (a2 + a3);
-  if (divide) acc /= ldpk(pk + d).x;
-  X[r * C + lane] = acc;
 }
 
-// LOWER: use row r's strict-lower part [ptr, diag) and walk the block's rows
-// forward (L, Uᵀ); otherwise the strict-upper part (diag, end), rows backward (U, Lᵀ).
+template <int C>
+__device__ __forceinline__ void chain_step(const double2* __restrict__ pk, const double* X, Chain& c, int lane) {
+  if (c.s < c.t) {
+    const double2 q = ldpk(pk + c.s);
+    c.acc -= q.x * X[col_of(q) + lane];
+    ++c.s;
+  }
+}
+
+template <int C, bool LOWER>
+__device__ __forceinline__ void block_finish(const double2* __restrict__ pk, double* X, bool divide, int lane,
+                                             Chain& c0, Chain& c1, bool two) {
+  if (LOWER) {
+    double x0 = c0.acc;
+    if (divide) x0 /= ldpk(pk + c0.d).x;
+    X[c0.row * C + lane] = x0;
+    if (two) {
+      double x1 = c1.acc - ldpk(pk + c1.t).x * x0;  // the (v, θ) entry
+      if (divide) x1 /= ldpk(pk + c1.d).x;
+      X[c1.row * C + lane] = x1;
+    }
+  } else {
+    double x1 = 0.0;
+    if (two) {
+      x1 = c1.acc;
+      if (divide) x1 /= ldpk(pk + c1.d).x;
+      X[c1.row * C + lane] = x1;
+    }
+    double x0 = c0.acc;
+    if (two) x0 -= ldpk(pk + c0.d + 1).x * x1;   // the (θ, v) entry
+    if (divide) x0 /= ldpk(pk + c0.d).x;
+    X[c0.row * C + lane] = x0;
+  }
+}
+
+// A level-scheduled sweep.  Each team takes two blocks of the level at a time,
+// so up to four independent row chains keep four slab loads in flight.
 template <int C, bool LOWER>
 __device__ __forceinline__ void sweep(const DevNet& n, const double2* __restrict__ pk, double* X, bool divide,
                                       int lane, int team, int nteam) {
@@ -61,20 +110,21 @@ __device__ __forceinline__ void sweep(const DevNet& n, const double2* __restrict
   const int* lblk = LOWER ? n.levL_blk : n.levU_blk;
   for (int lev = 0; lev < nlev; ++lev) {
     const int b1 = __ldg(lptr + lev + 1);
-    for (int bi = __ldg(lptr + lev) + team; bi < b1; bi += nteam) {
-      const int p = __ldg(lblk + bi);
-      const int r0 = __ldg(n.blk_ptr + p), r1 = __ldg(n.blk_ptr + p + 1);
-      if (LOWER) {
-        for (int r = r0; r < r1; ++r) {
-          const int4 m = __ldg(n.rowmeta + r);
-          sweep_row<C>(pk, X, r, m.x, m.y, divide, m.y, lane);
-        }
-      } else {
-        for (int r = r1 - 1; r >= r0; --r) {
-          const int4 m = __ldg(n.rowmeta + r);
-          sweep_row<C>(pk, X, r, m.y + 1, m.z, divide, m.y, lane);
-        }
+    for (int bi = __ldg(lptr + lev) + team; bi < b1; bi += 2 * nteam) {
+      Chain a0, a1, b0, b1c;
+      bool ta, tb = false;
+      block_chains<C, LOWER>(n, pk, X, __ldg(lblk + bi), lane, a0, a1, ta);
+      const bool hasB = bi + nteam < b1;
+      if (hasB) block_chains<C, LOWER>(n, pk, X, __ldg(lblk + bi + nteam), lane, b0, b1c, tb);
+      else { b0.s = b0.t = 0; b1c.s = b1c.t = 0; }
+      while (a0.s < a0.t || a1.s < a1.t || b0.s < b0.t || b1c.s < b1c.t) {
+        chain_step<C>(pk, X, a0, lane);
+        chain_step<C>(pk, X, a1, lane);
+        chain_step<C>(pk, X, b0, lane);
+        chain_step<C>(pk, X, b1c, lane);
       }
+      block_finish<C, LOWER>(pk, X, divide, lane, a0, a1, ta);
+      if (hasB) block_finish<C, LOWER>(pk, X, divide, lane, b0, b1c, tb);
     }
     __syncthreads();
   }
@@ -330,6 +380,10 @@ void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int
 }  // namespace
 
 int pick_tile_cols(int n_x, int total_cols) {
+  if (const char* e = getenv("PF_TILE_COLS")) {  // experiments: force 8 / 16 / 32
+    const int c = atoi(e);
+    if (c == 8 || c == 16 || c == 32) return c;
+  }
   // Enough CTAs to fill 148 SMs twice, wide tiles when the work allows.
   if (total_cols >= 32 * 296) return 32;
   if (total_cols >= 16 * 296) return 16;
