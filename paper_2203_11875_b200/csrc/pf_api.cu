@@ -128,6 +128,15 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
   for (int r = 0; r < P.n_x; ++r) rowmeta[r] = make_int4(P.lu_ptr[r], P.lu_diag[r], P.lu_ptr[r + 1], P.row_blk[r]);
   d.C = h->C;
   d.lu_maxlen = P.lu_maxlen;
+  std::vector<int4> inc_rec(2 * (size_t)n_l);
+  for (int i = 0; i < n_b; ++i)
+    for (int e = P.inc_ptr[i]; e < P.inc_ptr[i + 1]; ++e) {
+      const int l = P.inc_line[e];
+      const bool from = line_from[l] == i;
+      const int o = from ? line_to[l] : line_from[l];
+      inc_rec[e] = make_int4(l, P.bus_pth[o], P.bus_pv[o] >= 0 ? P.bus_pv[o] : -1 - P.u_v[o],
+                             (from ? 1 : 0) | ((P.bus_gen[o] + 1) << 1));
+    }
 
   bool ok = up(h, lf, &d.lf) && up(h, lt, &d.lt) && up(h, coef, &d.coef) && up(h, gsh, &d.gsh) &&
             up(h, bsh, &d.bsh) && up(h, gb, &d.gen_bus) && up(h, P.bus_gen, &d.bus_gen) &&
@@ -146,7 +155,8 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
             up(h, P.levU_blk, &d.levU_blk) && up(h, P.guc_ptr, &d.guc_ptr) && up(h, P.guc_row, &d.guc_row) &&
             up(h, P.guc_src, &d.guc_src) && up(h, P.gur_ptr, &d.gur_ptr) && up(h, P.gur_col, &d.gur_col) &&
             up(h, P.gur_src, &d.gur_src) && up(h, P.bus_pth, &d.bus_pth) && up(h, P.bus_pv, &d.bus_pv) &&
-            up(h, gbus, &d.gbus) && up(h, rowmeta, &d.rowmeta) && up(h, P.hvp_bus, &d.hvp_bus);
+            up(h, gbus, &d.gbus) && up(h, rowmeta, &d.rowmeta) && up(h, P.hvp_bus, &d.hvp_bus) &&
+            up(h, inc_rec, &d.inc_rec);
   Work& w = h->w;
   const size_t S = max_scen;
   w.max_tiles = max_scen * ((max_batch + h->C - 1) / h->C);

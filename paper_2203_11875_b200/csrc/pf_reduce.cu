@@ -12,8 +12,8 @@
 //          e. K̂V = H_u − (P G_u)ᵀ Ψ̃  (column gathers, SMEM-transposed store)
 // Slabs are [n_x][C] per tile, direction fastest: a team of C lanes handles
 // one row, lane j = direction j, so every slab access is one contiguous C×8 B
-// run.  Sweep nonzeros are packed {value, column·C} (one 16-byte load each)
-// and summed with four independent accumulators for memory-level parallelism.
+// run.  Sweep nonzeros are packed {value, column·C} (one 16-byte load each),
+// fetched lane-parallel and broadcast by shuffles (see sweep()).
 // Every column's arithmetic is independent of N, the tile and the GPU count,
 // so K̂ is bit-identical across batch sizes.
 #include "pf_launch.h"
@@ -27,81 +27,87 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kCH = 64;        // u-columns per transposed output chunk
 constexpr int kBusPerCta = 64; // buses per k_hvp CTA
+#ifndef PF_SWEEP_MIN_BLOCKS
+#define PF_SWEEP_MIN_BLOCKS 3
+#endif
+constexpr int kSweepMinBlocks = PF_SWEEP_MIN_BLOCKS;  // CTAs per SM the sweep kernels are register-capped for
 
 __device__ __forceinline__ double2 ldpk(const double2* p) { return __ldg(p); }
-__device__ __forceinline__ long long col_of(double2 q) { return __double_as_longlong(q.y); }
 
-// One bus block of a triangular sweep, its one or two rows as independent
-// dot-product chains.  LOWER (L, Uᵀ: strict-lower part, forward): row r0 = θ,
-// row r0+1 = v depends on r0 only through its LAST lower entry (column r0),
-// which is applied after the other chain finishes.  Otherwise (U, Lᵀ:
-// strict-upper part, backward): row r0+1 first, row r0 depends on it through
-// its FIRST upper entry (column r0+1).
-struct Chain {
-  int s, t;       // remaining packed entries [s, t)
-  int row, d;     // row and its diagonal entry
-  double acc;
-};
+// A level-scheduled triangular sweep over bus blocks (1–2 rows each).
+// LOWER (L, Uᵀ: strict-lower row parts, rows forward): row r0 = θ, row r0+1 = v
+// depends on r0 only through its LAST lower entry (column r0), applied after
+// r0 is final.  Otherwise (U, Lᵀ: strict-upper parts, rows backward): row
+// r0+1 first, row r0 depends on it through its FIRST upper entry (column r0+1).
+// Each team takes two blocks (≤ 4 row chains) at a time; the chains' packed
+// {value, column·C} entries are fetched lane-parallel (one coalesced load per
+// C entries) and broadcast by shuffles, so every slab load of the block is
+// independent and in flight together.
+struct Rows { int s0, n0, s1, n1, r0, d0, d1; bool two; };
 
-template <int C, bool LOWER>
-__device__ __forceinline__ void block_chains(const DevNet& n, const double2* __restrict__ pk, const double* X, int p,
-                                             int lane, Chain& c0, Chain& c1, bool& two) {
-  const int r0 = __ldg(n.blk_ptr + p);
-  two = __ldg(n.blk_ptr + p + 1) - r0 == 2;
-  const int4 m0 = __ldg(n.rowmeta + r0);
-  if (LOWER) {
-    c0.s = m0.x; c0.t = m0.y;
+template <bool LOWER>
+__device__ __forceinline__ Rows block_rows(const DevNet& n, int p) {
+  Rows b;
+  b.r0 = __ldg(n.blk_ptr + p);
+  b.two = __ldg(n.blk_ptr + p + 1) - b.r0 == 2;
+  const int4 m0 = __ldg(n.rowmeta + b.r0);
+  b.d0 = m0.y;
+  if (LOWER) { b.s0 = m0.x; b.n0 = m0.y - m0.x; }
+  else { b.s0 = m0.y + 1 + (b.two ? 1 : 0); b.n0 = m0.z - b.s0; }   // θ row: skip its (θ, v) entry
+  if (b.two) {
+    const int4 m1 = __ldg(n.rowmeta + b.r0 + 1);
+    b.d1 = m1.y;
+    if (LOWER) { b.s1 = m1.x; b.n1 = m1.y - 1 - m1.x; }              // v row: skip its (v, θ) entry
+    else { b.s1 = m1.y + 1; b.n1 = m1.z - b.s1; }
   } else {
-    c0.s = m0.y + 1 + (two ? 1 : 0); c0.t = m0.z;  // θ row: skip its (θ, v) entry
+    b.s1 = 0; b.n1 = 0; b.d1 = 0;
   }
-  c0.row = r0; c0.d = m0.y; c0.acc = X[r0 * C + lane];
-  if (two) {
-    const int4 m1 = __ldg(n.rowmeta + r0 + 1);
-    if (LOWER) { c1.s = m1.x; c1.t = m1.y - 1; }   // v row: skip its (v, θ) entry
-    else { c1.s = m1.y + 1; c1.t = m1.z; }
-    c1.row = r0 + 1; c1.d = m1.y; c1.acc = X[(r0 + 1) * C + lane];
-  } else {
-    c1.s = c1.t = 0; c1.row = -1; c1.d = 0; c1.acc = 0.0;
-  }
+  return b;
 }
 
 template <int C>
-__device__ __forceinline__ void chain_step(const double2* __restrict__ pk, const double* X, Chain& c, int lane) {
-  if (c.s < c.t) {
-    const double2 q = ldpk(pk + c.s);
-    c.acc -= q.x * X[col_of(q) + lane];
-    ++c.s;
+__device__ __forceinline__ double2 lane_entry(const double2* __restrict__ pk, int s, int cnt, int i) {
+  return i < cnt ? ldpk(pk + s + i) : make_double2(0.0, 0.0);
+}
+
+// acc -= Σ over the chunk's entries (value, column) held one per lane.
+template <int C>
+__device__ __forceinline__ void chunk_dot(const double* X, double2 q, int m, int lane, double& acc) {
+  const unsigned mask = 0xffffffffu;
+#pragma unroll 4
+  for (int e = 0; e < m; ++e) {
+    const double v = __shfl_sync(mask, q.x, e, C);
+    const long long c = __double_as_longlong(__shfl_sync(mask, q.y, e, C));
+    acc -= v * X[c + lane];
   }
 }
 
 template <int C, bool LOWER>
 __device__ __forceinline__ void block_finish(const double2* __restrict__ pk, double* X, bool divide, int lane,
-                                             Chain& c0, Chain& c1, bool two) {
+                                             const Rows& b, double acc0, double acc1) {
   if (LOWER) {
-    double x0 = c0.acc;
-    if (divide) x0 /= ldpk(pk + c0.d).x;
-    X[c0.row * C + lane] = x0;
-    if (two) {
-      double x1 = c1.acc - ldpk(pk + c1.t).x * x0;  // the (v, θ) entry
-      if (divide) x1 /= ldpk(pk + c1.d).x;
-      X[c1.row * C + lane] = x1;
+    double x0 = acc0;
+    if (divide) x0 /= ldpk(pk + b.d0).x;
+    X[b.r0 * C + lane] = x0;
+    if (b.two) {
+      double x1 = acc1 - ldpk(pk + b.s1 + b.n1).x * x0;  // the (v, θ) entry
+      if (divide) x1 /= ldpk(pk + b.d1).x;
+      X[(b.r0 + 1) * C + lane] = x1;
     }
   } else {
     double x1 = 0.0;
-    if (two) {
-      x1 = c1.acc;
-      if (divide) x1 /= ldpk(pk + c1.d).x;
-      X[c1.row * C + lane] = x1;
+    if (b.two) {
+      x1 = acc1;
+      if (divide) x1 /= ldpk(pk + b.d1).x;
+      X[(b.r0 + 1) * C + lane] = x1;
     }
-    double x0 = c0.acc;
-    if (two) x0 -= ldpk(pk + c0.d + 1).x * x1;   // the (θ, v) entry
-    if (divide) x0 /= ldpk(pk + c0.d).x;
-    X[c0.row * C + lane] = x0;
+    double x0 = acc0;
+    if (b.two) x0 -= ldpk(pk + b.d0 + 1).x * x1;   // the (θ, v) entry
+    if (divide) x0 /= ldpk(pk + b.d0).x;
+    X[b.r0 * C + lane] = x0;
   }
 }
 
-// A level-scheduled sweep.  Each team takes two blocks of the level at a time,
-// so up to four independent row chains keep four slab loads in flight.
 template <int C, bool LOWER>
 __device__ __forceinline__ void sweep(const DevNet& n, const double2* __restrict__ pk, double* X, bool divide,
                                       int lane, int team, int nteam) {
@@ -111,20 +117,25 @@ __device__ __forceinline__ void sweep(const DevNet& n, const double2* __restrict
   for (int lev = 0; lev < nlev; ++lev) {
     const int b1 = __ldg(lptr + lev + 1);
     for (int bi = __ldg(lptr + lev) + team; bi < b1; bi += 2 * nteam) {
-      Chain a0, a1, b0, b1c;
-      bool ta, tb = false;
-      block_chains<C, LOWER>(n, pk, X, __ldg(lblk + bi), lane, a0, a1, ta);
+      const Rows A = block_rows<LOWER>(n, __ldg(lblk + bi));
       const bool hasB = bi + nteam < b1;
-      if (hasB) block_chains<C, LOWER>(n, pk, X, __ldg(lblk + bi + nteam), lane, b0, b1c, tb);
-      else { b0.s = b0.t = 0; b1c.s = b1c.t = 0; }
-      while (a0.s < a0.t || a1.s < a1.t || b0.s < b0.t || b1c.s < b1c.t) {
-        chain_step<C>(pk, X, a0, lane);
-        chain_step<C>(pk, X, a1, lane);
-        chain_step<C>(pk, X, b0, lane);
-        chain_step<C>(pk, X, b1c, lane);
+      Rows B;
+      if (hasB) B = block_rows<LOWER>(n, __ldg(lblk + bi + nteam));
+      else { B.n0 = B.n1 = 0; B.s0 = B.s1 = 0; B.two = false; }
+      double a0 = X[A.r0 * C + lane], a1 = A.two ? X[(A.r0 + 1) * C + lane] : 0.0;
+      double c0 = hasB ? X[B.r0 * C + lane] : 0.0, c1 = (hasB && B.two) ? X[(B.r0 + 1) * C + lane] : 0.0;
+      const int mx = max(max(A.n0, A.n1), max(B.n0, B.n1));
+      for (int base = 0; base < mx; base += C) {
+        const int i = base + lane;
+        const double2 qa0 = lane_entry<C>(pk, A.s0, A.n0, i), qa1 = lane_entry<C>(pk, A.s1, A.n1, i);
+        const double2 qb0 = lane_entry<C>(pk, B.s0, B.n0, i), qb1 = lane_entry<C>(pk, B.s1, B.n1, i);
+        chunk_dot<C>(X, qa0, min(C, A.n0 - base), lane, a0);
+        chunk_dot<C>(X, qa1, min(C, A.n1 - base), lane, a1);
+        chunk_dot<C>(X, qb0, min(C, B.n0 - base), lane, c0);
+        chunk_dot<C>(X, qb1, min(C, B.n1 - base), lane, c1);
       }
-      block_finish<C, LOWER>(pk, X, divide, lane, a0, a1, ta);
-      if (hasB) block_finish<C, LOWER>(pk, X, divide, lane, b0, b1c, tb);
+      block_finish<C, LOWER>(pk, X, divide, lane, A, a0, a1);
+      if (hasB) block_finish<C, LOWER>(pk, X, divide, lane, B, c0, c1);
     }
     __syncthreads();
   }
@@ -132,7 +143,7 @@ __device__ __forceinline__ void sweep(const DevNet& n, const double2* __restrict
 
 // ---------------------------------------------------------------- a, b
 template <int C>
-__global__ void __launch_bounds__(kThreads, 4) k_fwd(DevNet n, Work w, const double* __restrict__ V, int col0, int N) {
+__global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Work w, const double* __restrict__ V, int col0, int N) {
   const int ntile = (N + C - 1) / C;
   const int tile = blockIdx.x, s = blockIdx.y;
   const size_t cta = (size_t)s * ntile + tile;
@@ -188,6 +199,16 @@ __device__ __forceinline__ double dv_of(const DevNet& n, const Dir& d, int i) {
   const int p = __ldg(n.bus_pv + i);
   return p >= 0 ? d.X[p * C + d.lane] : d.vdir(__ldg(n.u_v + i));
 }
+// Direction at the far end of an incidence record {line, θ row, v row or
+// −1−(u index), 1·from | 2·(gen + 1)} of the far bus (pf_api.cu builds them).
+template <int C>
+__device__ __forceinline__ double rec_dth(const Dir& d, int4 rec) {
+  return rec.y >= 0 ? d.X[rec.y * C + d.lane] : 0.0;
+}
+template <int C>
+__device__ __forceinline__ double rec_dv(const Dir& d, int4 rec) {
+  return rec.z >= 0 ? d.X[rec.z * C + d.lane] : d.vdir(-1 - rec.z);
+}
 
 template <int C>
 __device__ __forceinline__ Dir make_dir(const DevNet& n, const Work& w, const double* V, int col0, int N, int s,
@@ -235,10 +256,10 @@ __global__ void __launch_bounds__(kThreads) k_mu(DevNet n, Work w, const double*
   const double dvi = dv_of<C>(n, d, i), dthi = dth_of<C>(n, d, i);
   double dP = 0.0, dQ = 0.0;
   for (int e = __ldg(n.inc_ptr + i); e < __ldg(n.inc_ptr + i + 1); ++e) {
-    const int l = __ldg(n.inc_line + e);
-    const bool from = __ldg(n.lf + l) == i;
-    const int o = from ? __ldg(n.lt + l) : __ldg(n.lf + l);
-    const double dvo = dv_of<C>(n, d, o), dtho = dth_of<C>(n, d, o);
+    const int4 rec = __ldg(n.inc_rec + e);
+    const int l = rec.x;
+    const bool from = rec.w & 1;
+    const double dvo = rec_dv<C>(d, rec), dtho = rec_dth<C>(d, rec);
     const double dvf = from ? dvi : dvo, dvt = from ? dvo : dvi;
     const double dD = from ? dthi - dtho : dtho - dthi;
     double J[12];
@@ -283,11 +304,10 @@ __global__ void __launch_bounds__(kThreads) k_hvp(DevNet n, Work w, const double
     const double mQi = gi_own >= 0 ? MU[(2 * gi_own + 1) * C + lane] : 0.0;
     double hv = 0.0, hth = 0.0;
     for (int e = __ldg(n.inc_ptr + i); e < __ldg(n.inc_ptr + i + 1); ++e) {
-      const int l = __ldg(n.inc_line + e);
-      const int f = __ldg(n.lf + l), t = __ldg(n.lt + l);
-      const bool from = f == i;
-      const int o = from ? t : f;
-      const double dvo = dv_of<C>(n, d, o), dtho = dth_of<C>(n, d, o);
+      const int4 rec = __ldg(n.inc_rec + e);
+      const int l = rec.x;
+      const bool from = rec.w & 1;
+      const double dvo = rec_dv<C>(d, rec), dtho = rec_dth<C>(d, rec);
       const double dvf = from ? dvi : dvo, dvt = from ? dvo : dvi;
       const double dD = from ? dthi - dtho : dtho - dthi;
       const double* p = lb + (size_t)l * LB_N;
@@ -296,7 +316,7 @@ __global__ void __launch_bounds__(kThreads) k_hvp(DevNet n, Work w, const double
       const double hvv = from ? h[0] * dvf + h[1] * dvt + h[2] * dD : h[1] * dvf + h[3] * dvt + h[4] * dD;
       double hD = h[2] * dvf + h[4] * dvt + h[5] * dD;
       double hvo = hvv;
-      const int go = __ldg(n.bus_gen + o);
+      const int go = (rec.w >> 1) - 1;
       if (gi_own >= 0 || go >= 0) {  // Jᵀ μ_A: only lines touching an r bus
         double J[12];
         load_j(p, J);
@@ -329,7 +349,7 @@ __global__ void __launch_bounds__(kThreads) k_hvp(DevNet n, Work w, const double
 
 // ---------------------------------------------------------------- d, e
 template <int C>
-__global__ void __launch_bounds__(kThreads, 4) k_adj(DevNet n, Work w, int N, double* __restrict__ KV) {
+__global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_adj(DevNet n, Work w, int N, double* __restrict__ KV) {
   __shared__ double T[C][kCH + 1];
   const int ntile = (N + C - 1) / C;
   const int tile = blockIdx.x, s = blockIdx.y;

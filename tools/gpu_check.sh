@@ -9,3 +9,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${NCU_K:-k_fwd|k_hvp|k_adj}" -c ${NCU_C:-3} -f \
     -o gpurun_out/prof_reduce python bench.py --profile-steps 1 --delta-w 1e6 ${BENCH_ARGS} > gpurun_out/ncu_full.log 2>&1
 tail -3 gpurun_out/pytest_gpu.log; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_chol_panel|k_chol_update|k_chol_solve|k_lu" -s 40 -c 4 -f \
+    -o gpurun_out/prof_chol python bench.py --profile-steps 1 --delta-w 1e6 ${BENCH_ARGS} > gpurun_out/ncu_chol.log 2>&1
