@@ -70,15 +70,15 @@ __device__ __forceinline__ double2 lane_entry(const double2* __restrict__ pk, in
   return i < cnt ? ldpk(pk + s + i) : make_double2(0.0, 0.0);
 }
 
-// acc -= Σ over the chunk's entries (value, column) held one per lane.
+// The lanes of this thread's team (C consecutive lanes of the warp): teams of
+// one warp follow different rows, so every shuffle names only its own team.
 template <int C>
-__device__ __forceinline__ void chunk_dot(const double* X, double2 q, int m, int lane, double& acc) {
-  const unsigned mask = 0xffffffffu;
-#pragma unroll 4
-  for (int e = 0; e < m; ++e) {
-    const double v = __shfl_sync(mask, q.x, e, C);
-    const long long c = __double_as_longlong(__shfl_sync(mask, q.y, e, C));
-    acc -= v * X[c + lane];
+__device__ __forceinline__ unsigned team_mask() {
+  if constexpr (C == 32) {
+    return 0xffffffffu;
+  } else {
+    const unsigned lane = threadIdx.x & 31;
+    return ((1u << C) - 1u) << (lane & ~(unsigned)(C - 1));
   }
 }
 
@@ -114,28 +114,40 @@ __device__ __forceinline__ void sweep(const DevNet& n, const double2* __restrict
   const int nlev = LOWER ? n.nlevL : n.nlevU;
   const int* lptr = LOWER ? n.levL_ptr : n.levU_ptr;
   const int* lblk = LOWER ? n.levL_blk : n.levU_blk;
+  const unsigned mask = team_mask<C>();
   for (int lev = 0; lev < nlev; ++lev) {
     const int b1 = __ldg(lptr + lev + 1);
-    for (int bi = __ldg(lptr + lev) + team; bi < b1; bi += 2 * nteam) {
+    for (int bi = __ldg(lptr + lev) + team; bi < b1; bi += nteam) {
       const Rows A = block_rows<LOWER>(n, __ldg(lblk + bi));
-      const bool hasB = bi + nteam < b1;
-      Rows B;
-      if (hasB) B = block_rows<LOWER>(n, __ldg(lblk + bi + nteam));
-      else { B.n0 = B.n1 = 0; B.s0 = B.s1 = 0; B.two = false; }
       double a0 = X[A.r0 * C + lane], a1 = A.two ? X[(A.r0 + 1) * C + lane] : 0.0;
-      double c0 = hasB ? X[B.r0 * C + lane] : 0.0, c1 = (hasB && B.two) ? X[(B.r0 + 1) * C + lane] : 0.0;
-      const int mx = max(max(A.n0, A.n1), max(B.n0, B.n1));
+      const int mx = max(A.n0, A.n1);
       for (int base = 0; base < mx; base += C) {
-        const int i = base + lane;
-        const double2 qa0 = lane_entry<C>(pk, A.s0, A.n0, i), qa1 = lane_entry<C>(pk, A.s1, A.n1, i);
-        const double2 qb0 = lane_entry<C>(pk, B.s0, B.n0, i), qb1 = lane_entry<C>(pk, B.s1, B.n1, i);
-        chunk_dot<C>(X, qa0, min(C, A.n0 - base), lane, a0);
-        chunk_dot<C>(X, qa1, min(C, A.n1 - base), lane, a1);
-        chunk_dot<C>(X, qb0, min(C, B.n0 - base), lane, c0);
-        chunk_dot<C>(X, qb1, min(C, B.n1 - base), lane, c1);
+        // one coalesced fetch of up to C packed entries per row ...
+        const double2 q0 = lane_entry<C>(pk, A.s0, A.n0, base + lane);
+        const double2 q1 = lane_entry<C>(pk, A.s1, A.n1, base + lane);
+        const int m0 = min(C, A.n0 - base), m1 = min(C, A.n1 - base), m = max(m0, m1);
+        // ... then, 8 entries of both rows at a time: all 16 slab loads are
+        // issued before the first FMA (in-order issue would otherwise stall
+        // on each load in turn)
+        for (int e0 = 0; e0 < m; e0 += 8) {
+          double x0[8], x1[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int e = (e0 + k) & (C - 1);
+            const long long c0 = __double_as_longlong(__shfl_sync(mask, q0.y, e, C));
+            const long long c1 = __double_as_longlong(__shfl_sync(mask, q1.y, e, C));
+            x0[k] = e0 + k < m0 ? X[c0 + lane] : 0.0;
+            x1[k] = e0 + k < m1 ? X[c1 + lane] : 0.0;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int e = (e0 + k) & (C - 1);
+            a0 -= __shfl_sync(mask, q0.x, e, C) * x0[k];
+            a1 -= __shfl_sync(mask, q1.x, e, C) * x1[k];
+          }
+        }
       }
       block_finish<C, LOWER>(pk, X, divide, lane, A, a0, a1);
-      if (hasB) block_finish<C, LOWER>(pk, X, divide, lane, B, c0, c1);
     }
     __syncthreads();
   }
