@@ -128,6 +128,21 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
   for (int r = 0; r < P.n_x; ++r) rowmeta[r] = make_int4(P.lu_ptr[r], P.lu_diag[r], P.lu_ptr[r + 1], P.row_blk[r]);
   d.C = h->C;
   d.lu_maxlen = P.lu_maxlen;
+  // sweep tasks (pf_reduce.cu): each row's packed range includes its diagonal and intra-block entry
+  const int nblk = (int)P.blk_bus.size();
+  std::vector<int4> taskL(nblk), taskU(nblk);
+  for (int bi = 0; bi < nblk; ++bi) {
+    int p = P.levL_blk[bi], r0 = P.blk_ptr[p];
+    bool two = P.blk_ptr[p + 1] - r0 == 2;
+    int s0 = P.lu_ptr[r0], c0 = P.lu_diag[r0] - s0 + 1;
+    int s1 = two ? P.lu_ptr[r0 + 1] : 0, c1 = two ? P.lu_diag[r0 + 1] - s1 + 1 : 0;
+    taskL[bi] = make_int4(r0 | (two ? (int)0x80000000u : 0), s0, s1, (c0 << 16) | c1);
+    p = P.levU_blk[bi]; r0 = P.blk_ptr[p];
+    two = P.blk_ptr[p + 1] - r0 == 2;
+    s0 = P.lu_diag[r0]; c0 = P.lu_ptr[r0 + 1] - s0;
+    s1 = two ? P.lu_diag[r0 + 1] : 0; c1 = two ? P.lu_ptr[r0 + 2] - s1 : 0;
+    taskU[bi] = make_int4(r0 | (two ? (int)0x80000000u : 0), s0, s1, (c0 << 16) | c1);
+  }
   std::vector<int4> inc_rec(2 * (size_t)n_l);
   for (int i = 0; i < n_b; ++i)
     for (int e = P.inc_ptr[i]; e < P.inc_ptr[i + 1]; ++e) {
@@ -156,7 +171,7 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
             up(h, P.guc_src, &d.guc_src) && up(h, P.gur_ptr, &d.gur_ptr) && up(h, P.gur_col, &d.gur_col) &&
             up(h, P.gur_src, &d.gur_src) && up(h, P.bus_pth, &d.bus_pth) && up(h, P.bus_pv, &d.bus_pv) &&
             up(h, gbus, &d.gbus) && up(h, rowmeta, &d.rowmeta) && up(h, P.hvp_bus, &d.hvp_bus) &&
-            up(h, inc_rec, &d.inc_rec);
+            up(h, inc_rec, &d.inc_rec) && up(h, taskL, &d.taskL) && up(h, taskU, &d.taskU);
   Work& w = h->w;
   const size_t S = max_scen;
   w.max_tiles = max_scen * ((max_batch + h->C - 1) / h->C);

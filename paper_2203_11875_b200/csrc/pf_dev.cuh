@@ -27,6 +27,7 @@ struct DevNet {
   const int *gbus;              // [n_gb] generator buses ascending (the r buses)
   const int4 *rowmeta;          // [n_x] {lu_ptr[r], lu_diag[r], lu_ptr[r+1], block of r}
   const int *hvp_bus;           // [n_b] buses in elimination order, the reference bus last
+  const int4 *taskL, *taskU;    // [n_blocks] sweep tasks in level order (pf_reduce.cu sweep())
   const int4 *inc_rec;          // [2 n_l] per incidence: {line, far θ row, far v row | −1−u, from | 2(gen+1)}
   int C;                        // directions per tile (slab row width)
   int lu_maxlen;                // longest row of the filled LU pattern

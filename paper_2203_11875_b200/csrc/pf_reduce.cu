@@ -27,6 +27,9 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kCH = 64;        // u-columns per transposed output chunk
 constexpr int kBusPerCta = 64; // buses per k_hvp CTA
+#ifndef PF_DOT_W
+#define PF_DOT_W 4
+#endif
 #ifndef PF_SWEEP_MIN_BLOCKS
 #define PF_SWEEP_MIN_BLOCKS 3
 #endif
@@ -34,41 +37,22 @@ constexpr int kSweepMinBlocks = PF_SWEEP_MIN_BLOCKS;  // CTAs per SM the sweep k
 
 __device__ __forceinline__ double2 ldpk(const double2* p) { return __ldg(p); }
 
-// A level-scheduled triangular sweep over bus blocks (1–2 rows each).
-// LOWER (L, Uᵀ: strict-lower row parts, rows forward): row r0 = θ, row r0+1 = v
-// depends on r0 only through its LAST lower entry (column r0), applied after
-// r0 is final.  Otherwise (U, Lᵀ: strict-upper parts, rows backward): row
-// r0+1 first, row r0 depends on it through its FIRST upper entry (column r0+1).
-// Each team takes two blocks (≤ 4 row chains) at a time; the chains' packed
-// {value, column·C} entries are fetched lane-parallel (one coalesced load per
-// C entries) and broadcast by shuffles, so every slab load of the block is
-// independent and in flight together.
-struct Rows { int s0, n0, s1, n1, r0, d0, d1; bool two; };
-
-template <bool LOWER>
-__device__ __forceinline__ Rows block_rows(const DevNet& n, int p) {
-  Rows b;
-  b.r0 = __ldg(n.blk_ptr + p);
-  b.two = __ldg(n.blk_ptr + p + 1) - b.r0 == 2;
-  const int4 m0 = __ldg(n.rowmeta + b.r0);
-  b.d0 = m0.y;
-  if (LOWER) { b.s0 = m0.x; b.n0 = m0.y - m0.x; }
-  else { b.s0 = m0.y + 1 + (b.two ? 1 : 0); b.n0 = m0.z - b.s0; }   // θ row: skip its (θ, v) entry
-  if (b.two) {
-    const int4 m1 = __ldg(n.rowmeta + b.r0 + 1);
-    b.d1 = m1.y;
-    if (LOWER) { b.s1 = m1.x; b.n1 = m1.y - 1 - m1.x; }              // v row: skip its (v, θ) entry
-    else { b.s1 = m1.y + 1; b.n1 = m1.z - b.s1; }
-  } else {
-    b.s1 = 0; b.n1 = 0; b.d1 = 0;
-  }
-  return b;
-}
-
-template <int C>
-__device__ __forceinline__ double2 lane_entry(const double2* __restrict__ pk, int s, int cnt, int i) {
-  return i < cnt ? ldpk(pk + s + i) : make_double2(0.0, 0.0);
-}
+// A level-scheduled triangular sweep over bus blocks (1–2 rows each), driven
+// by a per-level task list built on the host (pf_api.cu, one int4 per block):
+//   {r0 | two << 31, start of row 0's entries, start of row 1's, cnt0 << 16 | cnt1}
+// where each row's packed {value, column·C} entries are ONE contiguous range
+// that includes its diagonal and the intra-block entry:
+//   LOWER (L, Uᵀ; strict-lower parts, rows forward):
+//     row 0 (θ): [lower part..., diag]    row 1 (v): [lower part..., (v,θ), diag]
+//   UPPER (U, Lᵀ; strict-upper parts, rows backward):
+//     row 1 (v): [diag, upper part...]    row 0 (θ): [diag, (θ,v), upper part...]
+// The v row of a LOWER block (θ row of an UPPER block) depends on its partner
+// only through the intra entry, applied once the partner is final.  A row's
+// range is fetched lane-parallel (one coalesced load) and broadcast by
+// shuffles; the next block's task and ranges are prefetched while the current
+// block's slab loads (16 at a time, all issued before the first FMA) are in
+// flight, so a block costs about one memory round trip.
+struct Task { int r0, s0, s1, c0, c1; bool two; };
 
 // The lanes of this thread's team (C consecutive lanes of the warp): teams of
 // one warp follow different rows, so every shuffle names only its own team.
@@ -81,73 +65,126 @@ __device__ __forceinline__ unsigned team_mask() {
     return ((1u << C) - 1u) << (lane & ~(unsigned)(C - 1));
   }
 }
+__device__ __forceinline__ Task unpack(int4 t) {
+  Task k;
+  k.r0 = t.x & 0x7fffffff; k.two = (t.x >> 31) & 1;
+  k.s0 = t.y; k.s1 = t.z; k.c0 = t.w >> 16; k.c1 = t.w & 0xffff;
+  return k;
+}
 
-template <int C, bool LOWER>
-__device__ __forceinline__ void block_finish(const double2* __restrict__ pk, double* X, bool divide, int lane,
-                                             const Rows& b, double acc0, double acc1) {
-  if (LOWER) {
-    double x0 = acc0;
-    if (divide) x0 /= ldpk(pk + b.d0).x;
-    X[b.r0 * C + lane] = x0;
-    if (b.two) {
-      double x1 = acc1 - ldpk(pk + b.s1 + b.n1).x * x0;  // the (v, θ) entry
-      if (divide) x1 /= ldpk(pk + b.d1).x;
-      X[(b.r0 + 1) * C + lane] = x1;
+template <int C>
+__device__ __forceinline__ double2 fetch(const double2* __restrict__ pk, int s, int cnt, int i) {
+  return i < cnt ? ldpk(pk + s + i) : make_double2(0.0, 0.0);
+}
+
+constexpr int kDotW = PF_DOT_W;  // slab loads per row issued before the FMAs
+
+template <int C>
+__device__ __forceinline__ double shv(unsigned mask, double2 q, int e) { return __shfl_sync(mask, q.x, e, C); }
+
+// acc0 -= Σ_{k<n0} v0[o0+k] X[c0[o0+k]],  acc1 likewise (entries held one per
+// lane in q0 / q1, all within one fetch of ≤ C entries).
+template <int C>
+__device__ __forceinline__ void dot2(const double* X, unsigned mask, int lane, double2 q0, int o0, int n0,
+                                     double2 q1, int o1, int n1, double& acc0, double& acc1) {
+  const int m = max(n0, n1);
+  for (int e0 = 0; e0 < m; e0 += kDotW) {
+    double x0[kDotW], x1[kDotW];
+#pragma unroll
+    for (int k = 0; k < kDotW; ++k) {
+      const int i0 = (o0 + e0 + k) & (C - 1), i1 = (o1 + e0 + k) & (C - 1);
+      const long long c0 = __double_as_longlong(__shfl_sync(mask, q0.y, i0, C));
+      const long long c1 = __double_as_longlong(__shfl_sync(mask, q1.y, i1, C));
+      x0[k] = e0 + k < n0 ? X[c0 + lane] : 0.0;
+      x1[k] = e0 + k < n1 ? X[c1 + lane] : 0.0;
     }
-  } else {
-    double x1 = 0.0;
-    if (b.two) {
-      x1 = acc1;
-      if (divide) x1 /= ldpk(pk + b.d1).x;
-      X[(b.r0 + 1) * C + lane] = x1;
+#pragma unroll
+    for (int k = 0; k < kDotW; ++k) {
+      const int i0 = (o0 + e0 + k) & (C - 1), i1 = (o1 + e0 + k) & (C - 1);
+      acc0 -= (e0 + k < n0 ? __shfl_sync(mask, q0.x, i0, C) : 0.0) * x0[k];
+      acc1 -= (e0 + k < n1 ? __shfl_sync(mask, q1.x, i1, C) : 0.0) * x1[k];
     }
-    double x0 = acc0;
-    if (b.two) x0 -= ldpk(pk + b.d0 + 1).x * x1;   // the (θ, v) entry
-    if (divide) x0 /= ldpk(pk + b.d0).x;
-    X[b.r0 * C + lane] = x0;
   }
 }
 
+// Rows longer than one fetch (separator rows of the L part): chunked, no prefetch.
+template <int C>
+__device__ __forceinline__ double dot_long(const double2* __restrict__ pk, const double* X, unsigned mask, int lane,
+                                           int s, int n) {
+  double acc = 0.0, dummy = 0.0;
+  for (int base = 0; base < n; base += C) {
+    const double2 q = fetch<C>(pk, s + base, n - base, lane);
+    dot2<C>(X, mask, lane, q, 0, min(C, n - base), q, 0, 0, acc, dummy);
+  }
+  return acc;
+}
+
 template <int C, bool LOWER>
-__device__ __forceinline__ void sweep(const DevNet& n, const double2* __restrict__ pk, double* X, bool divide,
-                                      int lane, int team, int nteam) {
+__device__ __forceinline__ void sweep(const DevNet& n, const int4* __restrict__ tasks, const double2* __restrict__ pk,
+                                      double* X, bool divide, int lane, int team, int nteam) {
   const int nlev = LOWER ? n.nlevL : n.nlevU;
   const int* lptr = LOWER ? n.levL_ptr : n.levU_ptr;
-  const int* lblk = LOWER ? n.levL_blk : n.levU_blk;
   const unsigned mask = team_mask<C>();
   for (int lev = 0; lev < nlev; ++lev) {
     const int b1 = __ldg(lptr + lev + 1);
-    for (int bi = __ldg(lptr + lev) + team; bi < b1; bi += nteam) {
-      const Rows A = block_rows<LOWER>(n, __ldg(lblk + bi));
-      double a0 = X[A.r0 * C + lane], a1 = A.two ? X[(A.r0 + 1) * C + lane] : 0.0;
-      const int mx = max(A.n0, A.n1);
-      for (int base = 0; base < mx; base += C) {
-        // one coalesced fetch of up to C packed entries per row ...
-        const double2 q0 = lane_entry<C>(pk, A.s0, A.n0, base + lane);
-        const double2 q1 = lane_entry<C>(pk, A.s1, A.n1, base + lane);
-        const int m0 = min(C, A.n0 - base), m1 = min(C, A.n1 - base), m = max(m0, m1);
-        // ... then, 8 entries of both rows at a time: all 16 slab loads are
-        // issued before the first FMA (in-order issue would otherwise stall
-        // on each load in turn)
-        for (int e0 = 0; e0 < m; e0 += 8) {
-          double x0[8], x1[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int e = (e0 + k) & (C - 1);
-            const long long c0 = __double_as_longlong(__shfl_sync(mask, q0.y, e, C));
-            const long long c1 = __double_as_longlong(__shfl_sync(mask, q1.y, e, C));
-            x0[k] = e0 + k < m0 ? X[c0 + lane] : 0.0;
-            x1[k] = e0 + k < m1 ? X[c1 + lane] : 0.0;
-          }
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int e = (e0 + k) & (C - 1);
-            a0 -= __shfl_sync(mask, q0.x, e, C) * x0[k];
-            a1 -= __shfl_sync(mask, q1.x, e, C) * x1[k];
-          }
-        }
+    int bi = __ldg(lptr + lev) + team;
+    Task nk;
+    double2 nq0 = make_double2(0.0, 0.0), nq1 = nq0;
+    if (bi < b1) {
+      nk = unpack(__ldg(tasks + bi));
+      nq0 = fetch<C>(pk, nk.s0, nk.c0, lane);
+      if (nk.two) nq1 = fetch<C>(pk, nk.s1, nk.c1, lane);
+    }
+    for (; bi < b1; bi += nteam) {
+      const Task k = nk;
+      const double2 q0 = nq0, q1 = nq1;
+      if (bi + nteam < b1) {  // prefetch the next block of this team
+        nk = unpack(__ldg(tasks + bi + nteam));
+        nq0 = fetch<C>(pk, nk.s0, nk.c0, lane);
+        if (nk.two) nq1 = fetch<C>(pk, nk.s1, nk.c1, lane);
       }
-      block_finish<C, LOWER>(pk, X, divide, lane, A, a0, a1);
+      double a0 = X[k.r0 * C + lane], a1 = k.two ? X[(k.r0 + 1) * C + lane] : 0.0;
+      if (LOWER) {
+        const int n0 = k.c0 - 1, n1 = k.two ? k.c1 - 2 : 0;      // entries before diag / intra
+        if (k.c0 <= C && k.c1 <= C) {
+          dot2<C>(X, mask, lane, q0, 0, n0, q1, 0, n1, a0, a1);
+        } else {
+          a0 -= dot_long<C>(pk, X, mask, lane, k.s0, n0);
+          if (k.two) a1 -= dot_long<C>(pk, X, mask, lane, k.s1, n1);
+        }
+        const double d0 = k.c0 <= C ? shv<C>(mask, q0, (k.c0 - 1) & (C - 1)) : ldpk(pk + k.s0 + k.c0 - 1).x;
+        double x0 = a0;
+        if (divide) x0 /= d0;
+        X[k.r0 * C + lane] = x0;
+        if (k.two) {
+          const bool in = k.c1 <= C;
+          const double intra = in ? shv<C>(mask, q1, (k.c1 - 2) & (C - 1)) : ldpk(pk + k.s1 + k.c1 - 2).x;
+          const double d1 = in ? shv<C>(mask, q1, (k.c1 - 1) & (C - 1)) : ldpk(pk + k.s1 + k.c1 - 1).x;
+          double x1 = a1 - intra * x0;
+          if (divide) x1 /= d1;
+          X[(k.r0 + 1) * C + lane] = x1;
+        }
+      } else {
+        // upper parts are short (≤ one fetch): row 1 = [diag, U...], row 0 = [diag, intra?, U...]
+        const int o0 = k.two ? 2 : 1;
+        const int n0 = k.c0 - o0, n1 = k.two ? k.c1 - 1 : 0;
+        if (k.c0 <= C && k.c1 <= C) {
+          dot2<C>(X, mask, lane, q0, o0, n0, q1, 1, n1, a0, a1);
+        } else {
+          a0 -= dot_long<C>(pk, X, mask, lane, k.s0 + o0, n0);
+          if (k.two) a1 -= dot_long<C>(pk, X, mask, lane, k.s1 + 1, n1);
+        }
+        double x1 = 0.0;
+        if (k.two) {
+          x1 = a1;
+          if (divide) x1 /= (k.c1 <= C ? shv<C>(mask, q1, 0) : ldpk(pk + k.s1).x);
+          X[(k.r0 + 1) * C + lane] = x1;
+        }
+        double x0 = a0;
+        if (k.two) x0 -= (k.c0 <= C ? shv<C>(mask, q0, 1) : ldpk(pk + k.s0 + 1).x) * x1;
+        if (divide) x0 /= (k.c0 <= C ? shv<C>(mask, q0, 0) : ldpk(pk + k.s0).x);
+        X[k.r0 * C + lane] = x0;
+      }
     }
     __syncthreads();
   }
@@ -185,8 +222,8 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
     }
   }
   __syncthreads();
-  sweep<C, true>(n, pk, X, false, lane, team, nteam);   // L^{-1}
-  sweep<C, false>(n, pk, X, true, lane, team, nteam);   // U^{-1}
+  sweep<C, true>(n, n.taskL, pk, X, false, lane, team, nteam);   // L^{-1}
+  sweep<C, false>(n, n.taskU, pk, X, true, lane, team, nteam);   // U^{-1}
 }
 
 // ---------------------------------------------------------------- directions in bus space
@@ -372,8 +409,8 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_adj(DevNet n, Wor
   const double* Hs = w.hu + cta * n_u * C;
   const double* gu = w.gu + (size_t)s * n.nnz_gu;
   const double2* pk = w.pkT + (size_t)s * n.nnz_lu;
-  sweep<C, true>(n, pk, Y, true, lane, team, nteam);    // U^{-T}
-  sweep<C, false>(n, pk, Y, false, lane, team, nteam);  // L^{-T}
+  sweep<C, true>(n, n.taskL, pk, Y, true, lane, team, nteam);    // U^{-T}
+  sweep<C, false>(n, n.taskU, pk, Y, false, lane, team, nteam);  // L^{-T}
   for (int c0 = 0; c0 < n_u; c0 += kCH) {
     for (int cc = team; cc < kCH && c0 + cc < n_u; cc += nteam) {
       const int c = c0 + cc;
