@@ -111,12 +111,12 @@ __device__ __forceinline__ void dot2(const double* X, unsigned mask, int lane, d
 template <int C>
 __device__ __forceinline__ double dot_long(const double2* __restrict__ pk, const double* X, unsigned mask, int lane,
                                            int s, int n) {
-  double acc = 0.0, dummy = 0.0;
+  double acc = 0.0, dummy = 0.0;  // dot2 subtracts: acc = −Σ, returned as +Σ
   for (int base = 0; base < n; base += C) {
     const double2 q = fetch<C>(pk, s + base, n - base, lane);
     dot2<C>(X, mask, lane, q, 0, min(C, n - base), q, 0, 0, acc, dummy);
   }
-  return acc;
+  return -acc;
 }
 
 template <int C, bool LOWER>
