@@ -8,10 +8,12 @@
 //   k_chol_update  A[j:, j] −= L[j:, :j] L[j, :j]ᵀ  — the O(n³) part, a deep-K
 //                  GEMM on the FP64 tensor pipe (mma.sync m8n8k4 f64 = SASS
 //                  DMMA.8x8x4; tcgen05 has no kind::f64), operands streamed
-//                  through a 2-stage cp.async SMEM pipeline; each panel tile
-//                  is written once.
-//   k_chol_panel   factor the 64×64 diagonal block in SMEM and solve the
-//                  panel rows below it (X L_jjᵀ = A).
+//                  through a 2-stage cp.async SMEM pipeline.  K is split so
+//                  that ~2 CTAs per SM work on every panel; the last CTA of a
+//                  tile (arrival counter) sums the split-K partials in fixed
+//                  order — deterministic — and writes the updated panel tile.
+//   k_chol_panel   factor the 64×64 diagonal block in SMEM (4×4 tiles of
+//                  16×16) and solve the panel rows below it (X L_jjᵀ = A).
 // k_chol_solve     forward/backward substitution, cooperative: the CTAs of a
 //                  scenario own 64-row blocks, one grid barrier per block.
 // Batched over scenarios; a scenario whose factorization failed (info ≠ 0)
@@ -32,25 +34,45 @@ constexpr int KC = 32;        // K chunk of the update GEMM
 constexpr int LDT = NB + 4;   // SMEM stride of the [k][row] operand tiles (conflict-free fragments)
 constexpr int kUpdSmem = 2 * 2 * KC * LDT * (int)sizeof(double);
 constexpr int kPanelSmem = 2 * NB * (NB + 1) * (int)sizeof(double);
+constexpr int TS = 32;        // symmetrize tile
 
-__global__ void k_chol_init(int n, int n_scen, double* __restrict__ K, const double* __restrict__ sig_u,
-                            double delta, int* __restrict__ info_ws) {
-  const long long total = (long long)n_scen * n * n;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int s = (int)(t / ((long long)n * n));
-    const long long rem = t % ((long long)n * n);
-    const int jc = (int)(rem / n), i = (int)(rem % n);  // column-major (row i, column jc)
-    double* A = K + (size_t)s * n * n;
-    if (i > jc) {
-      const double a = 0.5 * (A[(size_t)jc * n + i] + A[(size_t)i * n + jc]);
-      A[(size_t)jc * n + i] = a;
-      A[(size_t)i * n + jc] = 0.0;
-    } else if (i == jc) {
-      A[(size_t)jc * n + i] += (sig_u ? sig_u[(size_t)s * n + i] : 0.0) + delta;
-    }
-    if (rem == 0) info_ws[s] = 0;
+// sym + shift: lower ← (A + Aᵀ)/2 (+ Σ_u + δ_w on the diagonal), upper ← 0,
+// through 32×32 SMEM tiles so both the tile and its mirror are read coalesced.
+__global__ void __launch_bounds__(256) k_chol_sym(int n, double* __restrict__ K, const double* __restrict__ sig_u,
+                                                  double delta, int* __restrict__ info_ws) {
+  __shared__ double a[TS][TS + 1], b[TS][TS + 1];
+  const int s = blockIdx.y;
+  const int nt = (n + TS - 1) / TS;
+  int I = (int)((sqrt(8.0 * blockIdx.x + 1.0) - 1.0) * 0.5);  // lower tile (I ≥ J)
+  while ((I + 1) * (I + 2) / 2 <= (int)blockIdx.x) ++I;
+  while (I * (I + 1) / 2 > (int)blockIdx.x) --I;
+  const int J = blockIdx.x - I * (I + 1) / 2;
+  if (I >= nt) return;
+  double* A = K + (size_t)s * n * n;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 × 8
+  for (int c = ty; c < TS; c += 8) {
+    const int col = J * TS + c, row = I * TS + tx;           // tile (I, J): A[col][row] column-major
+    a[c][tx] = (row < n && col < n) ? A[(size_t)col * n + row] : 0.0;
+    const int col2 = I * TS + c, row2 = J * TS + tx;         // mirror tile (J, I)
+    b[c][tx] = (row2 < n && col2 < n) ? A[(size_t)col2 * n + row2] : 0.0;
   }
+  __syncthreads();
+  for (int c = ty; c < TS; c += 8) {
+    const int col = J * TS + c, row = I * TS + tx;
+    if (row < n && col < n) {
+      // element (row, col) of the lower triangle; its mirror (col, row) is b[tx][c]
+      double v;
+      if (row > col) v = 0.5 * (a[c][tx] + b[tx][c]);
+      else if (row == col) v = a[c][tx] + (sig_u ? sig_u[(size_t)s * n + row] : 0.0) + delta;
+      else v = 0.0;  // strict upper part of a diagonal tile
+      A[(size_t)col * n + row] = v;
+    }
+    if (I != J) {
+      const int col2 = I * TS + c, row2 = J * TS + tx;
+      if (row2 < n && col2 < n) A[(size_t)col2 * n + row2] = 0.0;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) info_ws[s] = 0;
 }
 
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
@@ -65,17 +87,20 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N_>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N_)); }
 
-// Split-K partial Gram products of the left-looking update:
-//   P[ks][t] = Σ_{k ∈ chunk range ks} L[j0 + 64t : +64, k] · L[j0 : j0+64, k]ᵀ
-// for the 64×64 tiles t of panel j (tile 0 is the diagonal block).  4 warps ×
-// 32×32 outputs, K streamed in 32-wide chunks through 2 cp.async SMEM stages.
-// The panel kernel subtracts Σ_ks P[ks][t] (fixed order: deterministic).
-__global__ void __launch_bounds__(128) k_chol_update(int n, int j0, int T, int KS, const double* __restrict__ K,
-                                                     double* __restrict__ part, int slots, const int* __restrict__ info) {
+// Split-K Gram products of the left-looking update for the 64×64 tiles t of
+// panel j (tile 0 = the diagonal block):
+//   P[ks][t] = Σ_{k ∈ chunk range ks} L[j0 + 64t : +64, k] · L[j0 : j0+64, k]ᵀ.
+// 4 warps × 32×32 outputs, K streamed in 32-wide chunks through 2 cp.async
+// SMEM stages.  KS = 1: the CTA writes A − P itself; otherwise each CTA stores
+// its partial and the last to arrive sums them in ks order (deterministic).
+__global__ void __launch_bounds__(128) k_chol_update(int n, int j0, int T, int KS, double* __restrict__ K,
+                                                     double* __restrict__ part, int slots, int* __restrict__ count,
+                                                     int cnt_stride, const int* __restrict__ info) {
   const int s = blockIdx.y;
   if (info[s] != 0) return;
   extern __shared__ double sm_upd[];
-  const double* A = K + (size_t)s * n * n;
+  __shared__ int last;
+  double* A = K + (size_t)s * n * n;
   const int nb = min(NB, n - j0);
   const int tile = blockIdx.x % T, ks = blockIdx.x / T;
   const int I0 = j0 + tile * NB;
@@ -123,6 +148,23 @@ __global__ void __launch_bounds__(128) k_chol_update(int n, int j0, int T, int K
     }
     __syncthreads();
   }
+  auto store_final = [&](int r, int c, double sub) {  // tile-local (r, c)
+    const int gr = I0 + r;
+    if (gr < n && c < nb && gr >= j0 + c) {
+      double* p = A + (size_t)(j0 + c) * n + gr;
+      *p = *p - sub;
+    }
+  };
+  if (KS == 1) {
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          store_final(wr * 32 + mt * 8 + g, wc * 32 + nt * 8 + 2 * q + h, acc[mt][nt][h]);
+    return;
+  }
   double* P = part + ((size_t)s * slots + (size_t)ks * T + tile) * (NB * NB);
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
@@ -130,20 +172,34 @@ __global__ void __launch_bounds__(128) k_chol_update(int n, int j0, int T, int K
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int r = wr * 32 + mt * 8 + g;
-        const int c = wc * 32 + nt * 8 + 2 * q + h;
-        P[c * NB + r] = acc[mt][nt][h];
+        const int r = wr * 32 + mt * 8 + g, c = wc * 32 + nt * 8 + 2 * q + h;
+        __stcg(P + c * NB + r, acc[mt][nt][h]);
       }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int* cnt = count + (size_t)s * cnt_stride + tile;
+    last = atomicAdd(cnt, 1) == KS - 1;
+    if (last) *cnt = 0;  // ready for the next panel / call
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const double* P0 = part + ((size_t)s * slots + tile) * (NB * NB);
+  for (int idx = threadIdx.x; idx < NB * NB; idx += blockDim.x) {
+    const int c = idx / NB, r = idx % NB;
+    double sum = 0.0;
+    for (int k = 0; k < KS; ++k) sum += __ldcg(P0 + (size_t)k * T * (NB * NB) + idx);
+    store_final(r, c, sum);
+  }
 }
 
-// Panel step.  Every CTA (a) loads the diagonal block minus its split-K
-// partials and factors it in SMEM as a 4×4 grid of 16×16 tiles (warp-level
-// 16×16 Cholesky, tile TRSM, tile SYRK: 12 CTA barriers instead of 3 per
-// column); CTA 0 writes L_jj back and reports the first failing column in
-// info; (b) loads its 64-row block of the panel minus partials and solves
-// X L_jjᵀ = A (4 lanes per row, shuffle-reduced dot products).
-__global__ void __launch_bounds__(256) k_chol_panel(int n, int k0, int T, int KS, double* __restrict__ K,
-                                                    const double* __restrict__ part, int slots, int* __restrict__ info) {
+// Panel step.  Every CTA factors the 64×64 diagonal block in SMEM as a 4×4
+// grid of 16×16 tiles (warp-level 16×16 Cholesky, tile TRSM, tile SYRK: 12 CTA
+// barriers instead of 3 per column); CTA 0 writes L_jj back and reports the
+// first failing column in info; then the CTA solves its 64-row block of the
+// panel, X L_jjᵀ = A (4 lanes per row, shuffle-reduced dot products).
+__global__ void __launch_bounds__(256) k_chol_panel(int n, int k0, double* __restrict__ K, int* __restrict__ info) {
   const int s = blockIdx.y;
   if (info[s] != 0) return;
   extern __shared__ double smem_panel[];
@@ -153,16 +209,11 @@ __global__ void __launch_bounds__(256) k_chol_panel(int n, int k0, int T, int KS
   __shared__ int fail;
   double* A = K + (size_t)s * n * n;
   const int nb = min(NB, n - k0);
-  const double* Ps = part + (size_t)s * slots * (NB * NB);
   for (int idx = threadIdx.x; idx < NB * NB; idx += blockDim.x) {
     const int c = idx / NB, r = idx % NB;
     double v;
-    if (r < nb && c < nb) {
-      if (r >= c) {
-        v = A[(size_t)(k0 + c) * n + k0 + r];
-        for (int ks = 0; ks < KS; ++ks) v -= Ps[(size_t)(ks * T) * (NB * NB) + c * NB + r];
-      } else v = 0.0;
-    } else v = (r == c) ? 1.0 : 0.0;  // identity padding past the matrix edge
+    if (r < nb && c < nb) v = r >= c ? A[(size_t)(k0 + c) * n + k0 + r] : 0.0;
+    else v = (r == c) ? 1.0 : 0.0;  // identity padding past the matrix edge
     L[r][c] = v;
   }
   if (threadIdx.x == 0) fail = 0;
@@ -224,12 +275,7 @@ __global__ void __launch_bounds__(256) k_chol_panel(int n, int k0, int T, int KS
   if (i0 >= n) return;
   for (int idx = threadIdx.x; idx < nb * NB; idx += blockDim.x) {
     const int c = idx / NB, r = idx % NB;
-    double v = 0.0;
-    if (i0 + r < n) {
-      v = A[(size_t)(k0 + c) * n + i0 + r];
-      for (int ks = 0; ks < KS; ++ks) v -= Ps[(size_t)(ks * T + blockIdx.x + 1) * (NB * NB) + c * NB + r];
-    }
-    X[r][c] = v;
+    X[r][c] = (i0 + r < n) ? A[(size_t)(k0 + c) * n + i0 + r] : 0.0;
   }
   __syncthreads();
   const int r = threadIdx.x >> 2, q = threadIdx.x & 3;
@@ -297,20 +343,21 @@ __global__ void __launch_bounds__(kSolveThreads) k_chol_solve(int n, const doubl
       if (active) {
         for (int t = threadIdx.x; t < nb; t += blockDim.x) yb[t] = __ldcg(b + j0 + t);
         __syncthreads();
+        // rows of the owned blocks I > J, 4 lanes per row (16 columns each)
+        const int q = threadIdx.x & 3;
         for (int I = J + 1 + ((sub - (J + 1)) % P + P) % P; I < nblk; I += P) {
           const int i0 = I * NB, ni = min(NB, n - i0);
-          for (int t = threadIdx.x; t < ni; t += blockDim.x) {
+          for (int t = threadIdx.x >> 2; t < ni; t += blockDim.x >> 2) {
             const int i = i0 + t;
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            int j = 0;
-            for (; j + 3 < nb; j += 4) {
+            double a0 = 0.0, a1 = 0.0;
+            for (int j = q; j < nb; j += 8) {
               a0 += L[(size_t)(j0 + j) * n + i] * yb[j];
-              a1 += L[(size_t)(j0 + j + 1) * n + i] * yb[j + 1];
-              a2 += L[(size_t)(j0 + j + 2) * n + i] * yb[j + 2];
-              a3 += L[(size_t)(j0 + j + 3) * n + i] * yb[j + 3];
+              if (j + 4 < nb) a1 += L[(size_t)(j0 + j + 4) * n + i] * yb[j + 4];
             }
-            for (; j < nb; ++j) a0 += L[(size_t)(j0 + j) * n + i] * yb[j];
-            __stcg(b + i, __ldcg(b + i) - ((a0 + a1) + (a2 + a3)));
+            double a = a0 + a1;
+            a += __shfl_xor_sync(0xffffffffu, a, 1);
+            a += __shfl_xor_sync(0xffffffffu, a, 2);
+            if (q == 0) __stcg(b + i, __ldcg(b + i) - a);
           }
         }
         __syncthreads();
@@ -379,23 +426,22 @@ int launch_chol(const DevNet& net, const Work& w, int n_scen, double* K, const d
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     solve_cap = std::max(1, per_sm) * sms;
   }
-  const long long tot = (long long)n_scen * n * n;
-  const int blocks = (int)std::min<long long>((tot + 255) / 256, 148LL * 32);
-  k_chol_init<<<blocks, 256, 0, st>>>(n, n_scen, K, sigma_u, delta_w, info_ws);
+  const int nts = (n + TS - 1) / TS;
+  k_chol_sym<<<dim3(nts * (nts + 1) / 2, n_scen), 256, 0, st>>>(n, K, sigma_u, delta_w, info_ws);
   ++launches;
+  const int cnt_stride = (n + NB - 1) / NB + 1;
   for (int j0 = 0; j0 < n; j0 += NB) {
     const int rows = n - j0;
     const int T = (rows + NB - 1) / NB;   // tiles of the panel, tile 0 = diagonal block
-    int KS = 0;
     if (j0 > 0) {  // split K so that ~2 CTAs per SM work on every panel
       const int nchunk = j0 / KC;
-      KS = std::max(1, std::min({(296 + T * n_scen - 1) / (T * n_scen), nchunk, 16}));
+      int KS = std::max(1, std::min({(296 + T * n_scen - 1) / (T * n_scen), nchunk, 16}));
       KS = std::min(KS, std::max(1, w.cpart_slots / T));
-      k_chol_update<<<dim3(T * KS, n_scen), 128, kUpdSmem, st>>>(n, j0, T, KS, K, w.cpart, w.cpart_slots, info_ws);
+      k_chol_update<<<dim3(T * KS, n_scen), 128, kUpdSmem, st>>>(n, j0, T, KS, K, w.cpart, w.cpart_slots,
+                                                                   w.ccount, cnt_stride, info_ws);
       ++launches;
     }
-    k_chol_panel<<<dim3(std::max(T - 1, 1), n_scen), 256, kPanelSmem, st>>>(n, j0, T, KS, K, w.cpart,
-                                                                               w.cpart_slots, info_ws);
+    k_chol_panel<<<dim3(std::max(T - 1, 1), n_scen), 256, kPanelSmem, st>>>(n, j0, K, info_ws);
     ++launches;
   }
   if (nrhs > 0) {

@@ -61,6 +61,7 @@ struct Work {
   double* mu;      // [max_tiles][n_gb][2][C]
   double* cpart;   // Cholesky split-K partial sums: [max_scen][kCholSlots][64*64]
   int cpart_slots; // tiles × K-splits per scenario that fit cpart
+  int* ccount;     // [max_scen][64-row tiles] split-K arrival counters (zero between calls)
   int max_tiles;
 };
 

@@ -18,6 +18,7 @@
 #include "pf_launch.h"
 
 #include <cstdlib>
+#include <type_traits>
 
 namespace pf {
 
@@ -133,9 +134,34 @@ __device__ __forceinline__ void dot_long(const double2* __restrict__ pk, const d
   }
 }
 
-template <int C, bool LOWER>
+// Initial row values of a sweep: the slab itself, or (first forward sweep) the
+// right-hand side B = −P G_u V computed on the fly from G_u's row, so the slab
+// needs no zero-fill pass.
+struct FromSlab {};
+template <int C>
+struct FromRhs {
+  const int* gur_ptr; const int* gur_col; const int* gur_src; const double* gu;
+  const double* Vs;  // dense V rows of this lane's first direction (stride n_u per W directions), or null = unit
+  int base, nvalid, n_u, lane;  // base = col0 + tile*C: the u column of direction 0 of the tile
+  __device__ __forceinline__ void operator()(int r, double* a) const {
+    constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) a[j] = 0.0;
+    for (int e = __ldg(gur_ptr + r); e < __ldg(gur_ptr + r + 1); ++e) {
+      const int c = __ldg(gur_col + e);
+      const double g = gu[__ldg(gur_src + e)];
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        const int jl = lane + W * j;
+        if (jl < nvalid) a[j] -= g * (Vs ? Vs[(size_t)W * j * n_u + c] : (c == base + jl ? 1.0 : 0.0));
+      }
+    }
+  }
+};
+
+template <int C, bool LOWER, class Init = FromSlab>
 __device__ __forceinline__ void sweep(const DevNet& n, const int4* __restrict__ tasks, const double2* __restrict__ pk,
-                                      double* X, bool divide, int lane, int team, int nteam) {
+                                      double* X, bool divide, int lane, int team, int nteam, Init init = Init()) {
   constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
   const int nlev = LOWER ? n.nlevL : n.nlevU;
   const int* lptr = LOWER ? n.levL_ptr : n.levU_ptr;
@@ -161,8 +187,18 @@ __device__ __forceinline__ void sweep(const DevNet& n, const int4* __restrict__ 
       double* x0p = X + (size_t)k.r0 * C + lane;
       double* x1p = x0p + C;
       double a0[CPL], a1[CPL];
+      if constexpr (std::is_same<Init, FromSlab>::value) {
 #pragma unroll
-      for (int j = 0; j < CPL; ++j) { a0[j] = x0p[W * j]; a1[j] = k.two ? x1p[W * j] : 0.0; }
+        for (int j = 0; j < CPL; ++j) { a0[j] = x0p[W * j]; a1[j] = k.two ? x1p[W * j] : 0.0; }
+      } else {
+        init(k.r0, a0);
+        if (k.two) {
+          init(k.r0 + 1, a1);
+        } else {
+#pragma unroll
+          for (int j = 0; j < CPL; ++j) a1[j] = 0.0;
+        }
+      }
       const bool fits = k.c0 <= W && k.c1 <= W;
       if (LOWER) {
         const int n0 = k.c0 - 1, n1 = k.two ? k.c1 - 2 : 0;      // entries before diag / intra
@@ -277,7 +313,7 @@ __device__ __forceinline__ void load_j(const double* p, double* j) {
 // ---------------------------------------------------------------- a, b
 template <int C>
 __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Work w, const double* __restrict__ V, int col0, int N) {
-  constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
+  constexpr int W = Geo<C>::W;
   const int ntile = (N + C - 1) / C;
   const int tile = blockIdx.x, s = blockIdx.y;
   const size_t cta = (size_t)s * ntile + tile;
@@ -287,31 +323,12 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
   double* X = w.slabZ + cta * n_x * C;
   const double* gu = w.gu + (size_t)s * n.nnz_gu;
   const double2* pk = w.pkA + (size_t)s * n.nnz_lu;
-  if (V == nullptr) {  // A7.1 for unit directions: a scatter of G_u's column col0 + j
-    for (size_t idx = threadIdx.x; idx < (size_t)n_x * C; idx += blockDim.x) X[idx] = 0.0;
-    __syncthreads();
-    for (int jl = threadIdx.x; jl < nvalid; jl += blockDim.x) {
-      const int c = col0 + tile * C + jl;
-      for (int e = __ldg(n.guc_ptr + c); e < __ldg(n.guc_ptr + c + 1); ++e)
-        X[(size_t)__ldg(n.guc_row + e) * C + jl] = -gu[__ldg(n.guc_src + e)];
-    }
-  } else {             // A7.1 for dense directions: B = −P G_u V (row SpMM)
-    for (int r = team; r < n_x; r += nteam) {
-#pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        const int jl = lane + W * j;
-        double acc = 0.0;
-        if (jl < nvalid) {
-          const double* Vs = V + ((size_t)s * N + tile * C + jl) * n_u;
-          for (int e = __ldg(n.gur_ptr + r); e < __ldg(n.gur_ptr + r + 1); ++e)
-            acc += gu[__ldg(n.gur_src + e)] * Vs[__ldg(n.gur_col + e)];
-        }
-        X[(size_t)r * C + jl] = -acc;
-      }
-    }
-  }
-  __syncthreads();
-  sweep<C, true>(n, n.taskL, pk, X, false, lane, team, nteam);   // L^{-1}
+  // A7.1 fused into the first sweep: B = −P G_u V row by row (unit V: G_u's column col0 + j)
+  FromRhs<C> rhs;
+  rhs.gur_ptr = n.gur_ptr; rhs.gur_col = n.gur_col; rhs.gur_src = n.gur_src; rhs.gu = gu;
+  rhs.Vs = V ? V + ((size_t)s * N + tile * C + lane) * n_u : nullptr;
+  rhs.base = col0 + tile * C; rhs.nvalid = nvalid; rhs.n_u = n_u; rhs.lane = lane;
+  sweep<C, true>(n, n.taskL, pk, X, false, lane, team, nteam, rhs);   // L^{-1} B
   sweep<C, false>(n, n.taskU, pk, X, true, lane, team, nteam);   // U^{-1}
 }
 
