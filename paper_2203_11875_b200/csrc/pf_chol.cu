@@ -347,17 +347,20 @@ __global__ void __launch_bounds__(kSolveThreads) k_chol_solve(int n, const doubl
         const int q = threadIdx.x & 3;
         for (int I = J + 1 + ((sub - (J + 1)) % P + P) % P; I < nblk; I += P) {
           const int i0 = I * NB, ni = min(NB, n - i0);
-          for (int t = threadIdx.x >> 2; t < ni; t += blockDim.x >> 2) {
+          // warp-uniform trip count: the shuffles below need all 32 lanes
+          for (int t0 = 0; t0 < ni; t0 += blockDim.x >> 2) {
+            const int t = t0 + (threadIdx.x >> 2);
             const int i = i0 + t;
             double a0 = 0.0, a1 = 0.0;
-            for (int j = q; j < nb; j += 8) {
-              a0 += L[(size_t)(j0 + j) * n + i] * yb[j];
-              if (j + 4 < nb) a1 += L[(size_t)(j0 + j + 4) * n + i] * yb[j + 4];
-            }
+            if (t < ni)
+              for (int j = q; j < nb; j += 8) {
+                a0 += L[(size_t)(j0 + j) * n + i] * yb[j];
+                if (j + 4 < nb) a1 += L[(size_t)(j0 + j + 4) * n + i] * yb[j + 4];
+              }
             double a = a0 + a1;
             a += __shfl_xor_sync(0xffffffffu, a, 1);
             a += __shfl_xor_sync(0xffffffffu, a, 2);
-            if (q == 0) __stcg(b + i, __ldcg(b + i) - a);
+            if (q == 0 && t < ni) __stcg(b + i, __ldcg(b + i) - a);
           }
         }
         __syncthreads();

@@ -238,105 +238,100 @@ __global__ void k_gather(DevNet n, Work w, int n_scen, double* __restrict__ Gx,
 
 // ---------------------------------------------------------------- A5
 // Numeric LU of P G_x Pᵀ with the fixed symbolic pattern and static pivots
-// (R18): up-looking IKJ rows, one warp per bus block, the blocks of one level
-// spread over all warps of the scenario's CTA group; a grid-wide barrier
-// (cooperative launch, all CTAs co-resident) separates levels.  Values
-// written by other SMs are read with ld.global.cg (L2), never a stale L1 line.
-constexpr int kLuThreads = 256;
+// (R18): up-looking IKJ rows, one warp per bus block (the row kept in a SMEM
+// workspace, the pivot rows' U parts and update targets prefetched one step
+// ahead), the blocks of one level spread over all warps of the scenario's
+// thread-block CLUSTER; a cluster barrier (≈0.2 µs, no grid-wide sync)
+// separates levels.  One cluster per scenario, so scenarios run independently.
+// Values written by other SMs of the cluster are read with ld.global.cg (L2).
+constexpr int kLuThreads = 512;
 
-__global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int n_scen, int P, int* __restrict__ info_out) {
-  cg::grid_group grid = cg::this_grid();
-  const int s = blockIdx.x / P, sub = blockIdx.x % P;
-  const bool active = s < n_scen;
-  double* lu = w.lu + (size_t)(active ? s : 0) * n.nnz_lu;
-  double* rowmax = w.rowmax + (size_t)(active ? s : 0) * n.n_x;
-  const double* jb = w.jb + (size_t)(active ? s : 0) * n.nnz_jb;
+__global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int CS) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int s = blockIdx.x / CS, sub = (int)cluster.block_rank();
+  double* lu = w.lu + (size_t)s * n.nnz_lu;
+  double* rowmax = w.rowmax + (size_t)s * n.n_x;
+  const double* jb = w.jb + (size_t)s * n.nnz_jb;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  const int gthread = sub * blockDim.x + threadIdx.x, nthread = P * blockDim.x;
-  const int gwarp = sub * nwarp + warp, ngwarp = P * nwarp;
-  if (active) {
-    if (gthread == 0) w.info[s] = INT_MAX;
-    for (int r = gthread; r < n.n_x; r += nthread) {
-      double mx = 0.0;
-      for (int e = __ldg(n.lu_ptr + r); e < __ldg(n.lu_ptr + r + 1); ++e) {
-        const int src = __ldg(n.lu_src + e);
-        const double val = src >= 0 ? jb[src] : 0.0;
-        __stcg(lu + e, val);
-        mx = fmax(mx, fabs(val));
-      }
-      rowmax[r] = mx;
+  const int gthread = sub * blockDim.x + threadIdx.x, nthread = CS * blockDim.x;
+  const int gwarp = sub * nwarp + warp, ngwarp = CS * nwarp;
+  if (gthread == 0) w.info[s] = INT_MAX;
+  for (int r = gthread; r < n.n_x; r += nthread) {
+    double mx = 0.0;
+    for (int e = __ldg(n.lu_ptr + r); e < __ldg(n.lu_ptr + r + 1); ++e) {
+      const int src = __ldg(n.lu_src + e);
+      const double val = src >= 0 ? jb[src] : 0.0;
+      __stcg(lu + e, val);
+      mx = fmax(mx, fabs(val));
     }
+    rowmax[r] = mx;
   }
-  grid.sync();
+  cluster.sync();
   extern __shared__ double lu_ws[];
   double* ws = lu_ws + warp * n.lu_maxlen;  // the warp's dense row workspace
-  double* invd = w.invd + (size_t)(active ? s : 0) * n.n_x;
+  double* invd = w.invd + (size_t)s * n.n_x;
   for (int lev = 0; lev < n.nlevL; ++lev) {
-    if (active) {
-      const int b0 = __ldg(n.levL_ptr + lev), b1 = __ldg(n.levL_ptr + lev + 1);
-      for (int bi = b0 + gwarp; bi < b1; bi += ngwarp) {
-        const int p = __ldg(n.levL_blk + bi);
-        for (int r = __ldg(n.blk_ptr + p); r < __ldg(n.blk_ptr + p + 1); ++r) {
-          const int base = __ldg(n.lu_ptr + r), len = __ldg(n.lu_ptr + r + 1) - base;
-          const int dl = __ldg(n.lu_diag + r) - base;
-          for (int a = lane; a < len; a += 32) ws[a] = __ldcg(lu + base + a);
-          __syncwarp();
-          // IKJ over the row's L entries; the U row of the next pivot is
-          // prefetched into registers while the current update runs.
-          double pu[4], pin = 0.0;
-          int pq0 = 0, pcnt = 0, pu0 = 0;
-          auto fetch = [&](int a) {
-            const int e = base + a, k = __ldg(n.lu_idx + e);
-            pu0 = __ldg(n.lu_diag + k) + 1;
-            pq0 = __ldg(n.upd_ptr + e);
-            pcnt = __ldg(n.upd_ptr + e + 1) - pq0;
-            pin = __ldcg(invd + k);
+    const int b0 = __ldg(n.levL_ptr + lev), b1 = __ldg(n.levL_ptr + lev + 1);
+    for (int bi = b0 + gwarp; bi < b1; bi += ngwarp) {
+      const int p = __ldg(n.levL_blk + bi);
+      for (int r = __ldg(n.blk_ptr + p); r < __ldg(n.blk_ptr + p + 1); ++r) {
+        const int base = __ldg(n.lu_ptr + r), len = __ldg(n.lu_ptr + r + 1) - base;
+        const int dl = __ldg(n.lu_diag + r) - base;
+        for (int a = lane; a < len; a += 32) ws[a] = __ldcg(lu + base + a);
+        __syncwarp();
+        // IKJ over the row's L entries; the U row of the next pivot and the
+        // update targets are prefetched into registers while this one runs.
+        double pu[4], pin = 0.0;
+        int pd[4], pq0 = 0, pcnt = 0, pu0 = 0;
+        auto fetch = [&](int a) {
+          const int e = base + a, k = __ldg(n.lu_idx + e);
+          pu0 = __ldg(n.lu_diag + k) + 1;
+          pq0 = __ldg(n.upd_ptr + e);
+          pcnt = __ldg(n.upd_ptr + e + 1) - pq0;
+          pin = __ldcg(invd + k);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int t = lane + 32 * j;
-              pu[j] = t < pcnt ? __ldcg(lu + pu0 + t) : 0.0;
-            }
-          };
-          if (dl > 0) fetch(0);
-          for (int a = 0; a < dl; ++a) {
-            double cu[4] = {pu[0], pu[1], pu[2], pu[3]};
-            const double cin = pin;
-            const int q0 = pq0, cnt = pcnt, u0 = pu0;
-            if (a + 1 < dl) fetch(a + 1);
-            const double l = ws[a] * cin;
+          for (int j = 0; j < 4; ++j) {
+            const int t = lane + 32 * j;
+            pu[j] = t < pcnt ? __ldcg(lu + pu0 + t) : 0.0;
+            pd[j] = t < pcnt ? __ldg(n.upd_dst + pq0 + t) : 0;
+          }
+        };
+        if (dl > 0) fetch(0);
+        for (int a = 0; a < dl; ++a) {
+          const double cu[4] = {pu[0], pu[1], pu[2], pu[3]};
+          const int cd[4] = {pd[0], pd[1], pd[2], pd[3]};
+          const double cin = pin;
+          const int q0 = pq0, cnt = pcnt, u0 = pu0;
+          if (a + 1 < dl) fetch(a + 1);
+          const double l = ws[a] * cin;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int t = lane + 32 * j;
-              if (t < cnt) ws[__ldg(n.upd_dst + q0 + t)] -= l * cu[j];
-            }
-            for (int t = lane + 128; t < cnt; t += 32) ws[__ldg(n.upd_dst + q0 + t)] -= l * __ldcg(lu + u0 + t);
-            __syncwarp();
-            if (lane == 0) ws[a] = l;
-          }
+          for (int j = 0; j < 4; ++j)
+            if (lane + 32 * j < cnt) ws[cd[j]] -= l * cu[j];
+          for (int t = lane + 128; t < cnt; t += 32) ws[__ldg(n.upd_dst + q0 + t)] -= l * __ldcg(lu + u0 + t);
           __syncwarp();
-          for (int a = lane; a < len; a += 32) __stcg(lu + base + a, ws[a]);
-          if (lane == 0) {
-            const double d = ws[dl];
-            __stcg(invd + r, 1.0 / d);
-            if (!(fabs(d) >= 1e-12 * rowmax[r]) || !isfinite(d) || d == 0.0) atomicMin(w.info + s, r + 1);
-          }
-          __syncwarp();
+          if (lane == 0) ws[a] = l;
         }
+        __syncwarp();
+        for (int a = lane; a < len; a += 32) __stcg(lu + base + a, ws[a]);
+        if (lane == 0) {
+          const double d = ws[dl];
+          __stcg(invd + r, 1.0 / d);
+          if (!(fabs(d) >= 1e-12 * rowmax[r]) || !isfinite(d) || d == 0.0) atomicMin(w.info + s, r + 1);
+        }
+        __syncwarp();
       }
     }
-    grid.sync();
+    cluster.sync();
   }
-  if (active) {
-    double* luT = w.luT + (size_t)s * n.nnz_lu;
-    double2* pkA = w.pkA + (size_t)s * n.nnz_lu;
-    double2* pkT = w.pkT + (size_t)s * n.nnz_lu;
-    for (int e = gthread; e < n.nnz_lu; e += nthread) {
-      const double t = __ldcg(lu + __ldg(n.lu_tpos + e));
-      const double c = __longlong_as_double((long long)__ldg(n.lu_idx + e) * n.C);
-      luT[e] = t;
-      pkA[e] = make_double2(__ldcg(lu + e), c);
-      pkT[e] = make_double2(t, c);
-    }
+  double* luT = w.luT + (size_t)s * n.nnz_lu;
+  double2* pkA = w.pkA + (size_t)s * n.nnz_lu;
+  double2* pkT = w.pkT + (size_t)s * n.nnz_lu;
+  for (int e = gthread; e < n.nnz_lu; e += nthread) {
+    const double t = __ldcg(lu + __ldg(n.lu_tpos + e));
+    const double c = __longlong_as_double((long long)__ldg(n.lu_idx + e) * n.C);
+    luT[e] = t;
+    pkA[e] = make_double2(__ldcg(lu + e), c);
+    pkT[e] = make_double2(t, c);
   }
 }
 
@@ -501,18 +496,32 @@ int launch_jacobian(const DevNet& n, const Work& w, int n_scen, const double* v,
   k_jbus<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen);
   k_gather<<<blocks_for((long long)n_scen * (n.nnz_gx + n.nnz_gu + n.nnz_a)), kThreads, 0, st>>>(n, w, n_scen, Gx, Gu, A);
   const size_t smem = (size_t)(kLuThreads / 32) * n.lu_maxlen * sizeof(double);
+  static int CS = 0;
+  if (!CS) {  // 16-CTA clusters (non-portable) when the part supports them, else 8
+    cudaFuncSetAttribute(k_lu, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int cs : {16, 8, 4, 2, 1}) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(cs); cfg.blockDim = dim3(kLuThreads); cfg.dynamicSmemBytes = smem;
+      cfg.attrs = at; cfg.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, (void*)k_lu, &cfg) == cudaSuccess && nc > 0) { CS = cs; break; }
+    }
+    cudaGetLastError();
+    if (!CS) CS = 1;
+  }
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 0, dev = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lu, kLuThreads, smem);
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int lu_grid = std::max(1, per_sm) * sms;
-  int P = std::max(1, lu_grid / n_scen);
-  int grid = P * n_scen;
-  if (grid > lu_grid) { P = 1; grid = n_scen; }  // more scenarios than co-resident CTAs: not supported cooperatively
-  void* args[] = {(void*)&n, (void*)&w, (void*)&n_scen, (void*)&P, (void*)&info};
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(n_scen * CS); cfg.blockDim = dim3(kLuThreads); cfg.dynamicSmemBytes = smem;
+  cfg.stream = st; cfg.attrs = at; cfg.numAttrs = 1;
   if (ev) cudaEventRecord(ev[0], st);
-  cudaLaunchCooperativeKernel((void*)k_lu, dim3(grid), dim3(kLuThreads), args, smem, st);
+  cudaLaunchKernelEx(&cfg, k_lu, n, w, CS);
   if (ev) cudaEventRecord(ev[1], st);
   k_lu_info<<<1, 256, 0, st>>>(n_scen, w.info, info);
   return 6;
