@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libpf.so")
+_LIB_PATH = os.environ.get("PF_LIB") or os.path.join(_HERE, "libpf.so")  # PF_LIB: experiment builds
 
 PF_OK, PF_ERR_ARG, PF_ERR_TOPOLOGY, PF_ERR_CAPACITY, PF_ERR_CUDA, PF_ERR_STATE = range(6)
 _STATUS = {1: "PF_ERR_ARG", 2: "PF_ERR_TOPOLOGY", 3: "PF_ERR_CAPACITY", 4: "PF_ERR_CUDA", 5: "PF_ERR_STATE"}

@@ -2,7 +2,7 @@
 # One GPU round-trip: parity tests (incl. full-size sampled), bench, ncu launch list + full captures.
 mkdir -p gpurun_out
 python -m paper_2203_11875_b200._build
-timeout 600 python -m pytest tests -m gpu -q -x -p pytest_timeout --timeout 150 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
+timeout 600 python -m pytest tests -m gpu -q -x --timeout 150 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
 timeout 300 python bench.py --steps ${STEPS:-5} --warmup 3 ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --profile-steps 1 --delta-w 1e6 ${BENCH_ARGS} > gpurun_out/ncu_launch.log 2>&1
