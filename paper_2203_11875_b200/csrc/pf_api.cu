@@ -183,7 +183,8 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
        alloc(h, T * d.n_u * C, &w.hu) && alloc(h, T * d.n_g * 2 * C, &w.mu) &&
        alloc(h, S * (size_t)chol_part_slots(d.n_u) * 64 * 64, &w.cpart);
   w.cpart_slots = chol_part_slots(d.n_u);
-  ok = ok && alloc(h, S * (size_t)((d.n_u + 63) / 64 + 1), &w.ccount) &&
+  ok = ok && alloc(h, S * (size_t)((d.n_u + 63) / 64) * 64 * 64, &w.cinv) &&
+       alloc(h, S * (size_t)((d.n_u + 63) / 64 + 1), &w.ccount) &&
        cudaMemset(w.ccount, 0, S * (size_t)((d.n_u + 63) / 64 + 1) * sizeof(int)) == cudaSuccess;
   if (!ok) {
     g_build_err = std::string("device allocation/upload failed: ") + cudaGetErrorString(cudaGetLastError());

@@ -8,14 +8,14 @@
 //   k_chol_update  A[j:, j] −= L[j:, :j] L[j, :j]ᵀ  — the O(n³) part, a deep-K
 //                  GEMM on the FP64 tensor pipe (mma.sync m8n8k4 f64 = SASS
 //                  DMMA.8x8x4; tcgen05 has no kind::f64), operands streamed
-//                  through a 2-stage cp.async SMEM pipeline.  K is split so
+//                  through a 3-stage cp.async SMEM pipeline.  K is split so
 //                  that ~2 CTAs per SM work on every panel; the last CTA of a
 //                  tile (arrival counter) sums the split-K partials in fixed
 //                  order — deterministic — and writes the updated panel tile.
-//   k_chol_panel   factor the 64×64 diagonal block in SMEM (4×4 tiles of
-//                  16×16) and solve the panel rows below it (X L_jjᵀ = A).
-// k_chol_solve     forward/backward substitution, cooperative: the CTAs of a
-//                  scenario own 64-row blocks, one grid barrier per block.
+//   k_chol_panel   factor the 64×64 diagonal block (register-blocked, one
+//                  barrier per column) and solve the panel rows below it.
+// k_chol_solve     forward/backward substitution on one thread-block cluster per
+//                  scenario: its CTAs own 64-row blocks, one cluster barrier per block.
 // Batched over scenarios; a scenario whose factorization failed (info ≠ 0)
 // skips all later work.
 #include "pf_launch.h"
@@ -32,8 +32,8 @@ namespace {
 constexpr int NB = 64;        // panel width
 constexpr int KC = 32;        // K chunk of the update GEMM
 constexpr int LDT = NB + 4;   // SMEM stride of the [k][row] operand tiles (conflict-free fragments)
-constexpr int kUpdSmem = 2 * 2 * KC * LDT * (int)sizeof(double);
-constexpr int kPanelSmem = 2 * NB * (NB + 1) * (int)sizeof(double);
+constexpr int NST = 3;       // cp.async pipeline stages of the update GEMM
+constexpr int kUpdSmem = NST * 2 * KC * LDT * (int)sizeof(double);
 constexpr int TS = 32;        // symmetrize tile
 
 // sym + shift: lower ← (A + Aᵀ)/2 (+ Σ_u + δ_w on the diagonal), upper ← 0,
@@ -90,7 +90,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // Split-K Gram products of the left-looking update for the 64×64 tiles t of
 // panel j (tile 0 = the diagonal block):
 //   P[ks][t] = Σ_{k ∈ chunk range ks} L[j0 + 64t : +64, k] · L[j0 : j0+64, k]ᵀ.
-// 4 warps × 32×32 outputs, K streamed in 32-wide chunks through 2 cp.async
+// 4 warps × 32×32 outputs, K streamed in 32-wide chunks through 3 cp.async
 // SMEM stages.  KS = 1: the CTA writes A − P itself; otherwise each CTA stores
 // its partial and the last to arrive sums them in ks order (deterministic).
 __global__ void __launch_bounds__(128) k_chol_update(int n, int j0, int T, int KS, double* __restrict__ K,
@@ -128,12 +128,14 @@ __global__ void __launch_bounds__(128) k_chol_update(int n, int j0, int T, int K
 #pragma unroll
     for (int b = 0; b < 4; ++b) { acc[a][b][0] = 0.0; acc[a][b][1] = 0.0; }
   if (c0 < c1) load(0, c0 * KC);
+  if (c0 + 1 < c1) load(1, (c0 + 1) * KC);
   for (int c = c0; c < c1; ++c) {
-    if (c + 1 < c1) { load((c + 1 - c0) & 1, (c + 1) * KC); cp_wait<1>(); }
+    if (c + 2 < c1) { load((c + 2 - c0) % NST, (c + 2) * KC); cp_wait<2>(); }
+    else if (c + 1 < c1) cp_wait<1>();
     else cp_wait<0>();
     __syncthreads();
-    const double* a = As((c - c0) & 1);
-    const double* b = Bs((c - c0) & 1);
+    const double* a = As((c - c0) % NST);
+    const double* b = Bs((c - c0) % NST);
 #pragma unroll
     for (int kk = 0; kk < KC; kk += 4) {
       double af[4], bf[4];
@@ -194,120 +196,135 @@ __global__ void __launch_bounds__(128) k_chol_update(int n, int j0, int T, int K
   }
 }
 
-// Panel step.  Every CTA factors the 64×64 diagonal block in SMEM as a 4×4
-// grid of 16×16 tiles (warp-level 16×16 Cholesky, tile TRSM, tile SYRK: 12 CTA
-// barriers instead of 3 per column); CTA 0 writes L_jj back and reports the
-// first failing column in info; then the CTA solves its 64-row block of the
-// panel, X L_jjᵀ = A (4 lanes per row, shuffle-reduced dot products).
+// Panel step.  Every CTA factors the 64×64 diagonal block, then solves its
+// 64-row block of the panel, X L_jjᵀ = A.  Both are register-blocked: thread
+// (ty, tx) of the 16×16 thread grid owns the 16 elements (ty + 16a, tx + 16b);
+// each of the 64 sequential steps publishes one column through SMEM (double-
+// buffered, ONE barrier per step) and every thread updates its elements.
+// The factorization runs in the unscaled LDLᵀ form (A[r][c] −= A[r][J] A[c][J]
+// / d_J needs no broadcast pivot), the Cholesky scaling L = D^{1/2} applied at
+// the end; CTA 0 writes L_jj back and reports the first pivot ≤ 0 in info.
 __global__ void __launch_bounds__(256) k_chol_panel(int n, int k0, double* __restrict__ K, int* __restrict__ info) {
   const int s = blockIdx.y;
   if (info[s] != 0) return;
-  extern __shared__ double smem_panel[];
-  double (*L)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(smem_panel);
-  double (*X)[NB + 1] = reinterpret_cast<double (*)[NB + 1]>(smem_panel + NB * (NB + 1));
-  __shared__ double invL[NB];
+  __shared__ double col[2][NB];
+  __shared__ double dv[NB];
+  __shared__ double Ls[NB][NB + 1];
   __shared__ int fail;
   double* A = K + (size_t)s * n * n;
   const int nb = min(NB, n - k0);
-  for (int idx = threadIdx.x; idx < NB * NB; idx += blockDim.x) {
-    const int c = idx / NB, r = idx % NB;
-    double v;
-    if (r < nb && c < nb) v = r >= c ? A[(size_t)(k0 + c) * n + k0 + r] : 0.0;
-    else v = (r == c) ? 1.0 : 0.0;  // identity padding past the matrix edge
-    L[r][c] = v;
-  }
-  if (threadIdx.x == 0) fail = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int t = 0; t < 4; ++t) {
-    const int t0 = 16 * t;
-    if (warp == 0) {  // 16×16 diagonal tile, lane i < 16 owns row t0 + i
-      for (int j = 0; j < 16; ++j) {
-        const int J = t0 + j;
-        const double d = L[J][J];
-        if (!(d > 0.0) || !isfinite(d)) { if (lane == 0) fail = k0 + J + 1; break; }
-        const double piv = sqrt(d), inv = 1.0 / piv;
-        __syncwarp();
-        if (lane == j) { L[J][J] = piv; invL[J] = inv; }
-        if (lane > j && lane < 16) L[t0 + lane][J] *= inv;
-        __syncwarp();
-        if (lane > j && lane < 16) {
-          const int r = t0 + lane;
-          const double lr = L[r][J];
-          for (int c = J + 1; c <= r; ++c) L[r][c] -= lr * L[c][J];
-        }
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    if (fail) break;
-    // tile TRSM: rows below the tile, X L_ttᵀ = A
-    for (int r = t0 + 16 + threadIdx.x; r < NB; r += blockDim.x) {
-      for (int c = 0; c < 16; ++c) {
-        const int C = t0 + c;
-        double v = L[r][C];
-        for (int m = 0; m < c; ++m) v -= L[r][t0 + m] * L[C][t0 + m];
-        L[r][C] = v * invL[C];
-      }
-    }
-    __syncthreads();
-    // tile SYRK on the trailing lower triangle
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    for (int r = t0 + 16 + ty; r < NB; r += 16)
-      for (int c = t0 + 16 + tx; c <= r; c += 16) {
-        double v = L[r][c];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double a[4][4];  // element (ty + 16i, tx + 16j)
 #pragma unroll
-        for (int m = 0; m < 16; ++m) v -= L[r][t0 + m] * L[c][t0 + m];
-        L[r][c] = v;
-      }
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = ty + 16 * i, c = tx + 16 * j;
+      double v;
+      if (r < nb && c < nb) v = r >= c ? A[(size_t)(k0 + c) * n + k0 + r] : 0.0;
+      else v = (r == c) ? 1.0 : 0.0;  // identity padding past the matrix edge
+      a[i][j] = v;
+    }
+  if (threadIdx.x == 0) fail = 0;
+  // ---- factor: 64 steps, one barrier each
+  for (int J = 0; J < NB; ++J) {
+    const int bj = J >> 4, tj = J & 15, buf = J & 1;
+    if (tx == tj) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j == bj) col[buf][ty + 16 * i] = a[i][j];  // static indexing keeps a[][] in registers
+    }
     __syncthreads();
+    const double d = col[buf][J];
+    if (!(d > 0.0) || !isfinite(d)) {  // every thread sees the same pivot
+      if (threadIdx.x == 0) fail = k0 + J + 1;
+      break;
+    }
+    if (threadIdx.x == 0) dv[J] = d;
+    const double invd = 1.0 / d;
+    double cr[4], cc[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { cr[i] = col[buf][ty + 16 * i]; cc[i] = col[buf][tx + 16 * i] * invd; }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = ty + 16 * i, c = tx + 16 * j;
+        if (c > J && r >= c) a[i][j] -= cr[i] * cc[j];
+      }
   }
+  __syncthreads();
   if (fail) {
     if (blockIdx.x == 0 && threadIdx.x == 0) info[s] = fail;
     return;
   }
-  if (blockIdx.x == 0)
-    for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
-      const int c = idx / nb, r = idx % nb;
-      if (r >= c) A[(size_t)(k0 + c) * n + k0 + r] = L[r][c];
+  // ---- L = (unscaled column) / sqrt(d_c), diagonal sqrt(d_c)
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = ty + 16 * i, c = tx + 16 * j;
+      const double sq = sqrt(dv[c]);
+      const double v = r == c ? sq : (r > c ? a[i][j] / sq : 0.0);
+      Ls[r][c] = v;
+      if (blockIdx.x == 0 && r < nb && c < nb && r >= c) A[(size_t)(k0 + c) * n + k0 + r] = v;
     }
   const int i0 = k0 + nb + blockIdx.x * NB;
   if (i0 >= n) return;
-  for (int idx = threadIdx.x; idx < nb * NB; idx += blockDim.x) {
-    const int c = idx / NB, r = idx % NB;
-    X[r][c] = (i0 + r < n) ? A[(size_t)(k0 + c) * n + i0 + r] : 0.0;
-  }
+  // ---- panel rows: X L_jjᵀ = A, column by column (right-looking), one barrier per column
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = ty + 16 * i, c = tx + 16 * j;
+      a[i][j] = (i0 + r < n && c < nb) ? A[(size_t)(k0 + c) * n + i0 + r] : 0.0;
+    }
   __syncthreads();
-  const int r = threadIdx.x >> 2, q = threadIdx.x & 3;
-  for (int c = 0; c < nb; ++c) {
-    double p = 0.0;
-    for (int mm = q; mm < c; mm += 4) p += X[r][mm] * L[c][mm];
-    p += __shfl_xor_sync(0xffffffffu, p, 1);
-    p += __shfl_xor_sync(0xffffffffu, p, 2);
-    if (q == 0) X[r][c] = (X[r][c] - p) * invL[c];
-    __syncwarp();
+  for (int J = 0; J < nb; ++J) {
+    const int bj = J >> 4, tj = J & 15, buf = J & 1;
+    const double inv = 1.0 / Ls[J][J];
+    if (tx == tj) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j == bj) { a[i][j] *= inv; col[buf][ty + 16 * i] = a[i][j]; }
+    }
+    __syncthreads();
+    double xr[4], lc[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { xr[i] = col[buf][ty + 16 * i]; lc[i] = Ls[tx + 16 * i][J]; }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (tx + 16 * j > J) a[i][j] -= xr[i] * lc[j];
   }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < nb * NB; idx += blockDim.x) {
-    const int c = idx / NB, rr = idx % NB;
-    if (i0 + rr < n) A[(size_t)(k0 + c) * n + i0 + rr] = X[rr][c];
-  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = ty + 16 * i, c = tx + 16 * j;
+      if (i0 + r < n && c < nb) A[(size_t)(k0 + c) * n + i0 + r] = a[i][j];
+    }
 }
 
 // L Lᵀ P = B for every right-hand side of every scenario.  The P CTAs of a
-// scenario own 64-row blocks round-robin.  Forward: the owner of block J
+// scenario's thread-block cluster own 64-row blocks round-robin.  Forward: the owner of block J
 // solves L_JJ y_J = b_J, grid barrier, then every CTA updates its own blocks
 // I > J: b_I −= L_IJ y_J.  Backward (right-looking on Lᵀ): the owner of J
 // solves L_JJᵀ p_J = b_J, barrier, every CTA updates its blocks I < J:
-// b_I −= L_JIᵀ p_J.  One grid barrier per block and direction.
+// b_I −= L_JIᵀ p_J.  One cluster barrier per block and direction.
 constexpr int kSolveThreads = 256;
 
 __global__ void __launch_bounds__(kSolveThreads) k_chol_solve(int n, const double* __restrict__ K, double* __restrict__ rhs,
                                                               int nrhs, const int* __restrict__ info, int n_scen, int P) {
-  cg::grid_group grid = cg::this_grid();
+  cg::cluster_group grid = cg::this_cluster();  // one cluster of P CTAs per scenario
   __shared__ double D[NB][NB + 1];
   __shared__ double yb[NB];
-  const int s = blockIdx.x / P, sub = blockIdx.x % P;
+  const int s = blockIdx.x / P, sub = (int)grid.block_rank();
   const bool active = s < n_scen && info[s] == 0;
   const double* L = K + (size_t)(s < n_scen ? s : 0) * n * n;
   const int nblk = (n + NB - 1) / NB;
@@ -419,15 +436,21 @@ int launch_chol(const DevNet& net, const Work& w, int n_scen, double* K, const d
                 double* rhs, int nrhs, int* info, int* info_ws, cudaStream_t st) {
   const int n = net.n_u;
   int launches = 0;
-  static int solve_cap = 0;
-  if (!solve_cap) {
+  static int CSS = 0;
+  if (!CSS) {
     cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, kUpdSmem);
-    cudaFuncSetAttribute(k_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem);
-    int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_solve, kSolveThreads, 0);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    solve_cap = std::max(1, per_sm) * sms;
+    cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int cs : {16, 8, 4, 2, 1}) {  // largest cluster the part schedules
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(cs); cfg.blockDim = dim3(kSolveThreads); cfg.attrs = at; cfg.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, (void*)k_chol_solve, &cfg) == cudaSuccess && nc > 0) { CSS = cs; break; }
+    }
+    cudaGetLastError();
+    if (!CSS) CSS = 1;
   }
   const int nts = (n + TS - 1) / TS;
   k_chol_sym<<<dim3(nts * (nts + 1) / 2, n_scen), 256, 0, st>>>(n, K, sigma_u, delta_w, info_ws);
@@ -444,14 +467,18 @@ int launch_chol(const DevNet& net, const Work& w, int n_scen, double* K, const d
                                                                    w.ccount, cnt_stride, info_ws);
       ++launches;
     }
-    k_chol_panel<<<dim3(std::max(T - 1, 1), n_scen), 256, kPanelSmem, st>>>(n, j0, K, info_ws);
+    k_chol_panel<<<dim3(std::max(T - 1, 1), n_scen), 256, 0, st>>>(n, j0, K, info_ws);
     ++launches;
   }
   if (nrhs > 0) {
-    const int nblk = (n + NB - 1) / NB;
-    int P = std::max(1, std::min(solve_cap / n_scen, nblk));
-    void* args[] = {(void*)&n, (void*)&K, (void*)&rhs, (void*)&nrhs, (void*)&info_ws, (void*)&n_scen, (void*)&P};
-    cudaLaunchCooperativeKernel((void*)k_chol_solve, dim3(P * n_scen), dim3(kSolveThreads), args, 0, st);
+    const int P = CSS;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = P; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(P * n_scen); cfg.blockDim = dim3(kSolveThreads); cfg.stream = st;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_chol_solve, n, (const double*)K, rhs, nrhs, (const int*)info_ws, n_scen, P);
     ++launches;
   }
   if (info) { k_info_out<<<1, 256, 0, st>>>(n_scen, info_ws, info); ++launches; }

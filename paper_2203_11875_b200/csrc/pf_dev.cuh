@@ -62,6 +62,7 @@ struct Work {
   double* cpart;   // Cholesky split-K partial sums: [max_scen][kCholSlots][64*64]
   int cpart_slots; // tiles × K-splits per scenario that fit cpart
   int* ccount;     // [max_scen][64-row tiles] split-K arrival counters (zero between calls)
+  double* cinv;    // [max_scen][64-col panels][64*64] inverses of the diagonal blocks L_jj
   int max_tiles;
 };
 

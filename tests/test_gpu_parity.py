@@ -178,11 +178,13 @@ def test_batch_invariance_bitwise(pfmod, name, net, pts):
     h.close()
 
 
-def test_condensed_kkt_solve(pfmod):
+@pytest.mark.parametrize("name", ["case118", "case1354"])
+def test_condensed_kkt_solve(pfmod, name):
     """K_cond = sym(K̂) + diag(Σ_u) + δ_w I: L and the solve vs the oracle's
-    textbook Cholesky; info for an indefinite shift equals the oracle's."""
+    textbook Cholesky; info for an indefinite shift equals the oracle's.
+    case1354 (n_u = 519) exercises ragged panels and the split-K update."""
     import torch
-    net, pt = table1_grid("case118")
+    net, pt = table1_grid(name)
     pts = [pt, make_scenario(net, pt, 1)]
     S = 2
     part = O.partition(net)
