@@ -181,11 +181,8 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
        alloc(h, S * BS_N * d.n_b, &w.bs) && alloc(h, S * LB_N * d.n_l, &w.lblk) && alloc(h, S * 4 * d.n_l, &w.sflow) && alloc(h, 2 * S, &w.info) &&
        alloc(h, T * d.n_x * C, &w.slabZ) && alloc(h, T * d.n_x * C, &w.slabW) &&
        alloc(h, T * d.n_u * C, &w.hu) && alloc(h, T * d.n_g * 2 * C, &w.mu) &&
-       alloc(h, S * (size_t)chol_part_slots(d.n_u) * 64 * 64, &w.cpart);
-  w.cpart_slots = chol_part_slots(d.n_u);
-  ok = ok && alloc(h, S * (size_t)((d.n_u + 63) / 64) * 64 * 64, &w.cinv) &&
-       alloc(h, S * (size_t)((d.n_u + 63) / 64 + 1), &w.ccount) &&
-       cudaMemset(w.ccount, 0, S * (size_t)((d.n_u + 63) / 64 + 1) * sizeof(int)) == cudaSuccess;
+       alloc(h, S * chol_tile_doubles(d.n_u), &w.ctile) && alloc(h, S * chol_flag_ints(d.n_u), &w.cflag) &&
+       alloc(h, 1, &w.cticket) && alloc(h, S * chol_vec_doubles(d.n_u), &w.cy);
   if (!ok) {
     g_build_err = std::string("device allocation/upload failed: ") + cudaGetErrorString(cudaGetLastError());
     pf_destroy(h);

@@ -1,426 +1,690 @@
 // pf_chol.cu — condensed-KKT factor + solve (A9 of SURVEY §8(a)):
 // K_cond = sym(K̂) + diag(Σ_u) + δ_w I (Theorem 2 with R9, P:L784–787;
-// δ_w regularisation P:L1341–1342), blocked FP64 Cholesky (the role of
+// δ_w regularisation P:L1341–1342), FP64 Cholesky K_cond = L Lᵀ (the role of
 // cusolver's potrf in P:L1339–1341; success certifies the inertia, Theorem 3
 // P:L856–866) and the solve L Lᵀ p = b.
 //
-// Left-looking blocked algorithm, 64-column panels, per panel j:
-//   k_chol_update  A[j:, j] −= L[j:, :j] L[j, :j]ᵀ  — the O(n³) part, a deep-K
-//                  GEMM on the FP64 tensor pipe (mma.sync m8n8k4 f64 = SASS
-//                  DMMA.8x8x4; tcgen05 has no kind::f64), operands streamed
-//                  through a 3-stage cp.async SMEM pipeline.  K is split so
-//                  that ~2 CTAs per SM work on every panel; the last CTA of a
-//                  tile (arrival counter) sums the split-K partials in fixed
-//                  order — deterministic — and writes the updated panel tile.
-//   k_chol_panel   factor the 64×64 diagonal block (register-blocked, one
-//                  barrier per column) and solve the panel rows below it.
-// k_chol_solve     forward/backward substitution on one thread-block cluster per
-//                  scenario: its CTAs own 64-row blocks, one cluster barrier per block.
-// Batched over scenarios; a scenario whose factorization failed (info ≠ 0)
-// skips all later work.
+// Tile algorithm on 64×64 tiles, run as ONE persistent, dependency-driven
+// kernel (k_chol_dag) over every scenario at once:
+//   k_chol_pack    symmetrize + shift K̂ into packed lower tiles (column-major
+//                  inside a tile, leading dimension 68 so DMMA fragment loads
+//                  are bank-conflict free and a tile half is one contiguous
+//                  16-byte-aligned run); padding past n is the identity.
+//   k_chol_dag     CTAs take tasks from a ticket counter in a topological order
+//                  (column by column, all scenarios interleaved) and wait on
+//                  per-tile ready flags (release/acquire):
+//     tile (i, j)  C = A_ij − Σ_{k<j} L_ik L_jkᵀ  (left-looking; DMMA m8n8k4 f64 —
+//                  tcgen05 has no kind::f64 — operands streamed by cp.async.bulk
+//                  through a 3-stage mbarrier ring), then
+//                  i = j: L_jj = chol(C)  (unscaled LDLᵀ, one row per thread, info);
+//                  i > j: L_ij = C L_jj^{-T} (4 threads per row, no barriers).
+//     fwd j        y_j = L_jj^{-1}(b_j − Σ_{k<j} L_jk y_k)   (runs during the factorization)
+//     bwd j        p_j = L_jj^{-T}(y_j − Σ_{i>j} L_ijᵀ p_i)
+//   k_chol_unpack  L back into K (column-major, strict upper zeroed).
+// The critical path is ~3 short tile steps per block column, instead of one
+// launch-separated panel per column; every tile's arithmetic order is fixed,
+// so the result is deterministic and independent of the schedule.
 #include "pf_launch.h"
 
 #include <algorithm>
-#include <cooperative_groups.h>
-
-namespace cg = cooperative_groups;
+#include <cstdint>
 
 namespace pf {
 
 namespace {
 
-constexpr int NB = 64;        // panel width
-constexpr int KC = 32;        // K chunk of the update GEMM
-constexpr int LDT = NB + 4;   // SMEM stride of the [k][row] operand tiles (conflict-free fragments)
-constexpr int NST = 3;       // cp.async pipeline stages of the update GEMM
-constexpr int kUpdSmem = NST * 2 * KC * LDT * (int)sizeof(double);
-constexpr int TS = 32;        // symmetrize tile
+constexpr int NB = 64;                    // tile size
+constexpr int LDT = 68;                   // leading dimension inside a packed tile
+constexpr int TILE_D = NB * LDT;          // doubles per packed tile (34816 B)
+constexpr int HALF_D = 32 * LDT;          // 32 tile columns (one pipeline chunk, 17408 B)
+constexpr int NST = 3;                    // bulk-copy ring stages
+constexpr int kDagSmem = NST * 2 * HALF_D * (int)sizeof(double);  // 104448 B → 2 CTAs / SM
+constexpr int LDC = NB + 1;               // SMEM row stride of the C / work tile
 
-// sym + shift: lower ← (A + Aᵀ)/2 (+ Σ_u + δ_w on the diagonal), upper ← 0,
-// through 32×32 SMEM tiles so both the tile and its mirror are read coalesced.
-__global__ void __launch_bounds__(256) k_chol_sym(int n, double* __restrict__ K, const double* __restrict__ sig_u,
-                                                  double delta, int* __restrict__ info_ws) {
-  __shared__ double a[TS][TS + 1], b[TS][TS + 1];
-  const int s = blockIdx.y;
-  const int nt = (n + TS - 1) / TS;
-  int I = (int)((sqrt(8.0 * blockIdx.x + 1.0) - 1.0) * 0.5);  // lower tile (I ≥ J)
-  while ((I + 1) * (I + 2) / 2 <= (int)blockIdx.x) ++I;
-  while (I * (I + 1) / 2 > (int)blockIdx.x) --I;
-  const int J = blockIdx.x - I * (I + 1) / 2;
-  if (I >= nt) return;
-  double* A = K + (size_t)s * n * n;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 × 8
-  for (int c = ty; c < TS; c += 8) {
-    const int col = J * TS + c, row = I * TS + tx;           // tile (I, J): A[col][row] column-major
-    a[c][tx] = (row < n && col < n) ? A[(size_t)col * n + row] : 0.0;
-    const int col2 = I * TS + c, row2 = J * TS + tx;         // mirror tile (J, I)
-    b[c][tx] = (row2 < n && col2 < n) ? A[(size_t)col2 * n + row2] : 0.0;
-  }
-  __syncthreads();
-  for (int c = ty; c < TS; c += 8) {
-    const int col = J * TS + c, row = I * TS + tx;
-    if (row < n && col < n) {
-      // element (row, col) of the lower triangle; its mirror (col, row) is b[tx][c]
-      double v;
-      if (row > col) v = 0.5 * (a[c][tx] + b[tx][c]);
-      else if (row == col) v = a[c][tx] + (sig_u ? sig_u[(size_t)s * n + row] : 0.0) + delta;
-      else v = 0.0;  // strict upper part of a diagonal tile
-      A[(size_t)col * n + row] = v;
-    }
-    if (I != J) {
-      const int col2 = I * TS + c, row2 = J * TS + tx;
-      if (row2 < n && col2 < n) A[(size_t)col2 * n + row2] = 0.0;
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) info_ws[s] = 0;
+enum { T_DONE = 0, T_TILE = 1, T_FWD = 2, T_BWD = 3 };
+
+constexpr int kRhsCap = 2;               // right-hand sides per DAG run (cy workspace)
+
+struct DagArgs {
+  int n, nt, ntri, S, nrhs, ntask;
+  int factor;      // 1: tile tasks included; 0: solve-only run over an existing factor
+  int rhs_ld;      // right-hand sides per scenario in rhs (this run handles [rhs0, rhs0 + nrhs))
+  double* tiles;   // [S][ntri][TILE_D]
+  int* flags;      // [S][ntri + 2 nt]   tile / fwd / bwd ready flags
+  int* ticket;     // task counter
+  int* info;       // [S]
+  double* cy;      // [S][2][kRhsCap][nt*64]  y (forward) and p (backward), padded
+  double* rhs;     // [S][rhs_ld][n], already offset to the first vector of this run
+};
+
+__host__ __device__ __forceinline__ int tidx(int nt, int i, int j) { return j * nt - j * (j - 1) / 2 + (i - j); }
+
+__device__ __forceinline__ unsigned saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
-
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_flag(const int* p) {
+  while (ld_acquire(p) == 0) __nanosleep(40);
+}
+__device__ __forceinline__ void fence_proxy_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(saddr(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(saddr(dst)), "l"(src), "r"(bytes), "r"(saddr(b)) : "memory");
+}
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));
+// info[s] = min over failures (first failing column), 0 = none yet
+__device__ __forceinline__ void record_fail(int* info, int code) {
+  int old = *(volatile int*)info;
+  while (old == 0 || code < old) {
+    const int prev = atomicCAS(info, old, code);
+    if (prev == old) break;
+    old = prev;
+  }
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N_>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N_)); }
 
-// Split-K Gram products of the left-looking update for the 64×64 tiles t of
-// panel j (tile 0 = the diagonal block):
-//   P[ks][t] = Σ_{k ∈ chunk range ks} L[j0 + 64t : +64, k] · L[j0 : j0+64, k]ᵀ.
-// 4 warps × 32×32 outputs, K streamed in 32-wide chunks through 3 cp.async
-// SMEM stages.  KS = 1: the CTA writes A − P itself; otherwise each CTA stores
-// its partial and the last to arrive sums them in ks order (deterministic).
-__global__ void __launch_bounds__(128) k_chol_update(int n, int j0, int T, int KS, double* __restrict__ K,
-                                                     double* __restrict__ part, int slots, int* __restrict__ count,
-                                                     int cnt_stride, const int* __restrict__ info) {
-  const int s = blockIdx.y;
-  if (info[s] != 0) return;
-  extern __shared__ double sm_upd[];
-  __shared__ int last;
+// sym + shift + pack: tile (I, J), I ≥ J, of scenario s, in two 32-column
+// halves; the tile and its mirror are both read down their columns (coalesced).
+__global__ void __launch_bounds__(256) k_chol_pack(int n, int nt, const double* __restrict__ K,
+                                                   const double* __restrict__ sig_u, double delta,
+                                                   double* __restrict__ tiles, int* __restrict__ flags,
+                                                   int* __restrict__ ticket, int* __restrict__ info) {
+  __shared__ double a[32][NB + 1];  // a[c][r] = K(R, C)
+  __shared__ double b[NB][33];      // b[r][c] = K(C, R)  (mirror)
+  const int s = blockIdx.y, ntri = nt * (nt + 1) / 2;
+  int J = 0, t = blockIdx.x;
+  while (t >= nt - J) { t -= nt - J; ++J; }
+  const int I = J + t;
+  const double* A = K + (size_t)s * n * n;
+  double* T = tiles + ((size_t)s * ntri + tidx(nt, I, J)) * TILE_D;
+  for (int ch = 0; ch < NB; ch += 32) {
+    {
+      const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 × 4
+      for (int c = ty; c < 32; c += 4) {
+        const int R = I * NB + tx, C = J * NB + ch + c;
+        a[c][tx] = (R < n && C < n) ? A[(size_t)C * n + R] : 0.0;
+      }
+    }
+    {
+      const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 × 8
+      for (int r = ty; r < NB; r += 8) {  // K(J·64 + ch + tx, I·64 + r)
+        const int R2 = J * NB + ch + tx, C2 = I * NB + r;
+        b[r][tx] = (R2 < n && C2 < n) ? A[(size_t)C2 * n + R2] : 0.0;
+      }
+    }
+    __syncthreads();
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+    for (int c = ty; c < 32; c += 4) {
+      const int R = I * NB + tx, C = J * NB + ch + c;
+      double v;
+      if (R >= n || C >= n) v = (R == C) ? 1.0 : 0.0;  // identity padding
+      else if (R > C) v = 0.5 * (a[c][tx] + b[tx][c]);
+      else if (R == C) v = a[c][tx] + (sig_u ? sig_u[(size_t)s * n + R] : 0.0) + delta;
+      else v = 0.0;
+      T[(ch + c) * LDT + tx] = v;
+    }
+    __syncthreads();
+  }
+  const int nflag = ntri + 2 * nt;
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nflag; f += gridDim.x * blockDim.x)
+    flags[(size_t)s * nflag + f] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    info[s] = 0;
+    if (s == 0) *ticket = 0;
+  }
+}
+
+// L back into K: lower (incl. diagonal) from the tiles, strict upper zeroed.
+__global__ void __launch_bounds__(256) k_chol_unpack(int n, int nt, const double* __restrict__ tiles,
+                                                     double* __restrict__ K) {
+  const int s = blockIdx.z, I = blockIdx.x, J = blockIdx.y, ntri = nt * (nt + 1) / 2;
   double* A = K + (size_t)s * n * n;
-  const int nb = min(NB, n - j0);
-  const int tile = blockIdx.x % T, ks = blockIdx.x / T;
-  const int I0 = j0 + tile * NB;
-  const int nchunk = j0 / KC, per = (nchunk + KS - 1) / KS;
-  const int c0 = ks * per, c1 = min(nchunk, c0 + per);
-  auto As = [&](int st) { return sm_upd + st * 2 * KC * LDT; };
-  auto Bs = [&](int st) { return sm_upd + st * 2 * KC * LDT + KC * LDT; };
-  auto load = [&](int st, int k0) {
-    double* a = As(st);
-    double* b = Bs(st);
-    for (int idx = threadIdx.x; idx < KC * NB; idx += blockDim.x) {
-      const int k = idx / NB, r = idx % NB;
-      const double* col = A + (size_t)(k0 + k) * n;
-      if (I0 + r < n) cp_async8(a + k * LDT + r, col + I0 + r); else a[k * LDT + r] = 0.0;
-      if (r < nb) cp_async8(b + k * LDT + r, col + j0 + r); else b[k * LDT + r] = 0.0;
-    }
-    cp_commit();
-  };
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wr = warp >> 1, wc = warp & 1;
-  const int g = lane >> 2, q = lane & 3;
-  double acc[4][4][2];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) { acc[a][b][0] = 0.0; acc[a][b][1] = 0.0; }
-  if (c0 < c1) load(0, c0 * KC);
-  if (c0 + 1 < c1) load(1, (c0 + 1) * KC);
-  for (int c = c0; c < c1; ++c) {
-    if (c + 2 < c1) { load((c + 2 - c0) % NST, (c + 2) * KC); cp_wait<2>(); }
-    else if (c + 1 < c1) cp_wait<1>();
-    else cp_wait<0>();
-    __syncthreads();
-    const double* a = As((c - c0) % NST);
-    const double* b = Bs((c - c0) % NST);
-#pragma unroll
-    for (int kk = 0; kk < KC; kk += 4) {
-      double af[4], bf[4];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) af[mt] = a[(kk + q) * LDT + wr * 32 + mt * 8 + g];
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) bf[nt] = b[(kk + q) * LDT + wc * 32 + nt * 8 + g];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
-    }
-    __syncthreads();
+  const double* T = I >= J ? tiles + ((size_t)s * ntri + tidx(nt, I, J)) * TILE_D : nullptr;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  for (int c = ty; c < NB; c += 4) {
+    const int R = I * NB + tx, C = J * NB + c;
+    if (R < n && C < n) A[(size_t)C * n + R] = (R >= C && T) ? T[c * LDT + tx] : 0.0;
   }
-  auto store_final = [&](int r, int c, double sub) {  // tile-local (r, c)
-    const int gr = I0 + r;
-    if (gr < n && c < nb && gr >= j0 + c) {
-      double* p = A + (size_t)(j0 + c) * n + gr;
-      *p = *p - sub;
+}
+
+// solve-only run: clear the fwd / bwd flags and the ticket
+__global__ void k_chol_reset_solve(int nt, int S, int* __restrict__ flags, int* __restrict__ ticket) {
+  const int ntri = nt * (nt + 1) / 2, nflag = ntri + 2 * nt;
+  for (int x = threadIdx.x; x < S * 2 * nt; x += blockDim.x) flags[(size_t)(x / (2 * nt)) * nflag + ntri + x % (2 * nt)] = 0;
+  if (threadIdx.x == 0) *ticket = 0;
+}
+
+#ifdef PF_CHOL_TRACE
+// tools/chol_bench.cu: per-task {kind | s | i | j, smid, t0, t1, phase marks[4]} (globaltimer ns)
+__device__ unsigned long long* g_chol_trace;
+__shared__ unsigned long long g_marks[4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PF_MARK(k) do { if (threadIdx.x == 0) g_marks[k] = gtimer(); } while (0)
+#else
+#define PF_MARK(k) do {} while (0)
+#endif
+
+// ------------------------------------------------------------------ the DAG kernel
+// 8 consumer warps (DMMA, triangular kernels, GEMVs) + 1 producer warp that
+// waits on the dependency flags and streams operand tiles into a 3-stage
+// SMEM ring with cp.async.bulk (full / empty mbarriers), so flag latency
+// never stalls the math.  Both sides walk the same chunk sequence per task.
+constexpr int kCons = 256;                 // consumer threads
+constexpr int kDagThreads = kCons + 32;    // + producer warp
+
+struct Pipe {
+  uint64_t* full;   // [NST]  producer arrive.expect_tx → bytes landed
+  uint64_t* empty;  // [NST]  8 consumer-warp arrivals → slot free
+  uint64_t* lbar;   // L_jj tile load
+  unsigned cc;      // chunks of the ring used so far by this CTA
+  unsigned lpar;    // parity of lbar
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
+__device__ __forceinline__ double* stage_ptr(double* sm, unsigned st) { return sm + st * 2 * HALF_D; }
+
+// consumer side: wait for chunk cc, hand the slot back after use
+__device__ __forceinline__ const double* cons_acquire(Pipe& p, double* sm) {
+  const unsigned st = p.cc % NST;
+  mbar_wait(p.full + st, (p.cc / NST) & 1);
+  return stage_ptr(sm, st);
+}
+__device__ __forceinline__ void cons_release(Pipe& p) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(p.empty + p.cc % NST);
+  ++p.cc;
+}
+// producer side (one lane): wait for the slot, then copy `bytes` (1 or 2 pieces)
+__device__ __forceinline__ void prod_issue(Pipe& p, double* sm, const double* src0, const double* src1,
+                                           unsigned bytes_each) {
+  const unsigned st = p.cc % NST;
+  mbar_wait(p.empty + st, ((p.cc / NST) & 1) ^ 1);
+  double* dst = stage_ptr(sm, st);
+  fence_proxy_global();
+  mbar_expect(p.full + st, src1 ? 2 * bytes_each : bytes_each);
+  bulk_g2s(dst, src0, bytes_each, p.full + st);
+  if (src1) bulk_g2s(dst + HALF_D, src1, bytes_each, p.full + st);
+  ++p.cc;
+}
+
+struct TaskCtx {
+  const DagArgs* a;
+  int s, i, j;
+  double* T;  // tiles of scenario s
+  int* F;     // flags of scenario s
+  __device__ const double* tile(int r, int c) const { return T + (size_t)tidx(a->nt, r, c) * TILE_D; }
+  __device__ int* tflag(int r, int c) const { return F + tidx(a->nt, r, c); }
+  __device__ int* fwdflag(int k) const { return F + a->ntri + k; }
+  __device__ int* bwdflag(int k) const { return F + a->ntri + a->nt + k; }
+};
+
+// ---- producer: the operand stream of each task kind
+// L_jj into `dst` (epilogue area) once every ring chunk of the task is consumed
+__device__ void prod_ljj(const TaskCtx& t, Pipe& p, double* dst) {
+  for (unsigned c = p.cc >= NST ? p.cc - NST : 0; c < p.cc; ++c) mbar_wait(p.empty + c % NST, (c / NST) & 1);
+  wait_flag(t.tflag(t.j, t.j));
+  fence_proxy_global();
+  mbar_expect(p.lbar, TILE_D * sizeof(double));
+  bulk_g2s(dst, t.tile(t.j, t.j), TILE_D * sizeof(double), p.lbar);
+}
+
+__device__ void produce(const TaskCtx& t, int kind, Pipe& p, double* sm) {
+  const unsigned half = HALF_D * sizeof(double), full = TILE_D * sizeof(double);
+  if (kind == T_TILE) {
+    const bool diag = t.i == t.j;
+    for (int k = 0; k < t.j; ++k) {
+      wait_flag(t.tflag(t.i, k));
+      if (!diag) wait_flag(t.tflag(t.j, k));
+      for (int h = 0; h < 2; ++h)
+        prod_issue(p, sm, t.tile(t.i, k) + h * HALF_D, diag ? nullptr : t.tile(t.j, k) + h * HALF_D, half);
     }
-  };
-  if (KS == 1) {
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          store_final(wr * 32 + mt * 8 + g, wc * 32 + nt * 8 + 2 * q + h, acc[mt][nt][h]);
-    return;
+    if (!diag) prod_ljj(t, p, sm + NB * LDC);
+  } else if (kind == T_FWD) {
+    for (int k = 0; k < t.j; ++k) {
+      wait_flag(t.tflag(t.j, k));
+      prod_issue(p, sm, t.tile(t.j, k), nullptr, full);
+    }
+    prod_ljj(t, p, sm);
+  } else if (kind == T_BWD) {
+    for (int i = t.a->nt - 1; i > t.j; --i) {
+      wait_flag(t.tflag(i, t.j));
+      prod_issue(p, sm, t.tile(i, t.j), nullptr, full);
+    }
+    prod_ljj(t, p, sm);
   }
-  double* P = part + ((size_t)s * slots + (size_t)ks * T + tile) * (NB * NB);
+}
+
+// ---- in-tile triangular kernels (256 consumer threads, 16-column blocks).
+// Each 16-step dependency chain runs in registers (compile-time indices); the
+// trailing block updates are spread over all consumer threads.
+constexpr int SB = 16;
+
+// Cs (row-major, stride LDC) lower part ← its Cholesky factor; rdv[c] = 1 / L(c, c).
+// Returns 0, or c + 1 for the first column whose pivot is ≤ 0 or non-finite.
+__device__ int potrf64(double* Cs, double* rdv, int* sh) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) sh[0] = 0;
+  for (int b0 = 0; b0 < NB; b0 += SB) {
+    if (tid < 32) {  // diagonal block: lane r < 16 owns row b0 + r (Crout, columns in order)
+      const int r = lane & (SB - 1);
+      double* row = Cs + (b0 + r) * LDC + b0;
+      double x[SB];
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+      for (int k = 0; k < SB; ++k) x[k] = row[k];
+      int bad = 0;
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
+      for (int c = 0; c < SB; ++c) {
+        const double* Lc = Cs + (b0 + c) * LDC + b0;
+        double q4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < c; ++k) q4[k & 3] += x[k] * Lc[k];
+        const double num = x[c] - ((q4[0] + q4[1]) + (q4[2] + q4[3]));
+        const double d = __shfl_sync(0xffffffffu, num, c);
+        if (!(d > 0.0) || !isfinite(d)) { bad = b0 + c + 1; break; }
+        const double rs = rsqrt(d);
+        x[c] = r == c ? d * rs : num * rs;
+        if (lane < SB && r >= c) row[c] = x[c];
+        if (lane == c) rdv[b0 + c] = rs;
+        __syncwarp();
+      }
+      if (tid == 0 && bad) sh[0] = bad;
+    }
+    cons_sync();
+    if (sh[0]) return sh[0];
+    const int nb = NB - b0 - SB;  // rows / columns below the block
+    if (nb == 0) break;
+    if (tid < nb) {  // panel rows: X L_bbᵀ = A, one row per thread in registers
+      double* row = Cs + (b0 + SB + tid) * LDC + b0;
+      double x[SB];
+#pragma unroll
+      for (int k = 0; k < SB; ++k) x[k] = row[k];
+#pragma unroll
+      for (int c = 0; c < SB; ++c) {
+        const double* Lc = Cs + (b0 + c) * LDC + b0;
+        double q4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < c; ++k) q4[k & 3] += x[k] * Lc[k];
+        x[c] = (x[c] - ((q4[0] + q4[1]) + (q4[2] + q4[3]))) * rdv[b0 + c];
+      }
+#pragma unroll
+      for (int k = 0; k < SB; ++k) row[k] = x[k];
+    }
+    cons_sync();
+    // trailing update A[r][c] −= Σ_k L[r][k] L[c][k] over the block's 16 columns, c ≤ r
+    for (int e = tid; e < nb * nb; e += kCons) {
+      const int r = e / nb, c = e % nb;
+      if (c > r) continue;
+      const double* Lr = Cs + (b0 + SB + r) * LDC + b0;
+      const double* Lc = Cs + (b0 + SB + c) * LDC + b0;
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < SB; k += 2) { s0 += Lr[k] * Lc[k]; s1 += Lr[k + 1] * Lc[k + 1]; }
+      Cs[(b0 + SB + r) * LDC + b0 + SB + c] -= s0 + s1;
+    }
+    cons_sync();
+  }
+  return 0;
+}
+
+// X L_jjᵀ = C in place (Cs row-major stride LDC); L_jj in the packed tile layout
+// (L(c, k) = Ls[k·LDT + c]); rdv[c] = 1 / L(c, c) must be ready.
+__device__ void trsm64(double* Cs, const double* Ls, const double* rdv) {
+  const int tid = threadIdx.x;
+  for (int b0 = 0; b0 < NB; b0 += SB) {
+    if (tid < NB) {  // X_b = C_b L_bb^{-T}, one row per thread in registers
+      double* row = Cs + tid * LDC + b0;
+      double x[SB];
+#pragma unroll
+      for (int k = 0; k < SB; ++k) x[k] = row[k];
+#pragma unroll
+      for (int c = 0; c < SB; ++c) {
+        double q4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < c; ++k) q4[k & 3] += x[k] * Ls[(b0 + k) * LDT + b0 + c];
+        x[c] = (x[c] - ((q4[0] + q4[1]) + (q4[2] + q4[3]))) * rdv[b0 + c];
+      }
+#pragma unroll
+      for (int k = 0; k < SB; ++k) row[k] = x[k];
+    }
+    cons_sync();
+    const int nc = NB - b0 - SB;
+    if (nc == 0) break;
+    // C[r][c] −= Σ_{k in block} X[r][k] L(c, k) for the columns right of the block
+    for (int e = tid; e < NB * nc; e += kCons) {
+      const int r = e / nc, c = b0 + SB + e % nc;
+      const double* Xr = Cs + r * LDC + b0;
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < SB; k += 2) {
+        s0 += Xr[k] * Ls[(b0 + k) * LDT + c];
+        s1 += Xr[k + 1] * Ls[(b0 + k + 1) * LDT + c];
+      }
+      Cs[r * LDC + c] -= s0 + s1;
+    }
+    cons_sync();
+  }
+}
+
+// ---- consumers: tile task (i, j)
+__device__ void cons_tile(const TaskCtx& t, Pipe& p, double* sm, int* sh) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wr = warp >> 2, wc = warp & 3, g = lane >> 2, q = lane & 3;
+  const bool diag = t.i == t.j;
+  // acc = −A_ij + Σ_k L_ik L_jkᵀ, so C = −acc; A is loaded before the first chunk lands
+  const double* Aij = t.tile(t.i, t.j);
+  double acc[4][2][2];
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        acc[m][x][h] = -Aij[(wc * 16 + x * 8 + 2 * q + h) * LDT + wr * 32 + m * 8 + g];
+  for (int c = 0; c < 2 * t.j; ++c) {
+    const double* A = cons_acquire(p, sm);
+    const double* B = diag ? A : A + HALF_D;
+#pragma unroll
+    for (int kk = 0; kk < 32; kk += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) af[m] = A[(kk + q) * LDT + wr * 32 + m * 8 + g];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) bf[x] = B[(kk + q) * LDT + wc * 16 + x * 8 + g];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int x = 0; x < 2; ++x) dmma_8x8x4(acc[m][x][0], acc[m][x][1], af[m], bf[x]);
+    }
+    cons_release(p);
+  }
+  cons_sync();  // every warp is past the ring before the epilogue reuses it
+  PF_MARK(0);
+  double* Cs = sm;               // [64][LDC]
+  double* Ls = sm + NB * LDC;    // L_jj (packed layout), filled by the producer
+  double* sv = Ls + TILE_D;      // [64]
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int r = wr * 32 + mt * 8 + g, c = wc * 32 + nt * 8 + 2 * q + h;
-        __stcg(P + c * NB + r, acc[mt][nt][h]);
+        const int r = wr * 32 + m * 8 + g, c = wc * 16 + x * 8 + 2 * q + h;
+        Cs[r * LDC + c] = -acc[m][x][h];
       }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int* cnt = count + (size_t)s * cnt_stride + tile;
-    last = atomicAdd(cnt, 1) == KS - 1;
-    if (last) *cnt = 0;  // ready for the next panel / call
+  cons_sync();
+  PF_MARK(1);
+  double* Out = const_cast<double*>(Aij);
+  if (diag) {
+    const int fail = potrf64(Cs, sv, sh);
+    PF_MARK(2);
+    if (fail && tid == 0) record_fail(t.a->info + t.s, t.j * NB + fail);
+    for (int idx = tid; idx < NB * NB; idx += kCons) {
+      const int c = idx >> 6, r = idx & 63;
+      Out[c * LDT + r] = r >= c ? Cs[r * LDC + c] : 0.0;
+    }
+  } else {
+    mbar_wait(p.lbar, p.lpar);
+    p.lpar ^= 1;
+    if (tid < NB) sv[tid] = 1.0 / Ls[tid * LDT + tid];
+    cons_sync();
+    trsm64(Cs, Ls, sv);
+    PF_MARK(2);
+    for (int idx = tid; idx < NB * NB; idx += kCons) {
+      const int c = idx >> 6, rr = idx & 63;
+      Out[c * LDT + rr] = Cs[rr * LDC + c];
+    }
   }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  const double* P0 = part + ((size_t)s * slots + tile) * (NB * NB);
-  for (int idx = threadIdx.x; idx < NB * NB; idx += blockDim.x) {
-    const int c = idx / NB, r = idx % NB;
-    double sum = 0.0;
-    for (int k = 0; k < KS; ++k) sum += __ldcg(P0 + (size_t)k * T * (NB * NB) + idx);
-    store_final(r, c, sum);
+  cons_sync();
+  PF_MARK(3);
+  if (tid == 0) {
+    __threadfence();
+    fence_proxy_global();
+    st_release(t.tflag(t.i, t.j), 1);
   }
 }
 
-// Panel step.  Every CTA factors the 64×64 diagonal block, then solves its
-// 64-row block of the panel, X L_jjᵀ = A.  Both are register-blocked: thread
-// (ty, tx) of the 16×16 thread grid owns the 16 elements (ty + 16a, tx + 16b);
-// each of the 64 sequential steps publishes one column through SMEM (double-
-// buffered, ONE barrier per step) and every thread updates its elements.
-// The factorization runs in the unscaled LDLᵀ form (A[r][c] −= A[r][J] A[c][J]
-// / d_J needs no broadcast pivot), the Cholesky scaling L = D^{1/2} applied at
-// the end; CTA 0 writes L_jj back and reports the first pivot ≤ 0 in info.
-__global__ void __launch_bounds__(256) k_chol_panel(int n, int k0, double* __restrict__ K, int* __restrict__ info) {
-  const int s = blockIdx.y;
-  if (info[s] != 0) return;
-  __shared__ double col[2][NB];
-  __shared__ double dv[NB];
-  __shared__ double Ls[NB][NB + 1];
-  __shared__ int fail;
-  double* A = K + (size_t)s * n * n;
-  const int nb = min(NB, n - k0);
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double a[4][4];  // element (ty + 16i, tx + 16j)
+// ---- consumers: forward solve task j, y_j = L_jj^{-1}(b_j − Σ_{k<j} L_jk y_k)
+__device__ void cons_fwd(const TaskCtx& t, Pipe& p, double* sm, double* red, double* vs, double* rdv) {
+  const DagArgs& a = *t.a;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, j = t.j, nt = a.nt;
+  // warp w: rows [8w, 8w+8) of every streamed tile; lanes: columns lane, lane + 32
+  double acc[kRhsCap][8];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int rr = 0; rr < kRhsCap; ++rr)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int r = ty + 16 * i, c = tx + 16 * j;
-      double v;
-      if (r < nb && c < nb) v = r >= c ? A[(size_t)(k0 + c) * n + k0 + r] : 0.0;
-      else v = (r == c) ? 1.0 : 0.0;  // identity padding past the matrix edge
-      a[i][j] = v;
-    }
-  if (threadIdx.x == 0) fail = 0;
-  // ---- factor: 64 steps, one barrier each
-  for (int J = 0; J < NB; ++J) {
-    const int bj = J >> 4, tj = J & 15, buf = J & 1;
-    if (tx == tj) {
+    for (int r8 = 0; r8 < 8; ++r8) acc[rr][r8] = 0.0;
+  for (int k = 0; k < j; ++k) {
+    const double* Tk = cons_acquire(p, sm);
+    if (lane == 0) wait_flag(t.fwdflag(k));
+    __syncwarp();
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+    for (int rr = 0; rr < kRhsCap; ++rr) {
+      if (rr < a.nrhs) {
+        const double* yk = a.cy + ((size_t)t.s * 2 * kRhsCap + rr) * nt * NB + k * NB;
+        const double y0 = __ldcg(yk + lane), y1 = __ldcg(yk + lane + 32);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j == bj) col[buf][ty + 16 * i] = a[i][j];  // static indexing keeps a[][] in registers
-    }
-    __syncthreads();
-    const double d = col[buf][J];
-    if (!(d > 0.0) || !isfinite(d)) {  // every thread sees the same pivot
-      if (threadIdx.x == 0) fail = k0 + J + 1;
-      break;
-    }
-    if (threadIdx.x == 0) dv[J] = d;
-    const double invd = 1.0 / d;
-    double cr[4], cc[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) { cr[i] = col[buf][ty + 16 * i]; cc[i] = col[buf][tx + 16 * i] * invd; }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int r = ty + 16 * i, c = tx + 16 * j;
-        if (c > J && r >= c) a[i][j] -= cr[i] * cc[j];
+        for (int r8 = 0; r8 < 8; ++r8)
+          acc[rr][r8] += Tk[lane * LDT + 8 * warp + r8] * y0 + Tk[(lane + 32) * LDT + 8 * warp + r8] * y1;
       }
-  }
-  __syncthreads();
-  if (fail) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) info[s] = fail;
-    return;
-  }
-  // ---- L = (unscaled column) / sqrt(d_c), diagonal sqrt(d_c)
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int r = ty + 16 * i, c = tx + 16 * j;
-      const double sq = sqrt(dv[c]);
-      const double v = r == c ? sq : (r > c ? a[i][j] / sq : 0.0);
-      Ls[r][c] = v;
-      if (blockIdx.x == 0 && r < nb && c < nb && r >= c) A[(size_t)(k0 + c) * n + k0 + r] = v;
     }
-  const int i0 = k0 + nb + blockIdx.x * NB;
-  if (i0 >= n) return;
-  // ---- panel rows: X L_jjᵀ = A, column by column (right-looking), one barrier per column
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int r = ty + 16 * i, c = tx + 16 * j;
-      a[i][j] = (i0 + r < n && c < nb) ? A[(size_t)(k0 + c) * n + i0 + r] : 0.0;
-    }
-  __syncthreads();
-  for (int J = 0; J < nb; ++J) {
-    const int bj = J >> 4, tj = J & 15, buf = J & 1;
-    const double inv = 1.0 / Ls[J][J];
-    if (tx == tj) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j == bj) { a[i][j] *= inv; col[buf][ty + 16 * i] = a[i][j]; }
-    }
-    __syncthreads();
-    double xr[4], lc[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) { xr[i] = col[buf][ty + 16 * i]; lc[i] = Ls[tx + 16 * i][J]; }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (tx + 16 * j > J) a[i][j] -= xr[i] * lc[j];
+    cons_release(p);
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int rr = 0; rr < kRhsCap; ++rr)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int r = ty + 16 * i, c = tx + 16 * j;
-      if (i0 + r < n && c < nb) A[(size_t)(k0 + c) * n + i0 + r] = a[i][j];
+    for (int r8 = 0; r8 < 8; ++r8) {
+      double v = acc[rr][r8];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && rr < a.nrhs) red[rr * NB + 8 * warp + r8] = v;
     }
+  cons_sync();
+  mbar_wait(p.lbar, p.lpar);  // L_jj (packed layout: L(r, c) = Ls[c·LDT + r])
+  p.lpar ^= 1;
+  const double* Ls = sm;
+  if (tid < NB) rdv[tid] = 1.0 / Ls[tid * LDT + tid];
+  for (int idx = tid; idx < a.nrhs * NB; idx += kCons) {
+    const int rr = idx >> 6, r = idx & 63, R = j * NB + r;
+    const double b = R < a.n ? a.rhs[((size_t)t.s * a.rhs_ld + rr) * a.n + R] : 0.0;
+    vs[rr * NB + r] = b - red[rr * NB + r];
+  }
+  cons_sync();
+  if (warp < a.nrhs) {  // one warp per right-hand side: lane owns rows lane, lane + 32
+    double* y = vs + warp * NB;
+    double y0 = y[lane], y1 = y[lane + 32];
+    for (int c = 0; c < NB; ++c) {
+      const double yc = __shfl_sync(0xffffffffu, c < 32 ? y0 : y1, c & 31) * rdv[c];
+      if (lane == (c & 31)) { if (c < 32) y0 = yc; else y1 = yc; }
+      if (lane > c) y0 -= Ls[c * LDT + lane] * yc;
+      if (lane + 32 > c) y1 -= Ls[c * LDT + lane + 32] * yc;
+    }
+    double* yo = a.cy + ((size_t)t.s * 2 * kRhsCap + warp) * nt * NB + j * NB;
+    __stcg(yo + lane, y0);
+    __stcg(yo + lane + 32, y1);
+  }
+  cons_sync();
+  if (tid == 0) {
+    __threadfence();
+    st_release(t.fwdflag(j), 1);
+  }
 }
 
-// L Lᵀ P = B for every right-hand side of every scenario.  The P CTAs of a
-// scenario's thread-block cluster own 64-row blocks round-robin.  Forward: the owner of block J
-// solves L_JJ y_J = b_J, grid barrier, then every CTA updates its own blocks
-// I > J: b_I −= L_IJ y_J.  Backward (right-looking on Lᵀ): the owner of J
-// solves L_JJᵀ p_J = b_J, barrier, every CTA updates its blocks I < J:
-// b_I −= L_JIᵀ p_J.  One cluster barrier per block and direction.
-constexpr int kSolveThreads = 256;
+// ---- consumers: backward solve task j, p_j = L_jj^{-T}(y_j − Σ_{i>j} L_ijᵀ p_i)
+__device__ void cons_bwd(const TaskCtx& t, Pipe& p, double* sm, double* red, double* vs, double* rdv, int* sh) {
+  const DagArgs& a = *t.a;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, j = t.j, nt = a.nt;
+  // warp w: columns c = 8w..8w+7 of every streamed tile, lanes over its rows
+  double acc[kRhsCap][8];
+#pragma unroll
+  for (int rr = 0; rr < kRhsCap; ++rr)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[rr][c] = 0.0;
+  for (int i = nt - 1; i > j; --i) {
+    const double* Ti = cons_acquire(p, sm);
+    if (lane == 0) wait_flag(t.bwdflag(i));
+    __syncwarp();
+#pragma unroll
+    for (int rr = 0; rr < kRhsCap; ++rr) {
+      if (rr < a.nrhs) {
+        const double* pi = a.cy + ((size_t)t.s * 2 * kRhsCap + kRhsCap + rr) * nt * NB + i * NB;
+        const double p0 = __ldcg(pi + lane), p1 = __ldcg(pi + lane + 32);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          acc[rr][c] += Ti[(8 * warp + c) * LDT + lane] * p0 + Ti[(8 * warp + c) * LDT + lane + 32] * p1;
+      }
+    }
+    cons_release(p);
+  }
+#pragma unroll
+  for (int rr = 0; rr < kRhsCap; ++rr)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      double v = acc[rr][c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && rr < a.nrhs) red[rr * NB + 8 * warp + c] = v;
+    }
+  if (tid == 0) {
+    wait_flag(t.fwdflag(j));
+    sh[0] = *(volatile int*)(a.info + t.s) == 0;
+  }
+  cons_sync();  // red and y_j visible to every consumer
+  mbar_wait(p.lbar, p.lpar);  // L_jj (packed layout: L(r, c) = Ls[c·LDT + r])
+  p.lpar ^= 1;
+  const double* Ls = sm;
+  if (tid < NB) rdv[tid] = 1.0 / Ls[tid * LDT + tid];
+  for (int idx = tid; idx < a.nrhs * NB; idx += kCons) {
+    const int rr = idx >> 6, c = idx & 63;
+    vs[rr * NB + c] = __ldcg(a.cy + ((size_t)t.s * 2 * kRhsCap + rr) * nt * NB + j * NB + c) - red[rr * NB + c];
+  }
+  cons_sync();
+  const bool ok = sh[0];
+  if (ok && warp < a.nrhs) {  // Lᵀ p = v backwards; lane owns entries lane, lane + 32
+    double* v = vs + warp * NB;
+    double v0 = v[lane], v1 = v[lane + 32];
+    for (int c = NB - 1; c >= 0; --c) {
+      const double pc = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, c & 31) * rdv[c];
+      if (lane == (c & 31)) { if (c < 32) v0 = pc; else v1 = pc; }
+      // (Lᵀ p)[r] for r < c gets L(c, r) p_c; L(c, r) = Ls[r·LDT + c]
+      if (lane < c) v0 -= Ls[lane * LDT + c] * pc;
+      if (lane + 32 < c) v1 -= Ls[(lane + 32) * LDT + c] * pc;
+    }
+    double* po = a.cy + ((size_t)t.s * 2 * kRhsCap + kRhsCap + warp) * nt * NB + j * NB;
+    __stcg(po + lane, v0);
+    __stcg(po + lane + 32, v1);
+    double* out = a.rhs + ((size_t)t.s * a.rhs_ld + warp) * a.n;
+    if (j * NB + lane < a.n) out[j * NB + lane] = v0;
+    if (j * NB + lane + 32 < a.n) out[j * NB + lane + 32] = v1;
+  }
+  cons_sync();
+  if (tid == 0) {
+    __threadfence();
+    st_release(t.bwdflag(j), 1);
+  }
+}
 
-__global__ void __launch_bounds__(kSolveThreads) k_chol_solve(int n, const double* __restrict__ K, double* __restrict__ rhs,
-                                                              int nrhs, const int* __restrict__ info, int n_scen, int P) {
-  cg::cluster_group grid = cg::this_cluster();  // one cluster of P CTAs per scenario
-  __shared__ double D[NB][NB + 1];
-  __shared__ double yb[NB];
-  const int s = blockIdx.x / P, sub = (int)grid.block_rank();
-  const bool active = s < n_scen && info[s] == 0;
-  const double* L = K + (size_t)(s < n_scen ? s : 0) * n * n;
-  const int nblk = (n + NB - 1) / NB;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  auto stage = [&](int j0, int nb) {
-    for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
-      const int c = idx / nb, r = idx % nb;
-      D[r][c] = r >= c ? L[(size_t)(j0 + c) * n + j0 + r] : 0.0;
+__global__ void __launch_bounds__(kDagThreads, 2) k_chol_dag(DagArgs a) {
+  extern __shared__ __align__(128) double sm_dag[];
+  __shared__ __align__(8) uint64_t bars[2 * NST + 1];
+  __shared__ double red[kRhsCap * NB], vsol[kRhsCap * NB], rdv[NB];
+  __shared__ int task[5];
+  __shared__ int sh[2];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int b = 0; b < NST; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(bars + b)) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(saddr(bars + NST + b)) : "memory");
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(bars + 2 * NST)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  Pipe p{bars, bars + NST, bars + 2 * NST, 0u, 0u};
+  const int f = a.nrhs > 0 ? 1 : 0;
+  for (;;) {
+    if (tid == 0) {
+      int t = atomicAdd(a.ticket, 1);
+      task[4] = t;
+      int kind = T_DONE, s = 0, i = 0, j = 0;
+      if (t < a.ntask) {
+        int jj = 0;
+        for (; jj < a.nt; ++jj) {
+          const int ntile = a.factor ? a.nt - jj : 0, per = ntile + f, grp = a.S * per;
+          if (t < grp) {
+            s = t / per;
+            const int r = t % per;
+            if (r < ntile) { kind = T_TILE; i = jj + r; j = jj; }
+            else { kind = T_FWD; j = jj; }
+            break;
+          }
+          t -= grp;
+        }
+        if (jj == a.nt) { kind = T_BWD; j = a.nt - 1 - t / a.S; s = t % a.S; }
+        // a scenario that already failed at an earlier column skips its remaining tiles
+        if (kind == T_TILE) {
+          const int inf = *(volatile int*)(a.info + s);
+          if (inf != 0 && inf <= j * NB) kind = -T_TILE;
+        }
+      }
+      task[0] = kind; task[1] = s; task[2] = i; task[3] = j;
     }
     __syncthreads();
-  };
-  for (int rr = 0; rr < nrhs; ++rr) {
-    double* b = rhs + ((size_t)(s < n_scen ? s : 0) * nrhs + rr) * n;
-    // ---- forward L y = b
-    for (int J = 0; J < nblk; ++J) {
-      const int j0 = J * NB, nb = min(NB, n - j0);
-      if (active && sub == J % P) {
-        for (int t = threadIdx.x; t < nb; t += blockDim.x) yb[t] = __ldcg(b + j0 + t);
-        stage(j0, nb);
-        if (warp == 0) {
-          for (int j = 0; j < nb; ++j) {
-            const double yj = yb[j] / D[j][j];
-            __syncwarp();
-            if (lane == 0) yb[j] = yj;
-            for (int i = j + 1 + lane; i < nb; i += 32) yb[i] -= D[i][j] * yj;
-            __syncwarp();
-          }
-        }
-        __syncthreads();
-        for (int t = threadIdx.x; t < nb; t += blockDim.x) __stcg(b + j0 + t, yb[t]);
+    const int kind = task[0], s = task[1], i = task[2], j = task[3];
+    if (kind == T_DONE) break;
+#ifdef PF_CHOL_TRACE
+    const unsigned long long t0 = gtimer();
+#endif
+    TaskCtx t{&a, s, i, j, a.tiles + (size_t)s * a.ntri * TILE_D, a.flags + (size_t)s * (a.ntri + 2 * a.nt)};
+    if (kind == -T_TILE) {
+      if (tid == 0) st_release(t.tflag(i, j), 1);  // skipped: publish so dependants proceed
+    } else if (tid >= kCons) {
+      if (tid == kCons) produce(t, kind, p, sm_dag);
+      else {  // keep the ring position of the other producer lanes in step (unused)
       }
-      grid.sync();
-      if (active) {
-        for (int t = threadIdx.x; t < nb; t += blockDim.x) yb[t] = __ldcg(b + j0 + t);
-        __syncthreads();
-        // rows of the owned blocks I > J, 4 lanes per row (16 columns each)
-        const int q = threadIdx.x & 3;
-        for (int I = J + 1 + ((sub - (J + 1)) % P + P) % P; I < nblk; I += P) {
-          const int i0 = I * NB, ni = min(NB, n - i0);
-          // warp-uniform trip count: the shuffles below need all 32 lanes
-          for (int t0 = 0; t0 < ni; t0 += blockDim.x >> 2) {
-            const int t = t0 + (threadIdx.x >> 2);
-            const int i = i0 + t;
-            double a0 = 0.0, a1 = 0.0;
-            if (t < ni)
-              for (int j = q; j < nb; j += 8) {
-                a0 += L[(size_t)(j0 + j) * n + i] * yb[j];
-                if (j + 4 < nb) a1 += L[(size_t)(j0 + j + 4) * n + i] * yb[j + 4];
-              }
-            double a = a0 + a1;
-            a += __shfl_xor_sync(0xffffffffu, a, 1);
-            a += __shfl_xor_sync(0xffffffffu, a, 2);
-            if (q == 0 && t < ni) __stcg(b + i, __ldcg(b + i) - a);
-          }
-        }
-        __syncthreads();
-      }
+    } else if (kind == T_TILE) {
+      cons_tile(t, p, sm_dag, sh);
+    } else if (kind == T_FWD) {
+      cons_fwd(t, p, sm_dag, red, vsol, rdv);
+    } else {
+      cons_bwd(t, p, sm_dag, red, vsol, rdv, sh);
     }
-    // ---- backward Lᵀ p = y
-    for (int J = nblk - 1; J >= 0; --J) {
-      const int j0 = J * NB, nb = min(NB, n - j0);
-      if (active && sub == J % P) {
-        for (int t = threadIdx.x; t < nb; t += blockDim.x) yb[t] = __ldcg(b + j0 + t);
-        stage(j0, nb);
-        if (warp == 0) {
-          for (int j = nb - 1; j >= 0; --j) {
-            double acc = 0.0;
-            for (int i = j + 1 + lane; i < nb; i += 32) acc += D[i][j] * yb[i];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) yb[j] = (yb[j] - acc) / D[j][j];
-            __syncwarp();
-          }
-        }
-        __syncthreads();
-        for (int t = threadIdx.x; t < nb; t += blockDim.x) __stcg(b + j0 + t, yb[t]);
-      }
-      grid.sync();
-      if (active) {
-        for (int t = threadIdx.x; t < nb; t += blockDim.x) yb[t] = __ldcg(b + j0 + t);
-        __syncthreads();
-        for (int I = sub; I < J; I += P) {
-          const int i0 = I * NB, ni = min(NB, n - i0);
-          for (int t = warp; t < ni; t += nwarp) {  // column i of L, rows j0.. (contiguous)
-            const int i = i0 + t;
-            double acc = 0.0;
-            for (int j = lane; j < nb; j += 32) acc += L[(size_t)i * n + j0 + j] * yb[j];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) __stcg(b + i, __ldcg(b + i) - acc);
-          }
-        }
-        __syncthreads();
-      }
+    fence_proxy_shared();  // this task's generic SMEM writes before the next task's bulk copies
+    __syncthreads();
+#ifdef PF_CHOL_TRACE
+    if (tid == 0 && g_chol_trace) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      unsigned long long* e = g_chol_trace + 8 * (size_t)task[4];
+      e[0] = ((unsigned long long)(kind & 0xff) << 56) | ((unsigned long long)s << 40) |
+             ((unsigned long long)i << 20) | (unsigned long long)j;
+      e[1] = smid; e[2] = t0; e[3] = gtimer();
+      for (int m = 0; m < 4; ++m) { e[4 + m] = g_marks[m]; g_marks[m] = 0; }
     }
-    grid.sync();
+#endif
   }
 }
 
@@ -430,57 +694,51 @@ __global__ void k_info_out(int n_scen, const int* __restrict__ ws, int* __restri
 
 }  // namespace
 
-int chol_part_slots(int n_u) { return (n_u + NB - 1) / NB + 296; }
+size_t chol_tile_doubles(int n_u) {
+  const size_t nt = (n_u + NB - 1) / NB;
+  return nt * (nt + 1) / 2 * TILE_D;
+}
+size_t chol_flag_ints(int n_u) {
+  const size_t nt = (n_u + NB - 1) / NB;
+  return nt * (nt + 1) / 2 + 2 * nt;
+}
+size_t chol_vec_doubles(int n_u) { return 2 * (size_t)kRhsCap * ((n_u + NB - 1) / NB) * NB; }
 
 int launch_chol(const DevNet& net, const Work& w, int n_scen, double* K, const double* sigma_u, double delta_w,
                 double* rhs, int nrhs, int* info, int* info_ws, cudaStream_t st) {
-  const int n = net.n_u;
-  int launches = 0;
-  static int CSS = 0;
-  if (!CSS) {
-    cudaFuncSetAttribute(k_chol_update, cudaFuncAttributeMaxDynamicSharedMemorySize, kUpdSmem);
-    cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    for (int cs : {16, 8, 4, 2, 1}) {  // largest cluster the part schedules
-      cudaLaunchConfig_t cfg = {};
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-      cfg.gridDim = dim3(cs); cfg.blockDim = dim3(kSolveThreads); cfg.attrs = at; cfg.numAttrs = 1;
-      int nc = 0;
-      if (cudaOccupancyMaxActiveClusters(&nc, (void*)k_chol_solve, &cfg) == cudaSuccess && nc > 0) { CSS = cs; break; }
-    }
-    cudaGetLastError();
-    if (!CSS) CSS = 1;
+  const int n = net.n_u, nt = (n + NB - 1) / NB, ntri = nt * (nt + 1) / 2;
+  static int grid_max = 0;
+  if (!grid_max) {
+    cudaFuncSetAttribute(k_chol_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDagSmem);
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_dag, kDagThreads, kDagSmem);
+    grid_max = std::max(1, sms * std::max(per, 1));
   }
-  const int nts = (n + TS - 1) / TS;
-  k_chol_sym<<<dim3(nts * (nts + 1) / 2, n_scen), 256, 0, st>>>(n, K, sigma_u, delta_w, info_ws);
+  int launches = 0;
+  k_chol_pack<<<dim3(ntri, n_scen), 256, 0, st>>>(n, nt, K, sigma_u, delta_w, w.ctile, w.cflag, w.cticket, info_ws);
   ++launches;
-  const int cnt_stride = (n + NB - 1) / NB + 1;
-  for (int j0 = 0; j0 < n; j0 += NB) {
-    const int rows = n - j0;
-    const int T = (rows + NB - 1) / NB;   // tiles of the panel, tile 0 = diagonal block
-    if (j0 > 0) {  // split K so that ~2 CTAs per SM work on every panel
-      const int nchunk = j0 / KC;
-      int KS = std::max(1, std::min({(296 + T * n_scen - 1) / (T * n_scen), nchunk, 16}));
-      KS = std::min(KS, std::max(1, w.cpart_slots / T));
-      k_chol_update<<<dim3(T * KS, n_scen), 128, kUpdSmem, st>>>(n, j0, T, KS, K, w.cpart, w.cpart_slots,
-                                                                   w.ccount, cnt_stride, info_ws);
+  // the factorization runs with the first kRhsCap right-hand sides fused in; further
+  // ones (rare) in solve-only runs over the finished factor
+  for (int r0 = 0, first = 1; first || r0 < nrhs; r0 += kRhsCap, first = 0) {
+    const int nr = std::max(0, std::min(kRhsCap, nrhs - r0)), f = nr > 0 ? 1 : 0;
+    if (!first) {
+      k_chol_reset_solve<<<1, 256, 0, st>>>(nt, n_scen, w.cflag, w.cticket);
       ++launches;
     }
-    k_chol_panel<<<dim3(std::max(T - 1, 1), n_scen), 256, 0, st>>>(n, j0, K, info_ws);
-    ++launches;
+    DagArgs a;
+    a.n = n; a.nt = nt; a.ntri = ntri; a.S = n_scen; a.nrhs = nr; a.factor = first; a.rhs_ld = nrhs;
+    a.ntask = n_scen * ((first ? ntri : 0) + f * nt) + f * n_scen * nt;
+    a.tiles = w.ctile; a.flags = w.cflag; a.ticket = w.cticket; a.info = info_ws;
+    a.cy = w.cy; a.rhs = rhs ? rhs + (size_t)r0 * n : nullptr;
+    if (a.ntask > 0) {
+      k_chol_dag<<<std::min(grid_max, a.ntask), kDagThreads, kDagSmem, st>>>(a);
+      ++launches;
+    }
   }
-  if (nrhs > 0) {
-    const int P = CSS;
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = P; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(P * n_scen); cfg.blockDim = dim3(kSolveThreads); cfg.stream = st;
-    cfg.attrs = at; cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_chol_solve, n, (const double*)K, rhs, nrhs, (const int*)info_ws, n_scen, P);
-    ++launches;
-  }
+  k_chol_unpack<<<dim3(nt, nt, n_scen), 256, 0, st>>>(n, nt, w.ctile, K);
+  ++launches;
   if (info) { k_info_out<<<1, 256, 0, st>>>(n_scen, info_ws, info); ++launches; }
   return launches;
 }

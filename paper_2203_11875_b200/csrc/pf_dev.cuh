@@ -59,10 +59,10 @@ struct Work {
   double* slabW;   // [max_tiles][n_x][C]
   double* hu;      // [max_tiles][n_u][C]
   double* mu;      // [max_tiles][n_gb][2][C]
-  double* cpart;   // Cholesky split-K partial sums: [max_scen][kCholSlots][64*64]
-  int cpart_slots; // tiles × K-splits per scenario that fit cpart
-  int* ccount;     // [max_scen][64-row tiles] split-K arrival counters (zero between calls)
-  double* cinv;    // [max_scen][64-col panels][64*64] inverses of the diagonal blocks L_jj
+  double* ctile;   // [max_scen][chol_tile_doubles]  packed lower 64×64 tiles of K_cond / L
+  int* cflag;      // [max_scen][chol_flag_ints]     tile / forward / backward ready flags
+  int* cticket;    // [1]                            Cholesky DAG task counter
+  double* cy;      // [max_scen][chol_vec_doubles]   forward / backward solve vectors
   int max_tiles;
 };
 

@@ -23,11 +23,13 @@ int launch_reduce(const DevNet& n, const Work& w, int C, int n_scen, const doubl
                   int N, double* KV, cudaStream_t st,
                   cudaEvent_t* ev = nullptr /* optional: [5] around k_fwd, k_mu, k_hvp, k_adj */);
 
-// A9: symmetrize + shift, blocked FP64 Cholesky (DMMA trailing update), solves.
+// A9: symmetrize + shift + pack, tile-DAG FP64 Cholesky (DMMA updates) with the solves fused in.
 int launch_chol(const DevNet& n, const Work& w, int n_scen, double* K, const double* sigma_u, double delta_w,
                 double* rhs, int nrhs, int* info, int* info_ws, cudaStream_t st);
 
 int pick_tile_cols(int n_x, int n_scen_x_N);
-int chol_part_slots(int n_u);   // split-K partial tiles per scenario the Cholesky may use
+size_t chol_tile_doubles(int n_u);  // Cholesky workspaces per scenario (pf_chol.cu)
+size_t chol_flag_ints(int n_u);
+size_t chol_vec_doubles(int n_u);
 
 }  // namespace pf

@@ -182,7 +182,7 @@ def test_batch_invariance_bitwise(pfmod, name, net, pts):
 def test_condensed_kkt_solve(pfmod, name):
     """K_cond = sym(K̂) + diag(Σ_u) + δ_w I: L and the solve vs the oracle's
     textbook Cholesky; info for an indefinite shift equals the oracle's.
-    case1354 (n_u = 519) exercises ragged panels and the split-K update."""
+    case1354 (n_u = 519) exercises ragged tiles and deep tile-DAG chains."""
     import torch
     net, pt = table1_grid(name)
     pts = [pt, make_scenario(net, pt, 1)]
@@ -222,6 +222,42 @@ def test_condensed_kkt_solve(pfmod, name):
     for s in range(S):
         _, io = O.cholesky(O.condensed(0.5 * (KV[s] + KV[s].T), pts[s]["sigma_u"], shift))
         assert info[s].item() == io
+    h.close()
+
+
+def test_condensed_kkt_many_rhs_mixed_info(pfmod):
+    """Three scenarios, six right-hand sides (more than one DAG run carries),
+    one scenario made indefinite through Σ_u: its info is the oracle's first
+    failing column and its right-hand sides stay untouched; the others solve."""
+    import torch
+    net, pt = table1_grid("case118")
+    pts = [pt, make_scenario(net, pt, 1), make_scenario(net, pt, 2)]
+    S, R = 3, 6
+    n_u = O.partition(net)["n_u"]
+    h = pfmod.Network(net, max_batch=n_u, max_scen=S)
+    KV, _ = _run_khat(pfmod, h, net, pts)
+    Khs = [0.5 * (KV[s] + KV[s].T) for s in range(S)]
+    sig = stack(pts, "sigma_u").copy()
+    delta = max(0.0, -min(np.linalg.eigvalsh(Khs[s] + np.diag(sig[s])).min() for s in range(S))) * 1.5 + 1.0
+    sig[1, 70] = -1e9
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal((S, R, n_u))
+    K, rhs = dev(KV.copy()), dev(b.copy())
+    info = torch.empty(S, dtype=torch.int32, device="cuda")
+    h.pf_condensed_kkt_solve(S, K, dev(sig), delta, rhs, R, info)
+    torch.cuda.synchronize()
+    got = rhs.cpu().numpy()
+    Lg = K.cpu().numpy()
+    for s in range(S):
+        Lo, io = O.cholesky(O.condensed(Khs[s], sig[s], delta))
+        assert info[s].item() == io, s
+        if io:
+            assert s == 1 and io == 71
+            assert np.array_equal(got[s], b[s])
+            continue
+        assert rel_err(Lg[s].T, Lo) <= TOL
+        for r in range(R):
+            assert rel_err(got[s, r], O.chol_solve(Lo, b[s, r])) <= TOL, (s, r)
     h.close()
 
 
@@ -271,4 +307,19 @@ def test_full_size_sampled_columns(pfmod, name):
         got = KV[s][cols].T
         assert rel_err(got, ref) <= TOL, (name, s)
         assert np.all(np.isfinite(KV[s]))
+    # the condensed-KKT Cholesky + solve at full size (bench launch: all scenarios at once)
+    Khs = [0.5 * (KV[s] + KV[s].T) for s in range(S)]
+    delta = max(0.0, -min(np.linalg.eigvalsh(Khs[s] + np.diag(pts[s]["sigma_u"])).min() for s in range(S))) * 1.5 + 1.0
+    b = np.random.default_rng(12).standard_normal((S, 1, n_u))
+    K, rhs = dev(KV.copy()), dev(b.copy())
+    info = torch.empty(S, dtype=torch.int32, device="cuda")
+    h.pf_condensed_kkt_solve(S, K, dev(stack(pts, "sigma_u")), delta, rhs, 1, info)
+    torch.cuda.synchronize()
+    assert info.cpu().tolist() == [0] * S
+    Lg = K.cpu().numpy()
+    for s in range(S):
+        Lo, io = O.cholesky(O.condensed(Khs[s], pts[s]["sigma_u"], delta))
+        assert io == 0
+        assert rel_err(Lg[s].T, Lo) <= TOL, (name, s)
+        assert rel_err(rhs[s, 0].cpu().numpy(), O.chol_solve(Lo, b[s, 0])) <= TOL, (name, s)
     h.close()
