@@ -23,6 +23,7 @@ struct pf_net {
   std::string err;
   long long launches = 0;
   bool prof = false;         // instrumentation: events around the hot kernels
+  double reach_frac_l = 0.0, reach_frac_ua = 0.0;  // visited fraction of the L / Lᵀ sweep blocks
   cudaEvent_t ev[8] = {};    // [0..4] reduction kernels, [5..6] k_lu
 };
 
@@ -143,6 +144,43 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
     s1 = two ? P.lu_diag[r0 + 1] : 0; c1 = two ? P.lu_ptr[r0 + 2] - s1 : 0;
     taskU[bi] = make_int4(r0 | (two ? (int)0x80000000u : 0), s0, s1, (c0 << 16) | c1);
   }
+  // sparse-RHS reach (pf_dev.cuh): elimination tree of the filled L, then per
+  // canonical tile the union of the tree paths from its columns' G_u rows
+  std::vector<int> parent(P.n_x, -1);
+  for (int r = 0; r < P.n_x; ++r)
+    for (int e = P.lu_ptr[r]; e < P.lu_diag[r]; ++e)
+      if (parent[P.lu_idx[e]] < 0) parent[P.lu_idx[e]] = r;
+  const int TC = h->C, ntc = (P.n_u + TC - 1) / TC, bmw = (P.n_x + 31) / 32, nlevL = d.nlevL, nlevU = d.nlevU;
+  std::vector<int4> taskLr;
+  std::vector<int> levLr_ptr((size_t)ntc * (nlevL + 1), 0), row_mark(P.n_x, -1), blk_mark(nblk, -1);
+  std::vector<unsigned> rowbm((size_t)ntc * bmw, 0u);
+  auto climb = [&](int r, int stamp) {
+    for (; r >= 0 && row_mark[r] != stamp; r = parent[r]) { row_mark[r] = stamp; blk_mark[P.row_blk[r]] = stamp; }
+  };
+  for (int t = 0; t < ntc; ++t) {
+    for (int c = t * TC; c < std::min(P.n_u, (t + 1) * TC); ++c)
+      for (int e = P.guc_ptr[c]; e < P.guc_ptr[c + 1]; ++e) climb(P.guc_row[e], t);
+    for (int r = 0; r < P.n_x; ++r)
+      if (row_mark[r] == t) rowbm[(size_t)t * bmw + r / 32] |= 1u << (r % 32);
+    levLr_ptr[(size_t)t * (nlevL + 1)] = (int)taskLr.size();
+    for (int l = 0; l < nlevL; ++l) {
+      for (int bi = P.levL_ptr[l]; bi < P.levL_ptr[l + 1]; ++bi)
+        if (blk_mark[P.levL_blk[bi]] == t) taskLr.push_back(taskL[bi]);
+      levLr_ptr[(size_t)t * (nlevL + 1) + l + 1] = (int)taskLr.size();
+    }
+  }
+  for (int c = 0; c < P.n_u; ++c)
+    for (int e = P.guc_ptr[c]; e < P.guc_ptr[c + 1]; ++e) climb(P.guc_row[e], ntc);
+  std::vector<int4> taskUa;
+  std::vector<int> levUa_ptr(nlevU + 1, 0);
+  for (int l = 0; l < nlevU; ++l) {
+    for (int bi = P.levU_ptr[l]; bi < P.levU_ptr[l + 1]; ++bi)
+      if (blk_mark[P.levU_blk[bi]] == ntc) taskUa.push_back(taskU[bi]);
+    levUa_ptr[l + 1] = (int)taskUa.size();
+  }
+  d.ntc = ntc; d.bmw = bmw;
+  h->reach_frac_l = taskL.empty() ? 0.0 : (double)taskLr.size() / ((double)ntc * nblk);
+  h->reach_frac_ua = taskU.empty() ? 0.0 : (double)taskUa.size() / nblk;
   std::vector<int4> inc_rec(2 * (size_t)n_l);
   for (int i = 0; i < n_b; ++i)
     for (int e = P.inc_ptr[i]; e < P.inc_ptr[i + 1]; ++e) {
@@ -171,7 +209,9 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
             up(h, P.guc_src, &d.guc_src) && up(h, P.gur_ptr, &d.gur_ptr) && up(h, P.gur_col, &d.gur_col) &&
             up(h, P.gur_src, &d.gur_src) && up(h, P.bus_pth, &d.bus_pth) && up(h, P.bus_pv, &d.bus_pv) &&
             up(h, gbus, &d.gbus) && up(h, rowmeta, &d.rowmeta) && up(h, P.hvp_bus, &d.hvp_bus) &&
-            up(h, inc_rec, &d.inc_rec) && up(h, taskL, &d.taskL) && up(h, taskU, &d.taskU);
+            up(h, inc_rec, &d.inc_rec) && up(h, taskL, &d.taskL) && up(h, taskU, &d.taskU) &&
+            up(h, taskLr, &d.taskLr) && up(h, levLr_ptr, &d.levLr_ptr) && up(h, rowbm, &d.rowbm) &&
+            up(h, taskUa, &d.taskUa) && up(h, levUa_ptr, &d.levUa_ptr);
   Work& w = h->w;
   const size_t S = max_scen;
   w.max_tiles = max_scen * ((max_batch + h->C - 1) / h->C);

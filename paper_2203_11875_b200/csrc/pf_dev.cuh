@@ -28,6 +28,16 @@ struct DevNet {
   const int4 *rowmeta;          // [n_x] {lu_ptr[r], lu_diag[r], lu_ptr[r+1], block of r}
   const int *hvp_bus;           // [n_b] buses in elimination order, the reference bus last
   const int4 *taskL, *taskU;    // [n_blocks] sweep tasks in level order (pf_reduce.cu sweep())
+  // Sparse right-hand sides (Gilbert–Peierls reach): for unit directions the L sweep of
+  // canonical column tile t (columns [tC, tC+C)) only visits the blocks on the
+  // elimination-tree paths from G_u's nonzeros to the root; the Lᵀ sweep of the
+  // adjoint only needs the ancestors of G_u's rows (the projection reads Ψ there).
+  const int4 *taskLr;           // per canonical tile: its L tasks in level order (concatenated)
+  const int *levLr_ptr;         // [ntc][nlevL+1] absolute offsets into taskLr
+  const unsigned *rowbm;        // [ntc][bmw] bitmap of the tile's reach rows (permuted)
+  const int4 *taskUa;           // U-list blocks that are ancestors of a G_u row
+  const int *levUa_ptr;         // [nlevU+1]
+  int ntc, bmw;
   const int4 *inc_rec;          // [2 n_l] per incidence: {line, far θ row, far v row | −1−u, from | 2(gen+1)}
   int C;                        // directions per tile (slab row width)
   int lu_maxlen;                // longest row of the filled LU pattern

@@ -89,10 +89,19 @@ __device__ __forceinline__ double shv(unsigned mask, double2 q, int e) { return 
 
 // acc0[j] -= Σ_{k<n0} v0[o0+k] X[c0[o0+k] + lane + W j], acc1 likewise; the
 // entries are held one per lane in q0 / q1 (all within one fetch of ≤ W).
+// With a reach bitmap bm (SMEM, one bit per slab row), rows outside the reach
+// read as 0 (their slab rows were never written).
+__device__ __forceinline__ bool in_reach(const unsigned* bm, long long colC, int log2C) {
+  const int r = (int)(colC >> log2C);
+  return (bm[r >> 5] >> (r & 31)) & 1u;
+}
+
 template <int C>
 __device__ __forceinline__ void dot2(const double* X, unsigned mask, int lane, double2 q0, int o0, int n0,
-                                     double2 q1, int o1, int n1, double* acc0, double* acc1) {
+                                     double2 q1, int o1, int n1, double* acc0, double* acc1,
+                                     const unsigned* bm = nullptr) {
   constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL, DW = Geo<C>::DW;
+  constexpr int L2C = C == 8 ? 3 : C == 16 ? 4 : C == 32 ? 5 : 6;
   const int m = max(n0, n1);
   for (int e0 = 0; e0 < m; e0 += DW) {
     double x0[DW][CPL], x1[DW][CPL];
@@ -101,10 +110,12 @@ __device__ __forceinline__ void dot2(const double* X, unsigned mask, int lane, d
       const int i0 = (o0 + e0 + k) & (W - 1), i1 = (o1 + e0 + k) & (W - 1);
       const long long c0 = __double_as_longlong(__shfl_sync(mask, q0.y, i0, W));
       const long long c1 = __double_as_longlong(__shfl_sync(mask, q1.y, i1, W));
+      const bool ok0 = e0 + k < n0 && (!bm || in_reach(bm, c0, L2C));
+      const bool ok1 = e0 + k < n1 && (!bm || in_reach(bm, c1, L2C));
 #pragma unroll
       for (int j = 0; j < CPL; ++j) {
-        x0[k][j] = e0 + k < n0 ? X[c0 + lane + W * j] : 0.0;
-        x1[k][j] = e0 + k < n1 ? X[c1 + lane + W * j] : 0.0;
+        x0[k][j] = ok0 ? X[c0 + lane + W * j] : 0.0;
+        x1[k][j] = ok1 ? X[c1 + lane + W * j] : 0.0;
       }
     }
 #pragma unroll
@@ -125,12 +136,12 @@ __device__ __forceinline__ void dot2(const double* X, unsigned mask, int lane, d
 // chunks of W entries, no prefetch.
 template <int C>
 __device__ __forceinline__ void dot_long(const double2* __restrict__ pk, const double* X, unsigned mask, int lane,
-                                         int s, int n, double* acc) {
+                                         int s, int n, double* acc, const unsigned* bm = nullptr) {
   constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
   double dummy[CPL];
   for (int base = 0; base < n; base += W) {
     const double2 q = fetch(pk, s + base, n - base, lane);
-    dot2<C>(X, mask, lane, q, 0, min(W, n - base), q, 0, 0, acc, dummy);
+    dot2<C>(X, mask, lane, q, 0, min(W, n - base), q, 0, 0, acc, dummy, bm);
   }
 }
 
@@ -138,6 +149,8 @@ __device__ __forceinline__ void dot_long(const double2* __restrict__ pk, const d
 // right-hand side B = −P G_u V computed on the fly from G_u's row, so the slab
 // needs no zero-fill pass.
 struct FromSlab {};
+// U sweep after a reach-restricted L sweep: rows outside the reach start at 0
+struct FromSlabReach { const unsigned* bm; };
 template <int C>
 struct FromRhs {
   const int* gur_ptr; const int* gur_col; const int* gur_src; const double* gu;
@@ -160,11 +173,10 @@ struct FromRhs {
 };
 
 template <int C, bool LOWER, class Init = FromSlab>
-__device__ __forceinline__ void sweep(const DevNet& n, const int4* __restrict__ tasks, const double2* __restrict__ pk,
-                                      double* X, bool divide, int lane, int team, int nteam, Init init = Init()) {
+__device__ __forceinline__ void sweep(const int4* __restrict__ tasks, const int* __restrict__ lptr, int nlev,
+                                      const double2* __restrict__ pk, double* X, bool divide, int lane, int team,
+                                      int nteam, Init init = Init(), const unsigned* bm = nullptr) {
   constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
-  const int nlev = LOWER ? n.nlevL : n.nlevU;
-  const int* lptr = LOWER ? n.levL_ptr : n.levU_ptr;
   const unsigned mask = team_mask<W>();
   for (int lev = 0; lev < nlev; ++lev) {
     const int b1 = __ldg(lptr + lev + 1);
@@ -190,6 +202,11 @@ __device__ __forceinline__ void sweep(const DevNet& n, const int4* __restrict__ 
       if constexpr (std::is_same<Init, FromSlab>::value) {
 #pragma unroll
         for (int j = 0; j < CPL; ++j) { a0[j] = x0p[W * j]; a1[j] = k.two ? x1p[W * j] : 0.0; }
+      } else if constexpr (std::is_same<Init, FromSlabReach>::value) {
+        const bool in0 = (init.bm[k.r0 >> 5] >> (k.r0 & 31)) & 1u;
+        const bool in1 = k.two && ((init.bm[(k.r0 + 1) >> 5] >> ((k.r0 + 1) & 31)) & 1u);
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) { a0[j] = in0 ? x0p[W * j] : 0.0; a1[j] = in1 ? x1p[W * j] : 0.0; }
       } else {
         init(k.r0, a0);
         if (k.two) {
@@ -203,10 +220,10 @@ __device__ __forceinline__ void sweep(const DevNet& n, const int4* __restrict__ 
       if (LOWER) {
         const int n0 = k.c0 - 1, n1 = k.two ? k.c1 - 2 : 0;      // entries before diag / intra
         if (fits) {
-          dot2<C>(X, mask, lane, q0, 0, n0, q1, 0, n1, a0, a1);
+          dot2<C>(X, mask, lane, q0, 0, n0, q1, 0, n1, a0, a1, bm);
         } else {
-          dot_long<C>(pk, X, mask, lane, k.s0, n0, a0);
-          if (k.two) dot_long<C>(pk, X, mask, lane, k.s1, n1, a1);
+          dot_long<C>(pk, X, mask, lane, k.s0, n0, a0, bm);
+          if (k.two) dot_long<C>(pk, X, mask, lane, k.s1, n1, a1, bm);
         }
         const double d0 = fits ? shv<W>(mask, q0, (k.c0 - 1) & (W - 1)) : ldpk(pk + k.s0 + k.c0 - 1).x;
         double intra = 0.0, d1 = 1.0;
@@ -312,8 +329,10 @@ __device__ __forceinline__ void load_j(const double* p, double* j) {
 
 // ---------------------------------------------------------------- a, b
 template <int C>
-__global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Work w, const double* __restrict__ V, int col0, int N) {
+__global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Work w, const double* __restrict__ V, int col0,
+                                                                   int N, int rt) {
   constexpr int W = Geo<C>::W;
+  extern __shared__ unsigned bm_sm[];  // reach bitmap of this tile (rt ≥ 0)
   const int ntile = (N + C - 1) / C;
   const int tile = blockIdx.x, s = blockIdx.y;
   const size_t cta = (size_t)s * ntile + tile;
@@ -328,8 +347,18 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
   rhs.gur_ptr = n.gur_ptr; rhs.gur_col = n.gur_col; rhs.gur_src = n.gur_src; rhs.gu = gu;
   rhs.Vs = V ? V + ((size_t)s * N + tile * C + lane) * n_u : nullptr;
   rhs.base = col0 + tile * C; rhs.nvalid = nvalid; rhs.n_u = n_u; rhs.lane = lane;
-  sweep<C, true>(n, n.taskL, pk, X, false, lane, team, nteam, rhs);   // L^{-1} B
-  sweep<C, false>(n, n.taskU, pk, X, true, lane, team, nteam);   // U^{-1}
+  if (rt >= 0) {
+    // sparse RHS: only the tile's reach (tree paths of its columns' G_u rows) is nonzero
+    const unsigned* bmg = n.rowbm + (size_t)(rt + tile) * n.bmw;
+    for (int i = threadIdx.x; i < n.bmw; i += blockDim.x) bm_sm[i] = __ldg(bmg + i);
+    __syncthreads();
+    sweep<C, true>(n.taskLr, n.levLr_ptr + (size_t)(rt + tile) * (n.nlevL + 1), n.nlevL, pk, X, false, lane, team,
+                   nteam, rhs, bm_sm);                                                            // L^{-1} B
+    sweep<C, false>(n.taskU, n.levU_ptr, n.nlevU, pk, X, true, lane, team, nteam, FromSlabReach{bm_sm});  // U^{-1}
+  } else {
+    sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, X, false, lane, team, nteam, rhs);   // L^{-1} B
+    sweep<C, false>(n.taskU, n.levU_ptr, n.nlevU, pk, X, true, lane, team, nteam);       // U^{-1}
+  }
 }
 
 // ---------------------------------------------------------------- c1
@@ -476,8 +505,9 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_adj(DevNet n, Wor
   const double* Hs = w.hu + cta * n_u * C;
   const double* gu = w.gu + (size_t)s * n.nnz_gu;
   const double2* pk = w.pkT + (size_t)s * n.nnz_lu;
-  sweep<C, true>(n, n.taskL, pk, Y, true, lane, team, nteam);    // U^{-T}
-  sweep<C, false>(n, n.taskU, pk, Y, false, lane, team, nteam);  // L^{-T}
+  sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, Y, true, lane, team, nteam);        // U^{-T}
+  // L^{-T}: only the ancestors of G_u's rows (the projection reads Ψ there)
+  sweep<C, false>(n.taskUa, n.levUa_ptr, n.nlevU, pk, Y, false, lane, team, nteam);
   for (int c0 = 0; c0 < n_u; c0 += kCH) {
     for (int cc = team; cc < kCH && c0 + cc < n_u; cc += nteam) {
       const int c = c0 + cc;
@@ -509,7 +539,8 @@ void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int
                 cudaStream_t st, cudaEvent_t* ev) {
   const int ntile = (N + C - 1) / C;
   if (ev) cudaEventRecord(ev[0], st);
-  k_fwd<C><<<dim3(ntile, n_scen), kThreads, 0, st>>>(n, w, V, col0, N);
+  const int rt = (V == nullptr && col0 % C == 0) ? col0 / C : -1;  // canonical tile of the call's first tile
+  k_fwd<C><<<dim3(ntile, n_scen), kThreads, rt >= 0 ? n.bmw * sizeof(unsigned) : 0, st>>>(n, w, V, col0, N, rt);
   if (ev) cudaEventRecord(ev[1], st);
   k_mu<C><<<dim3((n.n_gb + kBusPerCta - 1) / kBusPerCta, ntile, n_scen), kThreads, 0, st>>>(n, w, V, col0, N);
   if (ev) cudaEventRecord(ev[2], st);
