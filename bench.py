@@ -51,8 +51,11 @@ def parse():
     ap.add_argument("--config", default="case9241x8", choices=list(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-generic", action="store_true", help="skip the dense-V generic-HVP timing")
     ap.add_argument("--profile-steps", type=int, default=0, help="run N untimed steps and exit (for ncu)")
     ap.add_argument("--delta-w", type=float, default=None, help="skip the regularisation search (profiling)")
+    ap.add_argument("--pipelines", type=int, default=1,
+                    help="scenario groups run as independent handle+stream pipelines (scenario mode)")
     return ap.parse_args()
 
 
@@ -212,7 +215,13 @@ def main():
     n_u, n_x, m = tmp.dims["n_u"], tmp.dims["n_x"], tmp.dims["m"]
     tmp.close()
     col0, ncols, cpad = column_partition(n_u, world, rank) if directions else (0, n_u, n_u)
-    h = Network(net, max_batch=max(cpad, 1), max_scen=S, device=local)
+    # P independent pipelines (one handle + one stream each) over contiguous scenario
+    # groups: the latency-bound phases of one group (LU refactor, Cholesky chain)
+    # overlap the bandwidth-bound reduction of the other.
+    P = args.pipelines if (not directions and S % max(args.pipelines, 1) == 0) else 1
+    Sg = S // P
+    hs = [Network(net, max_batch=max(cpad, 1), max_scen=Sg, device=local) for _ in range(P)]
+    h = hs[0]
     h.profile(True)
     d = h.dims
 
@@ -231,26 +240,45 @@ def main():
     rhs = torch.empty(S, n_u, dtype=f64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    streams = [stream] if P == 1 else [torch.cuda.Stream(dev) for _ in range(P)]
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     def step(t, red_ev=None, chol_ev=None):
-        h.pf_eval_constraints(S, t["v"], t["theta"], t["p_g"], t["q_g"], t["p_d"], t["q_d"], G, H)
-        h.pf_jacobian(S, t["v"], t["theta"], info=info_j)
-        if red_ev:
-            red_ev[0].record(stream)
-        if ncols > 0:  # direction mode has S = 1, so KV[:, :ncols] is contiguous
-            h.pf_reduced_hessian_batch(S, t["v"], t["theta"], t["lam"], t["y"], KV[:, :ncols], sigma_s=t["sigma_s"],
-                                       sigma_x=t["sigma_x"], col0=col0, N=ncols, p_d=t["p_d"])
-        if red_ev:
-            red_ev[1].record(stream)
-        K = allgather_columns(KV, n_u) if (directions and world > 1) else KV
+        go = torch.cuda.Event()
+        go.record(stream)
         rhs.copy_(t["rhs"])
-        if chol_ev:
-            chol_ev[0].record(stream)
-        h.pf_condensed_kkt_solve(S, K, t["sigma_u"], delta_w, rhs, 1, info_c)
-        if chol_ev:
-            chol_ev[1].record(stream)
-        return K
+        done = []
+        for g, (hg, sg) in enumerate(zip(hs, streams)):
+            a, b = g * Sg, (g + 1) * Sg
+            sl = {k: v[a:b] for k, v in t.items()}
+            sg.wait_event(go)
+            if sg is not stream:
+                sg.wait_stream(stream)
+            with torch.cuda.stream(sg):
+                hg.pf_eval_constraints(Sg, sl["v"], sl["theta"], sl["p_g"], sl["q_g"], sl["p_d"], sl["q_d"],
+                                       G[a:b], H[a:b])
+                hg.pf_jacobian(Sg, sl["v"], sl["theta"], info=info_j[a:b])
+                if red_ev and g == 0:
+                    red_ev[0].record(sg)
+                if ncols > 0:  # direction mode has S = 1, so KV[:, :ncols] is contiguous
+                    hg.pf_reduced_hessian_batch(Sg, sl["v"], sl["theta"], sl["lam"], sl["y"], KV[a:b, :ncols],
+                                                sigma_s=sl["sigma_s"], sigma_x=sl["sigma_x"], col0=col0, N=ncols,
+                                                p_d=sl["p_d"])
+                if red_ev and g == 0:
+                    red_ev[1].record(sg)
+                K = allgather_columns(KV, n_u) if (directions and world > 1) else KV[a:b]
+                if chol_ev and g == 0:
+                    chol_ev[0].record(sg)
+                hg.pf_condensed_kkt_solve(Sg, K, sl["sigma_u"], delta_w, rhs[a:b], 1, info_c[a:b])
+                if chol_ev and g == 0:
+                    chol_ev[1].record(sg)
+            if sg is not stream:
+                e = torch.cuda.Event()
+                e.record(sg)
+                done.append(e)
+        for e in done:
+            stream.wait_event(e)
+        return KV
 
     # ------------------------------------------------------------ δ_w: the paper's regularisation until PD
     delta_w = 0.0 if args.delta_w is None else args.delta_w
@@ -273,7 +301,7 @@ def main():
         step(devt)
     torch.cuda.synchronize()
     # ------------------------------------------------------------ timed loop (device-resident inputs)
-    launches0 = h.launch_count()
+    launches0 = sum(x.launch_count() for x in hs)
     step_ms, red_ms, chol_ms = [], [], []
     kern = {k: [] for k in h.KERNELS}
     with ClockSampler(local) as clk:
@@ -296,7 +324,7 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-    launches = h.launch_count() - launches0
+    launches = sum(x.launch_count() for x in hs) - launches0
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms, statistics.mean(red_ms), statistics.mean(chol_ms)], dtype=f64, device=dev)
     hv = torch.tensor([S * ncols], dtype=f64, device=dev)
@@ -306,6 +334,27 @@ def main():
     total_ms, red_avg, chol_avg = t.tolist()
     hvps_per_step = hv.item()
     value = hvps_per_step * args.steps / (total_ms / 1e3)
+
+    # ------------------------------------------------------------ generic-HVP variant: dense V ~ N(0,1)
+    generic = None
+    if ncols > 0 and not args.no_generic:
+        gen = torch.Generator(device=dev).manual_seed(7)
+        Vd = torch.randn(Sg, ncols, n_u, generator=gen, dtype=f64, device=dev)
+        gms = []
+        for k in range(args.warmup + args.steps):
+            flush.fill_(1.0)
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+            h.pf_reduced_hessian_batch(Sg, devt["v"][:Sg], devt["theta"][:Sg], devt["lam"][:Sg], devt["y"][:Sg],
+                                       KV[:Sg, :ncols], sigma_s=devt["sigma_s"][:Sg], sigma_x=devt["sigma_x"][:Sg],
+                                       V=Vd, N=ncols, p_d=devt["p_d"][:Sg])
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if k >= args.warmup:
+                gms.append(e0.elapsed_time(e1))
+        del Vd
+        generic = {"value": Sg * ncols / (statistics.mean(gms) / 1e3), "unit": "HVP/s", "ms": statistics.mean(gms),
+                   "directions": Sg * ncols, "V": "dense N(0,1), seed 7 (A7.1 a real SpMM)"}
 
     # ------------------------------------------------------------ end-to-end through the public API, host buffers
     e2e = None
@@ -348,14 +397,20 @@ def main():
     # ------------------------------------------------------------ roofline of the dominant kernel
     peaks = read_peaks()
     hbm = peaks.get("hbm_gbs")
-    dirs = S * ncols
-    # algorithmic DRAM bytes per direction of each kernel: slab rows
-    # written/read once per pass; factors, network and line state are per-launch
-    # constants (L2-resident) and are not counted.
-    per_dir = {"k_fwd": 8.0 * 5 * n_x,                    # zero-fill + L sweep (r+w) + U sweep (r+w)
-               "k_mu": 8.0 * 2 * n_g,                     # μ_A rows written (Z reads hit L2)
-               "k_hvp": 8.0 * (2 * n_x + n_u),            # Z read, H_x write, H_u write
-               "k_adj": 8.0 * (5 * n_x + 2 * n_u),        # Uᵀ, Lᵀ sweeps (r+w), Ψ read, H_u read, K̂V write
+    dirs = Sg * ncols  # per launch: the kernels of pipeline 0 (its Sg scenarios)
+    # algorithmic DRAM bytes per direction of each kernel: each slab row a
+    # kernel must produce is written once and each row it must consume is read once
+    # (gathers assumed cached); factors, network and line state are per-launch
+    # constants (L2-resident) and are not counted.  The forward L sweep only visits
+    # the tile's sparse-RHS reach (r rows), the Lᵀ sweep the ancestors of G_u's rows (a).
+    ntc = -(-n_u // d["tile_cols"])
+    r_mean = d["reach_rows_l"] / ntc if d["reach_rows_l"] else n_x
+    a_rows = d["reach_rows_ua"] or n_x
+    g_rows = d["gu_rows"] or n_x
+    per_dir = {"k_fwd": 8.0 * (2 * r_mean + n_x),             # L sweep writes r rows; U reads them, writes Z
+               "k_mu": 8.0 * 2 * n_g,                         # μ_A rows written (Z reads hit L2)
+               "k_hvp": 8.0 * (2 * n_x + n_u),                # Z read, H_x write, H_u write
+               "k_adj": 8.0 * (2 * n_x + 2 * a_rows + g_rows + 2 * n_u),  # Uᵀ r+w, Lᵀ r+w on a rows, Ψ at G_u rows, H_u, K̂V
                "k_lu": None}
     kstats = {}
     for k, v in kern.items():
@@ -396,10 +451,12 @@ def main():
                    "scenarios_per_gpu": S, "directions_per_step": int(hvps_per_step),
                    "tile_cols": d["tile_cols"], "levels_l": d["n_levels_l"], "levels_u": d["n_levels_u"],
                    "nnz_lu": d["nnz_lu"], "delta_w": delta_w,
+                   "pipelines_per_gpu": P,
                    "parallelism": ("scenario-sharded x%d" % world) if cfg["mode"] == "scenarios"
                    else ("direction-sharded x%d + NCCL all-gather" % world),
                    "l2": "flushed between steps (256 MiB write outside the timed region)"},
         "chol_ms_per_iter": chol_avg, "reduction_ms_per_iter": red_avg,
+        "generic_hvp": generic,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

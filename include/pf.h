@@ -59,6 +59,11 @@ typedef struct {
   int32_t n_blocks;               /* bus blocks (θ_i[, v_i]) of the ordering    */
   int32_t n_levels_l, n_levels_u; /* block level sets of the L / U sweeps       */
   int32_t max_batch, max_scen, tile_cols;
+  /* sparse right-hand sides (device handles; 0 for host-only ones): rows the
+     forward L sweep visits, summed over the canonical column tiles of width
+     tile_cols; rows the adjoint Lᵀ sweep visits (ancestors of G_u's rows);
+     distinct rows of G_u (where the projection G_uᵀΨ reads Ψ). */
+  int32_t reach_rows_l, reach_rows_ua, gu_rows;
 } pf_dims;
 
 /* Host copies of the integer structure, for bit-exact tests (R19, P15). */

@@ -23,7 +23,7 @@ struct pf_net {
   std::string err;
   long long launches = 0;
   bool prof = false;         // instrumentation: events around the hot kernels
-  double reach_frac_l = 0.0, reach_frac_ua = 0.0;  // visited fraction of the L / Lᵀ sweep blocks
+  int reach_rows_l = 0, reach_rows_ua = 0, gu_rows = 0;  // sparse-RHS statistics (pf_dims)
   cudaEvent_t ev[8] = {};    // [0..4] reduction kernels, [5..6] k_lu
 };
 
@@ -179,8 +179,9 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
     levUa_ptr[l + 1] = (int)taskUa.size();
   }
   d.ntc = ntc; d.bmw = bmw;
-  h->reach_frac_l = taskL.empty() ? 0.0 : (double)taskLr.size() / ((double)ntc * nblk);
-  h->reach_frac_ua = taskU.empty() ? 0.0 : (double)taskUa.size() / nblk;
+  for (size_t k = 0; k < rowbm.size(); ++k) h->reach_rows_l += __builtin_popcount(rowbm[k]);
+  for (int r = 0; r < P.n_x; ++r) h->reach_rows_ua += row_mark[r] == ntc;
+  for (int r = 0; r < P.n_x; ++r) h->gu_rows += P.gur_ptr[r + 1] > P.gur_ptr[r];
   std::vector<int4> inc_rec(2 * (size_t)n_l);
   for (int i = 0; i < n_b; ++i)
     for (int e = P.inc_ptr[i]; e < P.inc_ptr[i + 1]; ++e) {
@@ -254,6 +255,7 @@ pf_status pf_query(const pf_net* h, pf_dims* o) {
   o->nnz_lu = (int)P.lu_idx.size(); o->n_blocks = (int)P.blk_bus.size();
   o->n_levels_l = (int)P.levL_ptr.size() - 1; o->n_levels_u = (int)P.levU_ptr.size() - 1;
   o->max_batch = h->max_batch; o->max_scen = h->max_scen; o->tile_cols = h->C;
+  o->reach_rows_l = h->reach_rows_l; o->reach_rows_ua = h->reach_rows_ua; o->gu_rows = h->gu_rows;
   return PF_OK;
 }
 

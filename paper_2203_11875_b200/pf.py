@@ -37,7 +37,8 @@ class PFError(RuntimeError):
 class pf_dims(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "n_b", "n_l", "n_g", "n_x", "n_u", "m", "n_r", "n_h", "ref_bus", "ref_gen", "nnz_gx", "nnz_gu", "nnz_a",
-        "nnz_lu", "n_blocks", "n_levels_l", "n_levels_u", "max_batch", "max_scen", "tile_cols")]
+        "nnz_lu", "n_blocks", "n_levels_l", "n_levels_u", "max_batch", "max_scen", "tile_cols",
+        "reach_rows_l", "reach_rows_ua", "gu_rows")]
 
 
 _lib = None

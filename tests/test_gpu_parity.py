@@ -179,6 +179,37 @@ def test_batch_invariance_bitwise(pfmod, name, net, pts):
 
 
 @pytest.mark.parametrize("name", ["case118", "case1354"])
+def test_tile_width_invariance_bitwise(pfmod, name, monkeypatch):
+    """64-direction tiles (two directions per lane, the bench's launch shape) and
+    8-direction tiles (teams of 8 lanes) run the same arithmetic per direction,
+    so K̂ is bit-identical across tile widths, for unit directions
+    in aligned (sparse-RHS reach) and unaligned calls and for dense V, and it
+    matches the oracle."""
+    import torch
+    net, pt = table1_grid(name)
+    pts = [pt, make_scenario(net, pt, 1)]
+    n_u = O.partition(net)["n_u"]
+    outs = {}
+    rng = np.random.default_rng(21)
+    Vd = rng.standard_normal((len(pts), 70, n_u))
+    for c in ("8", "64"):
+        monkeypatch.setenv("PF_TILE_COLS", c)
+        h = pfmod.Network(net, max_batch=n_u, max_scen=len(pts))
+        assert h.dims["tile_cols"] == int(c)
+        full, _ = _run_khat(pfmod, h, net, pts)
+        part, _ = _run_khat(pfmod, h, net, pts, N=70, col0=37)      # unaligned: full L sweep
+        dense, _ = _run_khat(pfmod, h, net, pts, N=70, V=dev(Vd))  # dense directions
+        outs[c] = (full, part, dense)
+        h.close()
+    for a, b in zip(outs["8"], outs["64"]):
+        assert np.array_equal(a, b)
+    full = outs["64"][0]
+    assert np.array_equal(outs["64"][1], full[:, 37:107])
+    for s, p in enumerate(pts):
+        assert rel_err(full[s].T, oracle_khat(net, p)[0]) <= TOL
+
+
+@pytest.mark.parametrize("name", ["case118", "case1354"])
 def test_condensed_kkt_solve(pfmod, name):
     """K_cond = sym(K̂) + diag(Σ_u) + δ_w I: L and the solve vs the oracle's
     textbook Cholesky; info for an indefinite shift equals the oracle's.
