@@ -91,9 +91,22 @@ __device__ __forceinline__ double shv(unsigned mask, double2 q, int e) { return 
 // entries are held one per lane in q0 / q1 (all within one fetch of ≤ W).
 // With a reach bitmap bm (SMEM, one bit per slab row), rows outside the reach
 // read as 0 (their slab rows were never written).
-__device__ __forceinline__ bool in_reach(const unsigned* bm, long long colC, int log2C) {
-  const int r = (int)(colC >> log2C);
+__device__ __forceinline__ bool in_reach(const unsigned* bm, int colC, int log2C) {
+  const int r = colC >> log2C;
   return (bm[r >> 5] >> (r & 31)) & 1u;
+}
+
+// Lane l of a team owns the CPL adjacent directions l·CPL … l·CPL + CPL − 1, so a
+// gathered row piece is one 16-byte load for CPL = 2.
+template <int CPL>
+__device__ __forceinline__ void ld_dirs(const double* p, bool ok, double* x) {
+  if constexpr (CPL == 2) {
+    const double2 v = ok ? *reinterpret_cast<const double2*>(p) : make_double2(0.0, 0.0);
+    x[0] = v.x; x[1] = v.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) x[j] = ok ? p[j] : 0.0;
+  }
 }
 
 template <int C>
@@ -108,15 +121,12 @@ __device__ __forceinline__ void dot2(const double* X, unsigned mask, int lane, d
 #pragma unroll
     for (int k = 0; k < DW; ++k) {
       const int i0 = (o0 + e0 + k) & (W - 1), i1 = (o1 + e0 + k) & (W - 1);
-      const long long c0 = __double_as_longlong(__shfl_sync(mask, q0.y, i0, W));
-      const long long c1 = __double_as_longlong(__shfl_sync(mask, q1.y, i1, W));
+      const int c0 = __shfl_sync(mask, __double2loint(q0.y), i0, W);  // column · C (< 2^31)
+      const int c1 = __shfl_sync(mask, __double2loint(q1.y), i1, W);
       const bool ok0 = e0 + k < n0 && (!bm || in_reach(bm, c0, L2C));
       const bool ok1 = e0 + k < n1 && (!bm || in_reach(bm, c1, L2C));
-#pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        x0[k][j] = ok0 ? X[c0 + lane + W * j] : 0.0;
-        x1[k][j] = ok1 ? X[c1 + lane + W * j] : 0.0;
-      }
+      ld_dirs<CPL>(X + c0 + lane * CPL, ok0, x0[k]);
+      ld_dirs<CPL>(X + c1 + lane * CPL, ok1, x1[k]);
     }
 #pragma unroll
     for (int k = 0; k < DW; ++k) {
@@ -154,10 +164,10 @@ struct FromSlabReach { const unsigned* bm; };
 template <int C>
 struct FromRhs {
   const int* gur_ptr; const int* gur_col; const int* gur_src; const double* gu;
-  const double* Vs;  // dense V rows of this lane's first direction (stride n_u per W directions), or null = unit
+  const double* Vs;  // dense V row of this lane's first direction (the next ones follow at stride n_u), or null = unit
   int base, nvalid, n_u, lane;  // base = col0 + tile*C: the u column of direction 0 of the tile
   __device__ __forceinline__ void operator()(int r, double* a) const {
-    constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
+    constexpr int CPL = Geo<C>::CPL;
 #pragma unroll
     for (int j = 0; j < CPL; ++j) a[j] = 0.0;
     for (int e = __ldg(gur_ptr + r); e < __ldg(gur_ptr + r + 1); ++e) {
@@ -165,8 +175,8 @@ struct FromRhs {
       const double g = gu[__ldg(gur_src + e)];
 #pragma unroll
       for (int j = 0; j < CPL; ++j) {
-        const int jl = lane + W * j;
-        if (jl < nvalid) a[j] -= g * (Vs ? Vs[(size_t)W * j * n_u + c] : (c == base + jl ? 1.0 : 0.0));
+        const int jl = lane * CPL + j;
+        if (jl < nvalid) a[j] -= g * (Vs ? Vs[(size_t)j * n_u + c] : (c == base + jl ? 1.0 : 0.0));
       }
     }
   }
@@ -196,17 +206,17 @@ __device__ __forceinline__ void sweep(const int4* __restrict__ tasks, const int*
         nq0 = fetch(pk, nk.s0, nk.c0, lane);
         if (nk.two) nq1 = fetch(pk, nk.s1, nk.c1, lane);
       }
-      double* x0p = X + (size_t)k.r0 * C + lane;
+      double* x0p = X + (size_t)k.r0 * C + lane * CPL;
       double* x1p = x0p + C;
       double a0[CPL], a1[CPL];
       if constexpr (std::is_same<Init, FromSlab>::value) {
 #pragma unroll
-        for (int j = 0; j < CPL; ++j) { a0[j] = x0p[W * j]; a1[j] = k.two ? x1p[W * j] : 0.0; }
+        for (int j = 0; j < CPL; ++j) { a0[j] = x0p[j]; a1[j] = k.two ? x1p[j] : 0.0; }
       } else if constexpr (std::is_same<Init, FromSlabReach>::value) {
         const bool in0 = (init.bm[k.r0 >> 5] >> (k.r0 & 31)) & 1u;
         const bool in1 = k.two && ((init.bm[(k.r0 + 1) >> 5] >> ((k.r0 + 1) & 31)) & 1u);
 #pragma unroll
-        for (int j = 0; j < CPL; ++j) { a0[j] = in0 ? x0p[W * j] : 0.0; a1[j] = in1 ? x1p[W * j] : 0.0; }
+        for (int j = 0; j < CPL; ++j) { a0[j] = in0 ? x0p[j] : 0.0; a1[j] = in1 ? x1p[j] : 0.0; }
       } else {
         init(k.r0, a0);
         if (k.two) {
@@ -235,11 +245,11 @@ __device__ __forceinline__ void sweep(const int4* __restrict__ tasks, const int*
         for (int j = 0; j < CPL; ++j) {
           double x0 = a0[j];
           if (divide) x0 /= d0;
-          x0p[W * j] = x0;
+          x0p[j] = x0;
           if (k.two) {
             double x1 = a1[j] - intra * x0;
             if (divide) x1 /= d1;
-            x1p[W * j] = x1;
+            x1p[j] = x1;
           }
         }
       } else {
@@ -264,11 +274,11 @@ __device__ __forceinline__ void sweep(const int4* __restrict__ tasks, const int*
           if (k.two) {
             x1 = a1[j];
             if (divide) x1 /= d1;
-            x1p[W * j] = x1;
+            x1p[j] = x1;
           }
           double x0 = a0[j] - intra * x1;
           if (divide) x0 /= d0;
-          x0p[W * j] = x0;
+          x0p[j] = x0;
         }
       }
     }
@@ -345,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
   // A7.1 fused into the first sweep: B = −P G_u V row by row (unit V: G_u's column col0 + j)
   FromRhs<C> rhs;
   rhs.gur_ptr = n.gur_ptr; rhs.gur_col = n.gur_col; rhs.gur_src = n.gur_src; rhs.gu = gu;
-  rhs.Vs = V ? V + ((size_t)s * N + tile * C + lane) * n_u : nullptr;
+  rhs.Vs = V ? V + ((size_t)s * N + tile * C + lane * Geo<C>::CPL) * n_u : nullptr;
   rhs.base = col0 + tile * C; rhs.nvalid = nvalid; rhs.n_u = n_u; rhs.lane = lane;
   if (rt >= 0) {
     // sparse RHS: only the tile's reach (tree paths of its columns' G_u rows) is nonzero
