@@ -142,6 +142,50 @@ __device__ __forceinline__ void dot2(const double* X, unsigned mask, int lane, d
   }
 }
 
+// As dot2, with the block's entries in SMEM (e0[i] = entry i of row 0, read as a
+// broadcast): no shuffles, and the prefetched entries hold no registers, so a
+// whole row's gathers (up to DS per batch) are in flight at once.
+#ifndef PF_DOT_S
+#define PF_DOT_S 2
+#endif
+template <int C>
+__device__ __forceinline__ void dot2s(const double* X, int lane, const double2* e0, int n0, const double2* e1, int n1,
+                                      double* acc0, double* acc1, const unsigned* bm = nullptr) {
+  constexpr int CPL = Geo<C>::CPL, DS = PF_DOT_S;
+  constexpr int L2C = C == 8 ? 3 : C == 16 ? 4 : C == 32 ? 5 : 6;
+  const int m = max(n0, n1);
+  for (int b = 0; b < m; b += DS) {
+    double x0[DS][CPL], x1[DS][CPL];
+#pragma unroll
+    for (int k = 0; k < DS; ++k) {
+      const int c0 = b + k < n0 ? __double2loint(e0[b + k].y) : 0;  // column · C (< 2^31)
+      const int c1 = b + k < n1 ? __double2loint(e1[b + k].y) : 0;
+      const bool ok0 = b + k < n0 && (!bm || in_reach(bm, c0, L2C));
+      const bool ok1 = b + k < n1 && (!bm || in_reach(bm, c1, L2C));
+      ld_dirs<CPL>(X + c0 + lane * CPL, ok0, x0[k]);
+      ld_dirs<CPL>(X + c1 + lane * CPL, ok1, x1[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < DS; ++k) {
+      const double v0 = b + k < n0 ? e0[b + k].x : 0.0;
+      const double v1 = b + k < n1 ? e1[b + k].x : 0.0;
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        acc0[j] -= v0 * x0[k][j];
+        acc1[j] -= v1 * x1[k][j];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_ent(double2* dst, const double2* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N_>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N_) : "memory"); }
+
 // Rows longer than one fetch (separator rows of the L part): acc[j] -= Σ in
 // chunks of W entries, no prefetch.
 template <int C>
@@ -185,27 +229,32 @@ struct FromRhs {
 template <int C, bool LOWER, class Init = FromSlab>
 __device__ __forceinline__ void sweep(const int4* __restrict__ tasks, const int* __restrict__ lptr, int nlev,
                                       const double2* __restrict__ pk, double* X, bool divide, int lane, int team,
-                                      int nteam, Init init = Init(), const unsigned* bm = nullptr) {
+                                      int nteam, double2* ent, Init init = Init(), const unsigned* bm = nullptr) {
+  // ent: this team's entry buffers [2][2 rows][W] (double buffer, filled by cp.async)
   constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
   const unsigned mask = team_mask<W>();
+  auto fits = [](const Task& k) { return k.c0 <= W && k.c1 <= W; };
+  auto fill = [&](const Task& k, double2* e) {  // lane-parallel copy of the block's entry ranges
+    if (lane < k.c0) cp_ent(e + lane, pk + k.s0 + lane);
+    if (k.two && lane < k.c1) cp_ent(e + W + lane, pk + k.s1 + lane);
+  };
   for (int lev = 0; lev < nlev; ++lev) {
     const int b1 = __ldg(lptr + lev + 1);
     int bi = __ldg(lptr + lev) + team;
-    Task nk;
-    double2 nq0 = make_double2(0.0, 0.0), nq1 = nq0;
+    int buf = 0;
+    Task k, nk;
     if (bi < b1) {
-      nk = unpack(__ldg(tasks + bi));
-      nq0 = fetch(pk, nk.s0, nk.c0, lane);
-      if (nk.two) nq1 = fetch(pk, nk.s1, nk.c1, lane);
+      k = unpack(__ldg(tasks + bi));
+      if (fits(k)) fill(k, ent);
+      cp_commit();
+      if (bi + nteam < b1) nk = unpack(__ldg(tasks + bi + nteam));
     }
     for (; bi < b1; bi += nteam) {
-      const Task k = nk;
-      const double2 q0 = nq0, q1 = nq1;
-      if (bi + nteam < b1) {  // prefetch the next block of this team
-        nk = unpack(__ldg(tasks + bi + nteam));
-        nq0 = fetch(pk, nk.s0, nk.c0, lane);
-        if (nk.two) nq1 = fetch(pk, nk.s1, nk.c1, lane);
-      }
+      const bool hn = bi + nteam < b1;
+      if (hn && fits(nk)) fill(nk, ent + (buf ^ 1) * 2 * W);  // next block's entries in flight
+      cp_commit();
+      Task nnk = nk;
+      if (bi + 2 * nteam < b1) nnk = unpack(__ldg(tasks + bi + 2 * nteam));
       double* x0p = X + (size_t)k.r0 * C + lane * CPL;
       double* x1p = x0p + C;
       double a0[CPL], a1[CPL];
@@ -226,20 +275,24 @@ __device__ __forceinline__ void sweep(const int4* __restrict__ tasks, const int*
           for (int j = 0; j < CPL; ++j) a1[j] = 0.0;
         }
       }
-      const bool fits = k.c0 <= W && k.c1 <= W;
+      cp_wait<1>();  // this block's entries have landed (this lane's copies) …
+      __syncwarp(mask);  // … and every lane's
+      const double2* e0 = ent + buf * 2 * W;
+      const double2* e1 = e0 + W;
+      const bool f = fits(k);
       if (LOWER) {
         const int n0 = k.c0 - 1, n1 = k.two ? k.c1 - 2 : 0;      // entries before diag / intra
-        if (fits) {
-          dot2<C>(X, mask, lane, q0, 0, n0, q1, 0, n1, a0, a1, bm);
+        if (f) {
+          dot2s<C>(X, lane, e0, n0, e1, n1, a0, a1, bm);
         } else {
           dot_long<C>(pk, X, mask, lane, k.s0, n0, a0, bm);
           if (k.two) dot_long<C>(pk, X, mask, lane, k.s1, n1, a1, bm);
         }
-        const double d0 = fits ? shv<W>(mask, q0, (k.c0 - 1) & (W - 1)) : ldpk(pk + k.s0 + k.c0 - 1).x;
+        const double d0 = f ? e0[k.c0 - 1].x : ldpk(pk + k.s0 + k.c0 - 1).x;
         double intra = 0.0, d1 = 1.0;
         if (k.two) {
-          intra = fits ? shv<W>(mask, q1, (k.c1 - 2) & (W - 1)) : ldpk(pk + k.s1 + k.c1 - 2).x;
-          d1 = fits ? shv<W>(mask, q1, (k.c1 - 1) & (W - 1)) : ldpk(pk + k.s1 + k.c1 - 1).x;
+          intra = f ? e1[k.c1 - 2].x : ldpk(pk + k.s1 + k.c1 - 2).x;
+          d1 = f ? e1[k.c1 - 1].x : ldpk(pk + k.s1 + k.c1 - 1).x;
         }
 #pragma unroll
         for (int j = 0; j < CPL; ++j) {
@@ -256,17 +309,17 @@ __device__ __forceinline__ void sweep(const int4* __restrict__ tasks, const int*
         // row 1 = [diag, U...], row 0 = [diag, intra?, U...]
         const int o0 = k.two ? 2 : 1;
         const int n0 = k.c0 - o0, n1 = k.two ? k.c1 - 1 : 0;
-        if (fits) {
-          dot2<C>(X, mask, lane, q0, o0, n0, q1, 1, n1, a0, a1);
+        if (f) {
+          dot2s<C>(X, lane, e0 + o0, n0, e1 + 1, n1, a0, a1);
         } else {
           dot_long<C>(pk, X, mask, lane, k.s0 + o0, n0, a0);
           if (k.two) dot_long<C>(pk, X, mask, lane, k.s1 + 1, n1, a1);
         }
-        const double d0 = fits ? shv<W>(mask, q0, 0) : ldpk(pk + k.s0).x;
+        const double d0 = f ? e0[0].x : ldpk(pk + k.s0).x;
         double intra = 0.0, d1 = 1.0;
         if (k.two) {
-          intra = fits ? shv<W>(mask, q0, 1) : ldpk(pk + k.s0 + 1).x;
-          d1 = fits ? shv<W>(mask, q1, 0) : ldpk(pk + k.s1).x;
+          intra = f ? e0[1].x : ldpk(pk + k.s0 + 1).x;
+          d1 = f ? e1[0].x : ldpk(pk + k.s1).x;
         }
 #pragma unroll
         for (int j = 0; j < CPL; ++j) {
@@ -281,7 +334,12 @@ __device__ __forceinline__ void sweep(const int4* __restrict__ tasks, const int*
           x0p[j] = x0;
         }
       }
+      __syncwarp(mask);  // every lane is done with this buffer before it is refilled
+      buf ^= 1;
+      k = nk;
+      nk = nnk;
     }
+    cp_wait<0>();
     __syncthreads();
   }
 }
@@ -343,6 +401,7 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
                                                                    int N, int rt) {
   constexpr int W = Geo<C>::W;
   extern __shared__ unsigned bm_sm[];  // reach bitmap of this tile (rt ≥ 0)
+  __shared__ __align__(16) double2 ent_sm[kThreads / Geo<C>::W][2][2][Geo<C>::W];  // per-team entry buffers
   const int ntile = (N + C - 1) / C;
   const int tile = blockIdx.x, s = blockIdx.y;
   const size_t cta = (size_t)s * ntile + tile;
@@ -352,6 +411,7 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
   double* X = w.slabZ + cta * n_x * C;
   const double* gu = w.gu + (size_t)s * n.nnz_gu;
   const double2* pk = w.pkA + (size_t)s * n.nnz_lu;
+  double2* ent = &ent_sm[team][0][0][0];
   // A7.1 fused into the first sweep: B = −P G_u V row by row (unit V: G_u's column col0 + j)
   FromRhs<C> rhs;
   rhs.gur_ptr = n.gur_ptr; rhs.gur_col = n.gur_col; rhs.gur_src = n.gur_src; rhs.gu = gu;
@@ -363,11 +423,11 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
     for (int i = threadIdx.x; i < n.bmw; i += blockDim.x) bm_sm[i] = __ldg(bmg + i);
     __syncthreads();
     sweep<C, true>(n.taskLr, n.levLr_ptr + (size_t)(rt + tile) * (n.nlevL + 1), n.nlevL, pk, X, false, lane, team,
-                   nteam, rhs, bm_sm);                                                            // L^{-1} B
-    sweep<C, false>(n.taskU, n.levU_ptr, n.nlevU, pk, X, true, lane, team, nteam, FromSlabReach{bm_sm});  // U^{-1}
+                   nteam, ent, rhs, bm_sm);                                                       // L^{-1} B
+    sweep<C, false>(n.taskU, n.levU_ptr, n.nlevU, pk, X, true, lane, team, nteam, ent, FromSlabReach{bm_sm});  // U^{-1}
   } else {
-    sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, X, false, lane, team, nteam, rhs);   // L^{-1} B
-    sweep<C, false>(n.taskU, n.levU_ptr, n.nlevU, pk, X, true, lane, team, nteam);       // U^{-1}
+    sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, X, false, lane, team, nteam, ent, rhs);   // L^{-1} B
+    sweep<C, false>(n.taskU, n.levU_ptr, n.nlevU, pk, X, true, lane, team, nteam, ent);  // U^{-1}
   }
 }
 
@@ -505,7 +565,10 @@ __global__ void __launch_bounds__(kThreads) k_hvp(DevNet n, Work w, const double
 template <int C>
 __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_adj(DevNet n, Work w, int N, double* __restrict__ KV) {
   constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
-  __shared__ double T[C][kCH + 1];
+  // the sweeps' per-team entry buffers, then (after them) the projection's transpose tile
+  constexpr size_t kEnt = sizeof(double2) * (kThreads / W) * 4 * W, kT = sizeof(double) * C * (kCH + 1);
+  __shared__ __align__(16) unsigned char sm_adj[kEnt > kT ? kEnt : kT];
+  double (*T)[kCH + 1] = reinterpret_cast<double (*)[kCH + 1]>(sm_adj);
   const int ntile = (N + C - 1) / C;
   const int tile = blockIdx.x, s = blockIdx.y;
   const size_t cta = (size_t)s * ntile + tile;
@@ -515,9 +578,10 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_adj(DevNet n, Wor
   const double* Hs = w.hu + cta * n_u * C;
   const double* gu = w.gu + (size_t)s * n.nnz_gu;
   const double2* pk = w.pkT + (size_t)s * n.nnz_lu;
-  sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, Y, true, lane, team, nteam);        // U^{-T}
+  double2* ent = reinterpret_cast<double2*>(sm_adj) + (size_t)team * 4 * W;
+  sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, Y, true, lane, team, nteam, ent);   // U^{-T}
   // L^{-T}: only the ancestors of G_u's rows (the projection reads Ψ there)
-  sweep<C, false>(n.taskUa, n.levUa_ptr, n.nlevU, pk, Y, false, lane, team, nteam);
+  sweep<C, false>(n.taskUa, n.levUa_ptr, n.nlevU, pk, Y, false, lane, team, nteam, ent);
   for (int c0 = 0; c0 < n_u; c0 += kCH) {
     for (int cc = team; cc < kCH && c0 + cc < n_u; cc += nteam) {
       const int c = c0 + cc;
