@@ -292,6 +292,35 @@ def test_condensed_kkt_many_rhs_mixed_info(pfmod):
     h.close()
 
 
+@pytest.mark.parametrize("n_scen", [1, 3])
+def test_condensed_kkt_nonfinite_and_indefinite(pfmod, n_scen):
+    """Degenerate inputs never fault: a NaN K̂, an all-zero K̂ (first pivot 0) and a
+    negative-definite K̂ give info = 1 for every scenario, leave the right-hand
+    sides untouched, and the handle stays usable for a regular solve after."""
+    import torch
+    net, pt = table1_grid("case1354")
+    n_u = O.partition(net)["n_u"]
+    h = pfmod.Network(net, max_batch=n_u, max_scen=n_scen)
+    b = np.random.default_rng(4).standard_normal((n_scen, 1, n_u))
+    info = torch.empty(n_scen, dtype=torch.int32, device="cuda")
+    for fill in (np.nan, 0.0, -1.0):
+        Kbad = np.full((n_scen, n_u, n_u), fill) if fill != -1.0 else np.stack([-np.eye(n_u)] * n_scen)
+        K, rhs = dev(Kbad), dev(b.copy())
+        h.pf_condensed_kkt_solve(n_scen, K, None, 0.0, rhs, 1, info)
+        torch.cuda.synchronize()
+        assert info.cpu().tolist() == [1] * n_scen, fill
+        assert np.array_equal(rhs.cpu().numpy(), b)
+    A = np.random.default_rng(5).standard_normal((n_u, n_u))
+    Kgood = np.stack([A @ A.T / n_u + np.eye(n_u)] * n_scen)
+    K, rhs = dev(Kgood.copy()), dev(b.copy())
+    h.pf_condensed_kkt_solve(n_scen, K, None, 0.0, rhs, 1, info)
+    torch.cuda.synchronize()
+    assert info.cpu().tolist() == [0] * n_scen
+    Lo, _ = O.cholesky(Kgood[0])
+    assert rel_err(rhs[0, 0].cpu().numpy(), O.chol_solve(Lo, b[0, 0])) <= TOL
+    h.close()
+
+
 def test_capacity_and_argument_errors(pfmod):
     import torch
     net, pt = table1_grid("case118")
