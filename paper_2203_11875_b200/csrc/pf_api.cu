@@ -223,7 +223,7 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
        alloc(h, T * d.n_x * C, &w.slabZ) && alloc(h, T * d.n_x * C, &w.slabW) &&
        alloc(h, T * d.n_u * C, &w.hu) && alloc(h, T * d.n_g * 2 * C, &w.mu) &&
        alloc(h, S * chol_tile_doubles(d.n_u), &w.ctile) && alloc(h, S * chol_flag_ints(d.n_u), &w.cflag) &&
-       alloc(h, 1, &w.cticket) && alloc(h, S * chol_vec_doubles(d.n_u), &w.cy);
+       alloc(h, 1 + 1024, &w.cticket) && alloc(h, S * chol_vec_doubles(d.n_u), &w.cy);
   if (!ok) {
     g_build_err = std::string("device allocation/upload failed: ") + cudaGetErrorString(cudaGetLastError());
     pf_destroy(h);

@@ -55,7 +55,13 @@ struct DagArgs {
   int* info;       // [S]
   double* cy;      // [S][2][kRhsCap][nt*64]  y (forward) and p (backward), padded
   double* rhs;     // [S][rhs_ld][n], already offset to the first vector of this run
+  int* crit;       // [kMaxSm] per-SM count of critical-path tasks in their triangular phase
 };
+constexpr int kMaxSm = 1024;
+#ifndef PF_CHOL_LOOK
+#define PF_CHOL_LOOK 2
+#endif
+constexpr int kLook = PF_CHOL_LOOK;  // look-ahead band of the task order (k_chol_dag)
 
 __host__ __device__ __forceinline__ int tidx(int nt, int i, int j) { return j * nt - j * (j - 1) / 2 + (i - j); }
 
@@ -70,6 +76,16 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 }
 __device__ __forceinline__ void wait_flag(const int* p) {
   while (ld_acquire(p) == 0) __nanosleep(40);
+}
+__device__ __forceinline__ int smid() {
+  int v;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(v));
+  return v;
+}
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ __forceinline__ void fence_proxy_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -105,7 +121,8 @@ __device__ __forceinline__ void record_fail(int* info, int code) {
 __global__ void __launch_bounds__(256) k_chol_pack(int n, int nt, const double* __restrict__ K,
                                                    const double* __restrict__ sig_u, double delta,
                                                    double* __restrict__ tiles, int* __restrict__ flags,
-                                                   int* __restrict__ ticket, int* __restrict__ info) {
+                                                   int* __restrict__ ticket, int* __restrict__ info,
+                                                   int* __restrict__ crit) {
   __shared__ double a[32][NB + 1];  // a[c][r] = K(R, C)
   __shared__ double b[NB][33];      // b[r][c] = K(C, R)  (mirror)
   const int s = blockIdx.y, ntri = nt * (nt + 1) / 2;
@@ -149,6 +166,8 @@ __global__ void __launch_bounds__(256) k_chol_pack(int n, int nt, const double* 
     info[s] = 0;
     if (s == 0) *ticket = 0;
   }
+  if (blockIdx.x == 0 && s == 0)
+    for (int k = threadIdx.x; k < kMaxSm; k += blockDim.x) crit[k] = 0;
 }
 
 // L back into K: lower (incl. diagonal) from the tiles, strict upper zeroed.
@@ -256,7 +275,14 @@ __device__ void produce(const TaskCtx& t, int kind, Pipe& p, double* sm) {
   const unsigned half = HALF_D * sizeof(double), full = TILE_D * sizeof(double);
   if (kind == T_TILE) {
     const bool diag = t.i == t.j;
+    // the diagonal tile and the first one below it carry the column chain: while one
+    // of them runs its triangular kernel on this SM, the other CTA's (non-critical)
+    // GEMM stream pauses, so the latency-bound chain does not share the SM's pipes
+    const bool critical = t.i <= t.j + 1;
+    const int* crit = t.a->crit + smid();
     for (int k = 0; k < t.j; ++k) {
+      if (!critical)
+        while (ld_relaxed(crit) > 0) __nanosleep(200);
       wait_flag(t.tflag(t.i, k));
       if (!diag) wait_flag(t.tflag(t.j, k));
       for (int h = 0; h < 2; ++h)
@@ -435,6 +461,9 @@ __device__ void cons_tile(const TaskCtx& t, Pipe& p, double* sm, int* sh) {
         const int r = wr * 32 + m * 8 + g, c = wc * 16 + x * 8 + 2 * q + h;
         Cs[r * LDC + c] = -acc[m][x][h];
       }
+  const bool critical = t.i <= t.j + 1;
+  int* crit = t.a->crit + smid();
+  if (diag && tid == 0) atomicAdd(crit, 1);
   cons_sync();
   PF_MARK(1);
   double* Out = const_cast<double*>(Aij);
@@ -449,6 +478,7 @@ __device__ void cons_tile(const TaskCtx& t, Pipe& p, double* sm, int* sh) {
   } else {
     mbar_wait(p.lbar, p.lpar);
     p.lpar ^= 1;
+    if (critical && tid == 0) atomicAdd(crit, 1);  // L_jj is here: the chain runs on this SM now
     if (tid < NB) sv[tid] = 1.0 / Ls[tid * LDT + tid];
     cons_sync();
     trsm64(Cs, Ls, sv);
@@ -464,6 +494,7 @@ __device__ void cons_tile(const TaskCtx& t, Pipe& p, double* sm, int* sh) {
     __threadfence();
     fence_proxy_global();
     st_release(t.tflag(t.i, t.j), 1);
+    if (critical) atomicSub(crit, 1);
   }
 }
 
@@ -631,19 +662,33 @@ __global__ void __launch_bounds__(kDagThreads, 2) k_chol_dag(DagArgs a) {
       task[4] = t;
       int kind = T_DONE, s = 0, i = 0, j = 0;
       if (t < a.ntask) {
-        int jj = 0;
-        for (; jj < a.nt; ++jj) {
-          const int ntile = a.factor ? a.nt - jj : 0, per = ntile + f, grp = a.S * per;
+        // Topological order with a look-ahead band of kLook columns: group g holds,
+        // per scenario, row g+kLook's tiles (g+kLook, c) for c = max(g, 0) … g+kLook
+        // (the band next to the diagonal, in column order), then the rest of
+        // column g, (i, g) for i > g+kLook, then the forward-solve task g.  So the
+        // tiles on and next to the diagonal — the column chain — are handed out
+        // kLook columns early and have accumulated all but their last products
+        // when the chain reaches them.  Then the backward-solve tasks.
+        const int nt = a.nt;
+        auto band_g = [&](int g) {
+          const int r = g + kLook;
+          return (a.factor && r >= 0 && r < nt) ? r - max(g, 0) + 1 : 0;
+        };
+        auto rest_g = [&](int g) { return (a.factor && g >= 0) ? max(0, nt - (g + kLook + 1)) : 0; };
+        int g = -kLook;
+        for (; g < nt; ++g) {
+          const int nb = band_g(g), nr = rest_g(g), per = nb + nr + ((g >= 0 && f) ? 1 : 0), grp = a.S * per;
           if (t < grp) {
             s = t / per;
             const int r = t % per;
-            if (r < ntile) { kind = T_TILE; i = jj + r; j = jj; }
-            else { kind = T_FWD; j = jj; }
+            if (r < nb) { kind = T_TILE; i = g + kLook; j = max(g, 0) + r; }
+            else if (r < nb + nr) { kind = T_TILE; i = g + kLook + 1 + (r - nb); j = g; }
+            else { kind = T_FWD; j = g; }
             break;
           }
           t -= grp;
         }
-        if (jj == a.nt) { kind = T_BWD; j = a.nt - 1 - t / a.S; s = t % a.S; }
+        if (g == nt) { kind = T_BWD; j = nt - 1 - t / a.S; s = t % a.S; }
         // a scenario that already failed at an earlier column skips its remaining tiles
         if (kind == T_TILE) {
           const int inf = *(volatile int*)(a.info + s);
@@ -717,7 +762,8 @@ int launch_chol(const DevNet& net, const Work& w, int n_scen, double* K, const d
     grid_max = std::max(1, sms * std::max(per, 1));
   }
   int launches = 0;
-  k_chol_pack<<<dim3(ntri, n_scen), 256, 0, st>>>(n, nt, K, sigma_u, delta_w, w.ctile, w.cflag, w.cticket, info_ws);
+  k_chol_pack<<<dim3(ntri, n_scen), 256, 0, st>>>(n, nt, K, sigma_u, delta_w, w.ctile, w.cflag, w.cticket, info_ws,
+                                                   w.cticket + 1);
   ++launches;
   // the factorization runs with the first kRhsCap right-hand sides fused in; further
   // ones (rare) in solve-only runs over the finished factor
@@ -731,7 +777,7 @@ int launch_chol(const DevNet& net, const Work& w, int n_scen, double* K, const d
     a.n = n; a.nt = nt; a.ntri = ntri; a.S = n_scen; a.nrhs = nr; a.factor = first; a.rhs_ld = nrhs;
     a.ntask = n_scen * ((first ? ntri : 0) + f * nt) + f * n_scen * nt;
     a.tiles = w.ctile; a.flags = w.cflag; a.ticket = w.cticket; a.info = info_ws;
-    a.cy = w.cy; a.rhs = rhs ? rhs + (size_t)r0 * n : nullptr;
+    a.cy = w.cy; a.rhs = rhs ? rhs + (size_t)r0 * n : nullptr; a.crit = w.cticket + 1;
     if (a.ntask > 0) {
       k_chol_dag<<<std::min(grid_max, a.ntask), kDagThreads, kDagSmem, st>>>(a);
       ++launches;

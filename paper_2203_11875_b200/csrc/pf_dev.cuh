@@ -71,7 +71,7 @@ struct Work {
   double* mu;      // [max_tiles][n_gb][2][C]
   double* ctile;   // [max_scen][chol_tile_doubles]  packed lower 64×64 tiles of K_cond / L
   int* cflag;      // [max_scen][chol_flag_ints]     tile / forward / backward ready flags
-  int* cticket;    // [1]                            Cholesky DAG task counter
+  int* cticket;    // [1 + 1024]                     Cholesky DAG task counter, then per-SM critical-task counts
   double* cy;      // [max_scen][chol_vec_doubles]   forward / backward solve vectors
   int max_tiles;
 };

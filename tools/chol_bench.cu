@@ -29,7 +29,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&dinfo, S * 4); cudaMalloc(&dws, S * 4);
   cudaMalloc(&w.ctile, S * pf::chol_tile_doubles(n) * 8);
   cudaMalloc(&w.cflag, S * pf::chol_flag_ints(n) * 4);
-  cudaMalloc(&w.cticket, 4);
+  cudaMalloc(&w.cticket, 4 * (1 + 1024));
   cudaMalloc(&w.cy, S * pf::chol_vec_doubles(n) * 8);
   cudaMemcpy(dK0, K.data(), K.size() * 8, cudaMemcpyHostToDevice);
   const int ntask_max = S * (int)(pf::chol_flag_ints(n));
