@@ -4,7 +4,9 @@
 #include "pf_launch.h"
 #include "pf_plan.h"
 
+#include <algorithm>
 #include <cstdio>
+#include <numeric>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -24,8 +26,14 @@ struct pf_net {
   long long launches = 0;
   bool prof = false;         // instrumentation: events around the hot kernels
   int reach_rows_l = 0, reach_rows_ua = 0, gu_rows = 0;  // sparse-RHS statistics (pf_dims)
+  std::vector<int4> p1_task;  // bottom-subtree schedule (host copy for the upload)
+  std::vector<int> p1_ptr;
   cudaEvent_t ev[8] = {};    // [0..4] reduction kernels, [5..6] k_lu
 };
+
+#ifndef PF_P1_IMB
+#define PF_P1_IMB 10
+#endif
 
 static std::string g_build_err;
 
@@ -182,6 +190,72 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
   for (size_t k = 0; k < rowbm.size(); ++k) h->reach_rows_l += __builtin_popcount(rowbm[k]);
   for (int r = 0; r < P.n_x; ++r) h->reach_rows_ua += row_mark[r] == ntc;
   for (int r = 0; r < P.n_x; ++r) h->gu_rows += P.gur_ptr[r + 1] > P.gur_ptr[r];
+  // bottom-subtree schedule of the LOWER sweeps over all blocks (pf_reduce.cu sweep(),
+  // phase 1): levels < lev0 are split into the subtrees of the block elimination tree
+  // hanging below level lev0; each team of a CTA walks its subtrees in postorder.
+  // lev0 is the deepest cut whose largest team load stays within PF_P1_IMB% of the mean.
+  {
+    const int nteam = 256 / std::min(TC, 32);
+    std::vector<int> blk_lev(nblk), bpar(nblk, -1), root(nblk), task_of(nblk);
+    for (int l = 0; l < nlevL; ++l)
+      for (int bi = P.levL_ptr[l]; bi < P.levL_ptr[l + 1]; ++bi) { blk_lev[P.levL_blk[bi]] = l; task_of[P.levL_blk[bi]] = bi; }
+    for (int p = 0; p < nblk; ++p) {
+      const int last = P.blk_ptr[p + 1] - 1;
+      if (parent[last] >= 0) bpar[p] = P.row_blk[parent[last]];
+    }
+    std::vector<int> best_order, best_ptr(nteam + 1, 0);
+    int best_lev0 = 0;
+    for (int lev0 = 1; lev0 <= nlevL; ++lev0) {
+      // subtree roots: blocks below lev0 whose parent is at or above lev0
+      for (int l = lev0 - 1; l >= 0; --l)
+        for (int bi = P.levL_ptr[l]; bi < P.levL_ptr[l + 1]; ++bi) {
+          const int b = P.levL_blk[bi], q = bpar[b];
+          root[b] = (q >= 0 && blk_lev[q] < lev0) ? root[q] : b;
+        }
+      std::vector<std::vector<int>> kids(nblk);
+      std::vector<int> roots;
+      for (int l = 0; l < lev0; ++l)
+        for (int bi = P.levL_ptr[l]; bi < P.levL_ptr[l + 1]; ++bi) {
+          const int b = P.levL_blk[bi];
+          if (root[b] == b) roots.push_back(b); else kids[bpar[b]].push_back(b);
+        }
+      std::vector<int> size(nblk, 1);
+      for (int l = 0; l < lev0; ++l)  // subtree sizes, children before parents
+        for (int bi = P.levL_ptr[l]; bi < P.levL_ptr[l + 1]; ++bi) {
+          const int b = P.levL_blk[bi];
+          if (root[b] != b) size[bpar[b]] += size[b];
+        }
+      std::sort(roots.begin(), roots.end(), [&](int x, int y) { return size[x] != size[y] ? size[x] > size[y] : x < y; });
+      std::vector<long long> load(nteam, 0);
+      std::vector<std::vector<int>> mine(nteam);
+      for (int r : roots) {
+        const int t = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        load[t] += size[r];
+        mine[t].push_back(r);
+      }
+      const long long tot = std::accumulate(load.begin(), load.end(), 0LL);
+      const long long mx = *std::max_element(load.begin(), load.end());
+      if (lev0 > 1 && mx * 100 > tot * (100 + PF_P1_IMB) / nteam) break;  // imbalance beyond PF_P1_IMB%: keep the previous cut
+      std::vector<int> order, ptr(nteam + 1, 0);
+      for (int t = 0; t < nteam; ++t) {
+        for (int r : mine[t]) {  // iterative postorder of the subtree of r
+          std::vector<std::pair<int, size_t>> st{{r, 0}};
+          while (!st.empty()) {
+            auto& [b, c] = st.back();
+            if (c < kids[b].size()) { const int ch = kids[b][c++]; st.push_back({ch, 0}); }
+            else { order.push_back(b); st.pop_back(); }
+          }
+        }
+        ptr[t + 1] = (int)order.size();
+      }
+      best_order.swap(order); best_ptr.swap(ptr); best_lev0 = lev0;
+    }
+    std::vector<int4> p1_task(best_order.size());
+    for (size_t k = 0; k < best_order.size(); ++k) p1_task[k] = taskL[task_of[best_order[k]]];
+    d.p1_lev0 = best_lev0;
+    h->p1_task = p1_task;
+    h->p1_ptr = best_ptr;
+  }
   std::vector<int4> inc_rec(2 * (size_t)n_l);
   for (int i = 0; i < n_b; ++i)
     for (int e = P.inc_ptr[i]; e < P.inc_ptr[i + 1]; ++e) {
@@ -212,7 +286,8 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
             up(h, gbus, &d.gbus) && up(h, rowmeta, &d.rowmeta) && up(h, P.hvp_bus, &d.hvp_bus) &&
             up(h, inc_rec, &d.inc_rec) && up(h, taskL, &d.taskL) && up(h, taskU, &d.taskU) &&
             up(h, taskLr, &d.taskLr) && up(h, levLr_ptr, &d.levLr_ptr) && up(h, rowbm, &d.rowbm) &&
-            up(h, taskUa, &d.taskUa) && up(h, levUa_ptr, &d.levUa_ptr);
+            up(h, taskUa, &d.taskUa) && up(h, levUa_ptr, &d.levUa_ptr) && up(h, h->p1_task, &d.p1_task) &&
+            up(h, h->p1_ptr, &d.p1_ptr);
   Work& w = h->w;
   const size_t S = max_scen;
   w.max_tiles = max_scen * ((max_batch + h->C - 1) / h->C);

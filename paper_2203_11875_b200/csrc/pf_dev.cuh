@@ -38,6 +38,9 @@ struct DevNet {
   const int4 *taskUa;           // U-list blocks that are ancestors of a G_u row
   const int *levUa_ptr;         // [nlevU+1]
   int ntc, bmw;
+  const int4 *p1_task;          // bottom-subtree schedule of the LOWER sweeps: per team, its subtrees in postorder
+  const int *p1_ptr;            // [teams per CTA + 1]
+  int p1_lev0;                  // levels < p1_lev0 run from p1_task, the rest level by level
   const int4 *inc_rec;          // [2 n_l] per incidence: {line, far θ row, far v row | −1−u, from | 2(gen+1)}
   int C;                        // directions per tile (slab row width)
   int lu_maxlen;                // longest row of the filled LU pattern

@@ -226,11 +226,12 @@ struct FromRhs {
   }
 };
 
-template <int C, bool LOWER, class Init = FromSlab>
-__device__ __forceinline__ void sweep(const int4* __restrict__ tasks, const int* __restrict__ lptr, int nlev,
-                                      const double2* __restrict__ pk, double* X, bool divide, int lane, int team,
-                                      int nteam, double2* ent, Init init = Init(), const unsigned* bm = nullptr) {
-  // ent: this team's entry buffers [2][2 rows][W] (double buffer, filled by cp.async)
+// One team runs the blocks tasks[first], tasks[first + stride], … < end in
+// order (the blocks of one level, or the team's bottom subtrees in postorder).
+template <int C, bool LOWER, class Init>
+__device__ __forceinline__ void run_seq(const int4* __restrict__ tasks, int first, int end, int stride,
+                                        const double2* __restrict__ pk, double* X, bool divide, int lane,
+                                        double2* ent, const Init& init, const unsigned* bm) {
   constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
   const unsigned mask = team_mask<W>();
   auto fits = [](const Task& k) { return k.c0 <= W && k.c1 <= W; };
@@ -238,108 +239,126 @@ __device__ __forceinline__ void sweep(const int4* __restrict__ tasks, const int*
     if (lane < k.c0) cp_ent(e + lane, pk + k.s0 + lane);
     if (k.two && lane < k.c1) cp_ent(e + W + lane, pk + k.s1 + lane);
   };
-  for (int lev = 0; lev < nlev; ++lev) {
-    const int b1 = __ldg(lptr + lev + 1);
-    int bi = __ldg(lptr + lev) + team;
-    int buf = 0;
-    Task k, nk;
-    if (bi < b1) {
-      k = unpack(__ldg(tasks + bi));
-      if (fits(k)) fill(k, ent);
-      cp_commit();
-      if (bi + nteam < b1) nk = unpack(__ldg(tasks + bi + nteam));
-    }
-    for (; bi < b1; bi += nteam) {
-      const bool hn = bi + nteam < b1;
-      if (hn && fits(nk)) fill(nk, ent + (buf ^ 1) * 2 * W);  // next block's entries in flight
-      cp_commit();
-      Task nnk = nk;
-      if (bi + 2 * nteam < b1) nnk = unpack(__ldg(tasks + bi + 2 * nteam));
-      double* x0p = X + (size_t)k.r0 * C + lane * CPL;
-      double* x1p = x0p + C;
-      double a0[CPL], a1[CPL];
-      if constexpr (std::is_same<Init, FromSlab>::value) {
+  int bi = first, buf = 0;
+  Task k, nk;
+  if (bi < end) {
+    k = unpack(__ldg(tasks + bi));
+    if (fits(k)) fill(k, ent);
+    cp_commit();
+    if (bi + stride < end) nk = unpack(__ldg(tasks + bi + stride));
+  }
+  for (; bi < end; bi += stride) {
+    const bool hn = bi + stride < end;
+    if (hn && fits(nk)) fill(nk, ent + (buf ^ 1) * 2 * W);  // next block's entries in flight
+    cp_commit();
+    Task nnk = nk;
+    if (bi + 2 * stride < end) nnk = unpack(__ldg(tasks + bi + 2 * stride));
+    double* x0p = X + (size_t)k.r0 * C + lane * CPL;
+    double* x1p = x0p + C;
+    double a0[CPL], a1[CPL];
+    if constexpr (std::is_same<Init, FromSlab>::value) {
 #pragma unroll
-        for (int j = 0; j < CPL; ++j) { a0[j] = x0p[j]; a1[j] = k.two ? x1p[j] : 0.0; }
-      } else if constexpr (std::is_same<Init, FromSlabReach>::value) {
-        const bool in0 = (init.bm[k.r0 >> 5] >> (k.r0 & 31)) & 1u;
-        const bool in1 = k.two && ((init.bm[(k.r0 + 1) >> 5] >> ((k.r0 + 1) & 31)) & 1u);
+      for (int j = 0; j < CPL; ++j) { a0[j] = x0p[j]; a1[j] = k.two ? x1p[j] : 0.0; }
+    } else if constexpr (std::is_same<Init, FromSlabReach>::value) {
+      const bool in0 = (init.bm[k.r0 >> 5] >> (k.r0 & 31)) & 1u;
+      const bool in1 = k.two && ((init.bm[(k.r0 + 1) >> 5] >> ((k.r0 + 1) & 31)) & 1u);
 #pragma unroll
-        for (int j = 0; j < CPL; ++j) { a0[j] = in0 ? x0p[j] : 0.0; a1[j] = in1 ? x1p[j] : 0.0; }
+      for (int j = 0; j < CPL; ++j) { a0[j] = in0 ? x0p[j] : 0.0; a1[j] = in1 ? x1p[j] : 0.0; }
+    } else {
+      init(k.r0, a0);
+      if (k.two) {
+        init(k.r0 + 1, a1);
       } else {
-        init(k.r0, a0);
-        if (k.two) {
-          init(k.r0 + 1, a1);
-        } else {
 #pragma unroll
-          for (int j = 0; j < CPL; ++j) a1[j] = 0.0;
+        for (int j = 0; j < CPL; ++j) a1[j] = 0.0;
+      }
+    }
+    cp_wait<1>();  // this block's entries have landed (this lane's copies) …
+    __syncwarp(mask);  // … and every lane's
+    const double2* e0 = ent + buf * 2 * W;
+    const double2* e1 = e0 + W;
+    const bool f = fits(k);
+    if (LOWER) {
+      const int n0 = k.c0 - 1, n1 = k.two ? k.c1 - 2 : 0;      // entries before diag / intra
+      if (f) {
+        dot2s<C>(X, lane, e0, n0, e1, n1, a0, a1, bm);
+      } else {
+        dot_long<C>(pk, X, mask, lane, k.s0, n0, a0, bm);
+        if (k.two) dot_long<C>(pk, X, mask, lane, k.s1, n1, a1, bm);
+      }
+      const double d0 = f ? e0[k.c0 - 1].x : ldpk(pk + k.s0 + k.c0 - 1).x;
+      double intra = 0.0, d1 = 1.0;
+      if (k.two) {
+        intra = f ? e1[k.c1 - 2].x : ldpk(pk + k.s1 + k.c1 - 2).x;
+        d1 = f ? e1[k.c1 - 1].x : ldpk(pk + k.s1 + k.c1 - 1).x;
+      }
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        double x0 = a0[j];
+        if (divide) x0 /= d0;
+        x0p[j] = x0;
+        if (k.two) {
+          double x1 = a1[j] - intra * x0;
+          if (divide) x1 /= d1;
+          x1p[j] = x1;
         }
       }
-      cp_wait<1>();  // this block's entries have landed (this lane's copies) …
-      __syncwarp(mask);  // … and every lane's
-      const double2* e0 = ent + buf * 2 * W;
-      const double2* e1 = e0 + W;
-      const bool f = fits(k);
-      if (LOWER) {
-        const int n0 = k.c0 - 1, n1 = k.two ? k.c1 - 2 : 0;      // entries before diag / intra
-        if (f) {
-          dot2s<C>(X, lane, e0, n0, e1, n1, a0, a1, bm);
-        } else {
-          dot_long<C>(pk, X, mask, lane, k.s0, n0, a0, bm);
-          if (k.two) dot_long<C>(pk, X, mask, lane, k.s1, n1, a1, bm);
-        }
-        const double d0 = f ? e0[k.c0 - 1].x : ldpk(pk + k.s0 + k.c0 - 1).x;
-        double intra = 0.0, d1 = 1.0;
-        if (k.two) {
-          intra = f ? e1[k.c1 - 2].x : ldpk(pk + k.s1 + k.c1 - 2).x;
-          d1 = f ? e1[k.c1 - 1].x : ldpk(pk + k.s1 + k.c1 - 1).x;
-        }
-#pragma unroll
-        for (int j = 0; j < CPL; ++j) {
-          double x0 = a0[j];
-          if (divide) x0 /= d0;
-          x0p[j] = x0;
-          if (k.two) {
-            double x1 = a1[j] - intra * x0;
-            if (divide) x1 /= d1;
-            x1p[j] = x1;
-          }
-        }
+    } else {
+      // row 1 = [diag, U...], row 0 = [diag, intra?, U...]
+      const int o0 = k.two ? 2 : 1;
+      const int n0 = k.c0 - o0, n1 = k.two ? k.c1 - 1 : 0;
+      if (f) {
+        dot2s<C>(X, lane, e0 + o0, n0, e1 + 1, n1, a0, a1);
       } else {
-        // row 1 = [diag, U...], row 0 = [diag, intra?, U...]
-        const int o0 = k.two ? 2 : 1;
-        const int n0 = k.c0 - o0, n1 = k.two ? k.c1 - 1 : 0;
-        if (f) {
-          dot2s<C>(X, lane, e0 + o0, n0, e1 + 1, n1, a0, a1);
-        } else {
-          dot_long<C>(pk, X, mask, lane, k.s0 + o0, n0, a0);
-          if (k.two) dot_long<C>(pk, X, mask, lane, k.s1 + 1, n1, a1);
-        }
-        const double d0 = f ? e0[0].x : ldpk(pk + k.s0).x;
-        double intra = 0.0, d1 = 1.0;
-        if (k.two) {
-          intra = f ? e0[1].x : ldpk(pk + k.s0 + 1).x;
-          d1 = f ? e1[0].x : ldpk(pk + k.s1).x;
-        }
-#pragma unroll
-        for (int j = 0; j < CPL; ++j) {
-          double x1 = 0.0;
-          if (k.two) {
-            x1 = a1[j];
-            if (divide) x1 /= d1;
-            x1p[j] = x1;
-          }
-          double x0 = a0[j] - intra * x1;
-          if (divide) x0 /= d0;
-          x0p[j] = x0;
-        }
+        dot_long<C>(pk, X, mask, lane, k.s0 + o0, n0, a0);
+        if (k.two) dot_long<C>(pk, X, mask, lane, k.s1 + 1, n1, a1);
       }
-      __syncwarp(mask);  // every lane is done with this buffer before it is refilled
-      buf ^= 1;
-      k = nk;
-      nk = nnk;
+      const double d0 = f ? e0[0].x : ldpk(pk + k.s0).x;
+      double intra = 0.0, d1 = 1.0;
+      if (k.two) {
+        intra = f ? e0[1].x : ldpk(pk + k.s0 + 1).x;
+        d1 = f ? e1[0].x : ldpk(pk + k.s1).x;
+      }
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        double x1 = 0.0;
+        if (k.two) {
+          x1 = a1[j];
+          if (divide) x1 /= d1;
+          x1p[j] = x1;
+        }
+        double x0 = a0[j] - intra * x1;
+        if (divide) x0 /= d0;
+        x0p[j] = x0;
+      }
     }
-    cp_wait<0>();
+    __syncwarp(mask);  // every lane is done with this buffer before it is refilled
+    buf ^= 1;
+    k = nk;
+    nk = nnk;
+  }
+  cp_wait<0>();
+}
+
+// A level-scheduled triangular sweep.  With a phase-1 list (p1, p1ptr) the
+// bottom levels < lev0 are run first without barriers, each team walking its
+// own bottom subtrees in postorder (every row a LOWER row gathers is a
+// descendant, so a subtree is self-contained and its rows are re-read while
+// still in L2); the levels ≥ lev0 then run level by level.
+template <int C, bool LOWER, class Init = FromSlab>
+__device__ __forceinline__ void sweep(const int4* __restrict__ tasks, const int* __restrict__ lptr, int nlev,
+                                      const double2* __restrict__ pk, double* X, bool divide, int lane, int team,
+                                      int nteam, double2* ent, Init init = Init(), const unsigned* bm = nullptr,
+                                      const int4* __restrict__ p1 = nullptr, const int* __restrict__ p1ptr = nullptr,
+                                      int lev0 = 0) {
+  if (p1) {
+    run_seq<C, LOWER>(p1, __ldg(p1ptr + team), __ldg(p1ptr + team + 1), 1, pk, X, divide, lane, ent, init, bm);
+    __syncthreads();
+  } else {
+    lev0 = 0;
+  }
+  for (int lev = lev0; lev < nlev; ++lev) {
+    run_seq<C, LOWER>(tasks, __ldg(lptr + lev) + team, __ldg(lptr + lev + 1), nteam, pk, X, divide, lane, ent, init, bm);
     __syncthreads();
   }
 }
@@ -426,7 +445,8 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
                    nteam, ent, rhs, bm_sm);                                                       // L^{-1} B
     sweep<C, false>(n.taskU, n.levU_ptr, n.nlevU, pk, X, true, lane, team, nteam, ent, FromSlabReach{bm_sm});  // U^{-1}
   } else {
-    sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, X, false, lane, team, nteam, ent, rhs);   // L^{-1} B
+    sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, X, false, lane, team, nteam, ent, rhs, nullptr, n.p1_task,
+                   n.p1_ptr, n.p1_lev0);                                                  // L^{-1} B
     sweep<C, false>(n.taskU, n.levU_ptr, n.nlevU, pk, X, true, lane, team, nteam, ent);  // U^{-1}
   }
 }
@@ -579,7 +599,8 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_adj(DevNet n, Wor
   const double* gu = w.gu + (size_t)s * n.nnz_gu;
   const double2* pk = w.pkT + (size_t)s * n.nnz_lu;
   double2* ent = reinterpret_cast<double2*>(sm_adj) + (size_t)team * 4 * W;
-  sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, Y, true, lane, team, nteam, ent);   // U^{-T}
+  sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, Y, true, lane, team, nteam, ent, FromSlab(), nullptr, n.p1_task,
+                 n.p1_ptr, n.p1_lev0);                                                  // U^{-T}
   // L^{-T}: only the ancestors of G_u's rows (the projection reads Ψ there)
   sweep<C, false>(n.taskUa, n.levUa_ptr, n.nlevU, pk, Y, false, lane, team, nteam, ent);
   for (int c0 = 0; c0 < n_u; c0 += kCH) {
