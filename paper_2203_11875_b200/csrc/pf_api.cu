@@ -26,8 +26,10 @@ struct pf_net {
   long long launches = 0;
   bool prof = false;         // instrumentation: events around the hot kernels
   int reach_rows_l = 0, reach_rows_ua = 0, gu_rows = 0;  // sparse-RHS statistics (pf_dims)
-  std::vector<int4> p1_task;  // bottom-subtree schedule (host copy for the upload)
+  std::vector<int4> p1_task;  // bottom-subtree schedules (host copies for the upload)
   std::vector<int> p1_ptr;
+  std::vector<int4> u_top, u_bot, ua_top, ua_bot;
+  std::vector<int> u_top_ptr, u_bot_ptr, ua_top_ptr, ua_bot_ptr;
   cudaEvent_t ev[8] = {};    // [0..4] reduction kernels, [5..6] k_lu
 };
 
@@ -255,6 +257,31 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
     d.p1_lev0 = best_lev0;
     h->p1_task = p1_task;
     h->p1_ptr = best_ptr;
+    // UPPER sweeps (parents before children): the blocks above the cut in U-level
+    // order, then each team's bottom subtrees in reverse postorder; once over all
+    // blocks (U sweep) and once over the ancestors of G_u's rows (Lᵀ sweep).
+    std::vector<int> taskU_of(nblk);
+    for (int bi = 0; bi < nblk; ++bi) taskU_of[P.levU_blk[bi]] = bi;
+    auto build_upper = [&](bool only_anc, std::vector<int4>& top, std::vector<int>& top_ptr, std::vector<int4>& bot,
+                           std::vector<int>& bot_ptr) {
+      top.clear(); top_ptr.assign(nlevU + 1, 0); bot.clear(); bot_ptr.assign(nteam + 1, 0);
+      for (int l = 0; l < nlevU; ++l) {
+        for (int bi = P.levU_ptr[l]; bi < P.levU_ptr[l + 1]; ++bi) {
+          const int b = P.levU_blk[bi];
+          if (blk_lev[b] >= best_lev0 && (!only_anc || blk_mark[b] == ntc)) top.push_back(taskU[bi]);
+        }
+        top_ptr[l + 1] = (int)top.size();
+      }
+      for (int t = 0; t < nteam; ++t) {
+        for (int k = best_ptr[t + 1] - 1; k >= best_ptr[t]; --k) {
+          const int b = best_order[k];
+          if (!only_anc || blk_mark[b] == ntc) bot.push_back(taskU[taskU_of[b]]);
+        }
+        bot_ptr[t + 1] = (int)bot.size();
+      }
+    };
+    build_upper(false, h->u_top, h->u_top_ptr, h->u_bot, h->u_bot_ptr);
+    build_upper(true, h->ua_top, h->ua_top_ptr, h->ua_bot, h->ua_bot_ptr);
   }
   std::vector<int4> inc_rec(2 * (size_t)n_l);
   for (int i = 0; i < n_b; ++i)
@@ -287,7 +314,9 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
             up(h, inc_rec, &d.inc_rec) && up(h, taskL, &d.taskL) && up(h, taskU, &d.taskU) &&
             up(h, taskLr, &d.taskLr) && up(h, levLr_ptr, &d.levLr_ptr) && up(h, rowbm, &d.rowbm) &&
             up(h, taskUa, &d.taskUa) && up(h, levUa_ptr, &d.levUa_ptr) && up(h, h->p1_task, &d.p1_task) &&
-            up(h, h->p1_ptr, &d.p1_ptr);
+            up(h, h->p1_ptr, &d.p1_ptr) && up(h, h->u_top, &d.u_top) && up(h, h->u_top_ptr, &d.u_top_ptr) &&
+            up(h, h->u_bot, &d.u_bot) && up(h, h->u_bot_ptr, &d.u_bot_ptr) && up(h, h->ua_top, &d.ua_top) &&
+            up(h, h->ua_top_ptr, &d.ua_top_ptr) && up(h, h->ua_bot, &d.ua_bot) && up(h, h->ua_bot_ptr, &d.ua_bot_ptr);
   Work& w = h->w;
   const size_t S = max_scen;
   w.max_tiles = max_scen * ((max_batch + h->C - 1) / h->C);

@@ -41,6 +41,11 @@ struct DevNet {
   const int4 *p1_task;          // bottom-subtree schedule of the LOWER sweeps: per team, its subtrees in postorder
   const int *p1_ptr;            // [teams per CTA + 1]
   int p1_lev0;                  // levels < p1_lev0 run from p1_task, the rest level by level
+  // UPPER sweeps: blocks above the cut by U level (u_top, [nlevU+1] pointers), then the
+  // bottom subtrees per team parents-first (u_bot, [teams+1]); ua_*: the same restricted
+  // to the ancestors of G_u's rows (the Lᵀ sweep)
+  const int4 *u_top, *u_bot, *ua_top, *ua_bot;
+  const int *u_top_ptr, *u_bot_ptr, *ua_top_ptr, *ua_bot_ptr;
   const int4 *inc_rec;          // [2 n_l] per incidence: {line, far θ row, far v row | −1−u, from | 2(gen+1)}
   int C;                        // directions per tile (slab row width)
   int lu_maxlen;                // longest row of the filled LU pattern

@@ -351,14 +351,18 @@ __device__ __forceinline__ void sweep(const int4* __restrict__ tasks, const int*
                                       int nteam, double2* ent, Init init = Init(), const unsigned* bm = nullptr,
                                       const int4* __restrict__ p1 = nullptr, const int* __restrict__ p1ptr = nullptr,
                                       int lev0 = 0) {
-  if (p1) {
+  // LOWER: bottom subtrees (children first), then the levels ≥ lev0.  UPPER: the
+  // given (top) levels, then the bottom subtrees (parents first).
+  if (LOWER && p1) {
     run_seq<C, LOWER>(p1, __ldg(p1ptr + team), __ldg(p1ptr + team + 1), 1, pk, X, divide, lane, ent, init, bm);
     __syncthreads();
-  } else {
-    lev0 = 0;
   }
-  for (int lev = lev0; lev < nlev; ++lev) {
+  for (int lev = (LOWER && p1) ? lev0 : 0; lev < nlev; ++lev) {
     run_seq<C, LOWER>(tasks, __ldg(lptr + lev) + team, __ldg(lptr + lev + 1), nteam, pk, X, divide, lane, ent, init, bm);
+    __syncthreads();
+  }
+  if (!LOWER && p1) {
+    run_seq<C, LOWER>(p1, __ldg(p1ptr + team), __ldg(p1ptr + team + 1), 1, pk, X, divide, lane, ent, init, bm);
     __syncthreads();
   }
 }
@@ -443,11 +447,13 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
     __syncthreads();
     sweep<C, true>(n.taskLr, n.levLr_ptr + (size_t)(rt + tile) * (n.nlevL + 1), n.nlevL, pk, X, false, lane, team,
                    nteam, ent, rhs, bm_sm);                                                       // L^{-1} B
-    sweep<C, false>(n.taskU, n.levU_ptr, n.nlevU, pk, X, true, lane, team, nteam, ent, FromSlabReach{bm_sm});  // U^{-1}
+    sweep<C, false>(n.u_top, n.u_top_ptr, n.nlevU, pk, X, true, lane, team, nteam, ent, FromSlabReach{bm_sm}, nullptr,
+                    n.u_bot, n.u_bot_ptr);                                                 // U^{-1}
   } else {
     sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, X, false, lane, team, nteam, ent, rhs, nullptr, n.p1_task,
                    n.p1_ptr, n.p1_lev0);                                                  // L^{-1} B
-    sweep<C, false>(n.taskU, n.levU_ptr, n.nlevU, pk, X, true, lane, team, nteam, ent);  // U^{-1}
+    sweep<C, false>(n.u_top, n.u_top_ptr, n.nlevU, pk, X, true, lane, team, nteam, ent, FromSlab(), nullptr, n.u_bot,
+                    n.u_bot_ptr);                                                          // U^{-1}
   }
 }
 
@@ -602,7 +608,8 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_adj(DevNet n, Wor
   sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, Y, true, lane, team, nteam, ent, FromSlab(), nullptr, n.p1_task,
                  n.p1_ptr, n.p1_lev0);                                                  // U^{-T}
   // L^{-T}: only the ancestors of G_u's rows (the projection reads Ψ there)
-  sweep<C, false>(n.taskUa, n.levUa_ptr, n.nlevU, pk, Y, false, lane, team, nteam, ent);
+  sweep<C, false>(n.ua_top, n.ua_top_ptr, n.nlevU, pk, Y, false, lane, team, nteam, ent, FromSlab(), nullptr, n.ua_bot,
+                  n.ua_bot_ptr);
   for (int c0 = 0; c0 < n_u; c0 += kCH) {
     for (int cc = team; cc < kCH && c0 + cc < n_u; cc += nteam) {
       const int c = c0 + cc;
