@@ -30,6 +30,7 @@ struct pf_net {
   std::vector<int> p1_ptr;
   std::vector<int4> u_top, u_bot, ua_top, ua_bot;
   std::vector<int> u_top_ptr, u_bot_ptr, ua_top_ptr, ua_bot_ptr;
+  std::vector<int> hvp_order;  // k_hvp bus order (elimination-forest postorder)
   cudaEvent_t ev[8] = {};    // [0..4] reduction kernels, [5..6] k_lu
 };
 
@@ -282,6 +283,23 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
     };
     build_upper(false, h->u_top, h->u_top_ptr, h->u_bot, h->u_bot_ptr);
     build_upper(true, h->ua_top, h->ua_top_ptr, h->ua_bot, h->ua_bot_ptr);
+    // k_hvp bus order: postorder of the block elimination forest, so the 64 buses of
+    // a CTA (and their neighbours' slab rows) come from a few compact subtrees; the
+    // reference bus (no state rows) last
+    std::vector<std::vector<int>> ch(nblk);
+    std::vector<int> roots_all;
+    for (int b = 0; b < nblk; ++b) (bpar[b] >= 0 ? ch[bpar[b]] : roots_all).push_back(b);
+    h->hvp_order.clear();
+    for (int r : roots_all) {
+      std::vector<std::pair<int, size_t>> st{{r, 0}};
+      while (!st.empty()) {
+        auto& [b, c] = st.back();
+        if (c < ch[b].size()) { const int x = ch[b][c++]; st.push_back({x, 0}); }
+        else { h->hvp_order.push_back(P.blk_bus[b]); st.pop_back(); }
+      }
+    }
+    for (int i = 0; i < n_b; ++i)
+      if (P.bus_pth[i] < 0 && P.bus_pv[i] < 0) h->hvp_order.push_back(i);
   }
   std::vector<int4> inc_rec(2 * (size_t)n_l);
   for (int i = 0; i < n_b; ++i)
@@ -310,7 +328,7 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
             up(h, P.levU_blk, &d.levU_blk) && up(h, P.guc_ptr, &d.guc_ptr) && up(h, P.guc_row, &d.guc_row) &&
             up(h, P.guc_src, &d.guc_src) && up(h, P.gur_ptr, &d.gur_ptr) && up(h, P.gur_col, &d.gur_col) &&
             up(h, P.gur_src, &d.gur_src) && up(h, P.bus_pth, &d.bus_pth) && up(h, P.bus_pv, &d.bus_pv) &&
-            up(h, gbus, &d.gbus) && up(h, rowmeta, &d.rowmeta) && up(h, P.hvp_bus, &d.hvp_bus) &&
+            up(h, gbus, &d.gbus) && up(h, rowmeta, &d.rowmeta) && up(h, h->hvp_order.size() == (size_t)n_b ? h->hvp_order : P.hvp_bus, &d.hvp_bus) &&
             up(h, inc_rec, &d.inc_rec) && up(h, taskL, &d.taskL) && up(h, taskU, &d.taskU) &&
             up(h, taskLr, &d.taskLr) && up(h, levLr_ptr, &d.levLr_ptr) && up(h, rowbm, &d.rowbm) &&
             up(h, taskUa, &d.taskUa) && up(h, levUa_ptr, &d.levUa_ptr) && up(h, h->p1_task, &d.p1_task) &&
