@@ -467,6 +467,13 @@ pf_status pf_condensed_kkt_solve(pf_net* h, int32_t n_scen, double* K, const dou
   return cuda_check(h, "pf_condensed_kkt_solve");
 }
 
+#ifdef PF_LU_TRACE  // debug builds only (tools/lu_trace.py)
+int pf_debug_set_lu_trace(void* dev_ptr) {
+  pf::set_lu_trace(static_cast<unsigned long long*>(dev_ptr));
+  return 0;
+}
+#endif
+
 pf_status pf_profile(pf_net* h, int32_t enable) {
   if (!h) return PF_ERR_ARG;
   if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;

@@ -245,6 +245,78 @@ __global__ void k_gather(DevNet n, Work w, int n_scen, double* __restrict__ Gx,
 // separates levels.  One cluster per scenario, so scenarios run independently.
 // Values written by other SMs of the cluster are read with ld.global.cg (L2).
 constexpr int kLuThreads = 512;
+constexpr int kLuStageMin = 8;    // rows with at least this many pivots stage their working set
+constexpr int kLuMaxPiv = 128;    // … and at most this many
+constexpr int kLuStageCap = 768;  // update entries staged per warp
+constexpr int kLuStageWarps = 4;  // warps of a CTA with a staging area
+
+// A warp's staging area for one long LU row: per pivot a its 1/u_kk and the
+// offset of its update list; the lists' values (pivot U row) and targets.
+struct LuStage {
+  double* pin;  // [kLuMaxPiv]
+  double* val;  // [kLuStageCap]
+  int* off;     // [kLuMaxPiv + 1]
+  int* u0;      // [kLuMaxPiv] start of the pivot's U row in lu
+  int* q0;      // [kLuMaxPiv] start of the pivot's update list in upd_dst
+  int* dst;     // [kLuStageCap]
+};
+constexpr size_t kLuStageBytes = (size_t)kLuMaxPiv * 8 + kLuStageCap * 8 + (kLuMaxPiv + 1 + 1) * 4 +
+                                 2 * kLuMaxPiv * 4 + kLuStageCap * 4;
+
+// Lane-parallel gather of row (base, dl)'s IKJ working set: two dependent waves
+// for the pivot metadata, then every update entry — a flat loop, each lane
+// finding its pivot by binary search, 4 independent loads in flight per lane
+// (values finalized by earlier levels; __ldcg: written by other SMs of the
+// cluster).  False (nothing staged) when the lists exceed the staging area.
+__device__ bool stage_row(const DevNet& n, const double* lu, const double* invd, int base, int dl, int lane,
+                          const LuStage& st) {
+  for (int a = lane; a < dl; a += 32) {
+    const int e = base + a, k = __ldg(n.lu_idx + e);
+    const int q0 = __ldg(n.upd_ptr + e);
+    st.off[a + 1] = __ldg(n.upd_ptr + e + 1) - q0;
+    st.q0[a] = q0;
+    st.u0[a] = __ldg(n.lu_diag + k) + 1;
+    st.pin[a] = __ldcg(invd + k);
+  }
+  __syncwarp();
+  if (lane == 0) {  // prefix sum of the list lengths (dl ≤ 128: serial is fine)
+    int acc = 0;
+    st.off[0] = 0;
+    for (int a = 0; a < dl; ++a) { acc += st.off[a + 1]; st.off[a + 1] = acc; }
+  }
+  __syncwarp();
+  const int total = st.off[dl];
+  if (total > kLuStageCap) return false;
+  for (int i0 = 0; i0 < total; i0 += 128) {
+    double v[4];
+    int dd[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = i0 + 32 * q + lane;
+      if (idx < total) {
+        int lo = 0, hi = dl;  // st.off[lo] <= idx < st.off[hi]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (st.off[mid] <= idx) lo = mid; else hi = mid;
+        }
+        const int t = idx - st.off[lo];
+        v[q] = __ldcg(lu + st.u0[lo] + t);
+        dd[q] = __ldg(n.upd_dst + st.q0[lo] + t);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = i0 + 32 * q + lane;
+      if (idx < total) { st.val[idx] = v[q]; st.dst[idx] = dd[q]; }
+    }
+  }
+  __syncwarp();
+  return true;
+}
+
+#ifdef PF_LU_TRACE
+__device__ unsigned long long* g_lu_trace;  // tools/lu_trace.py: globaltimer after each level (cluster 0)
+#endif
 
 __global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int CS) {
   cg::cluster_group cluster = cg::this_cluster();
@@ -254,7 +326,9 @@ __global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int CS) {
   const double* jb = w.jb + (size_t)s * n.nnz_jb;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int gthread = sub * blockDim.x + threadIdx.x, nthread = CS * blockDim.x;
-  const int gwarp = sub * nwarp + warp, ngwarp = CS * nwarp;
+  // blocks go to the cluster's CTAs round-robin, so a narrow level puts at most a
+  // few rows on each CTA (on its low warps, which own the staging areas)
+  const int gwarp = warp * CS + sub, ngwarp = CS * nwarp;
   if (gthread == 0) w.info[s] = INT_MAX;
   for (int r = gthread; r < n.n_x; r += nthread) {
     double mx = 0.0;
@@ -267,8 +341,24 @@ __global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int CS) {
     rowmax[r] = mx;
   }
   cluster.sync();
+#ifdef PF_LU_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0 && g_lu_trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_lu_trace[0] = t;
+  }
+#endif
   extern __shared__ double lu_ws[];
   double* ws = lu_ws + warp * n.lu_maxlen;  // the warp's dense row workspace
+  unsigned char* stb = reinterpret_cast<unsigned char*>(lu_ws + (size_t)nwarp * n.lu_maxlen) +
+                       (size_t)min(warp, kLuStageWarps - 1) * kLuStageBytes;
+  LuStage st;
+  st.pin = reinterpret_cast<double*>(stb);
+  st.val = st.pin + kLuMaxPiv;
+  st.off = reinterpret_cast<int*>(st.val + kLuStageCap);
+  st.u0 = st.off + kLuMaxPiv + 2;
+  st.q0 = st.u0 + kLuMaxPiv;
+  st.dst = st.q0 + kLuMaxPiv;
   double* invd = w.invd + (size_t)s * n.n_x;
   for (int lev = 0; lev < n.nlevL; ++lev) {
     const int b0 = __ldg(n.levL_ptr + lev), b1 = __ldg(n.levL_ptr + lev + 1);
@@ -279,37 +369,49 @@ __global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int CS) {
         const int dl = __ldg(n.lu_diag + r) - base;
         for (int a = lane; a < len; a += 32) ws[a] = __ldcg(lu + base + a);
         __syncwarp();
-        // IKJ over the row's L entries; the U row of the next pivot and the
-        // update targets are prefetched into registers while this one runs.
-        double pu[4], pin = 0.0;
-        int pd[4], pq0 = 0, pcnt = 0, pu0 = 0;
-        auto fetch = [&](int a) {
-          const int e = base + a, k = __ldg(n.lu_idx + e);
-          pu0 = __ldg(n.lu_diag + k) + 1;
-          pq0 = __ldg(n.upd_ptr + e);
-          pcnt = __ldg(n.upd_ptr + e + 1) - pq0;
-          pin = __ldcg(invd + k);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int t = lane + 32 * j;
-            pu[j] = t < pcnt ? __ldcg(lu + pu0 + t) : 0.0;
-            pd[j] = t < pcnt ? __ldg(n.upd_dst + pq0 + t) : 0;
+        if (warp < kLuStageWarps && dl >= kLuStageMin && dl <= kLuMaxPiv && stage_row(n, lu, invd, base, dl, lane, st)) {
+          // long (separator) row: its whole IKJ working set is in SMEM, the chain runs there
+          for (int a = 0; a < dl; ++a) {
+            const double l = ws[a] * st.pin[a];
+            const int o = st.off[a], cnt = st.off[a + 1] - o;
+            for (int t = lane; t < cnt; t += 32) ws[st.dst[o + t]] -= l * st.val[o + t];
+            __syncwarp();  // the next pivot's entry may just have been updated
+            if (lane == 0) ws[a] = l;  // (entry a is not read again by the chain)
           }
-        };
-        if (dl > 0) fetch(0);
-        for (int a = 0; a < dl; ++a) {
-          const double cu[4] = {pu[0], pu[1], pu[2], pu[3]};
-          const int cd[4] = {pd[0], pd[1], pd[2], pd[3]};
-          const double cin = pin;
-          const int q0 = pq0, cnt = pcnt, u0 = pu0;
-          if (a + 1 < dl) fetch(a + 1);
-          const double l = ws[a] * cin;
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (lane + 32 * j < cnt) ws[cd[j]] -= l * cu[j];
-          for (int t = lane + 128; t < cnt; t += 32) ws[__ldg(n.upd_dst + q0 + t)] -= l * __ldcg(lu + u0 + t);
           __syncwarp();
-          if (lane == 0) ws[a] = l;
+        } else {
+          // IKJ over the row's L entries; the U row of the next pivot and the
+          // update targets are prefetched into registers while this one runs.
+          double pu[4], pin = 0.0;
+          int pd[4], pq0 = 0, pcnt = 0, pu0 = 0;
+          auto fetch = [&](int a) {
+            const int e = base + a, k = __ldg(n.lu_idx + e);
+            pu0 = __ldg(n.lu_diag + k) + 1;
+            pq0 = __ldg(n.upd_ptr + e);
+            pcnt = __ldg(n.upd_ptr + e + 1) - pq0;
+            pin = __ldcg(invd + k);
+  #pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int t = lane + 32 * j;
+              pu[j] = t < pcnt ? __ldcg(lu + pu0 + t) : 0.0;
+              pd[j] = t < pcnt ? __ldg(n.upd_dst + pq0 + t) : 0;
+            }
+          };
+          if (dl > 0) fetch(0);
+          for (int a = 0; a < dl; ++a) {
+            const double cu[4] = {pu[0], pu[1], pu[2], pu[3]};
+            const int cd[4] = {pd[0], pd[1], pd[2], pd[3]};
+            const double cin = pin;
+            const int q0 = pq0, cnt = pcnt, u0 = pu0;
+            if (a + 1 < dl) fetch(a + 1);
+            const double l = ws[a] * cin;
+  #pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (lane + 32 * j < cnt) ws[cd[j]] -= l * cu[j];
+            for (int t = lane + 128; t < cnt; t += 32) ws[__ldg(n.upd_dst + q0 + t)] -= l * __ldcg(lu + u0 + t);
+            __syncwarp();
+            if (lane == 0) ws[a] = l;
+          }
         }
         __syncwarp();
         for (int a = lane; a < len; a += 32) __stcg(lu + base + a, ws[a]);
@@ -322,6 +424,13 @@ __global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int CS) {
       }
     }
     cluster.sync();
+#ifdef PF_LU_TRACE
+    if (blockIdx.x == 0 && threadIdx.x == 0 && g_lu_trace) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_lu_trace[lev + 1] = t;
+    }
+#endif
   }
   double* luT = w.luT + (size_t)s * n.nnz_lu;
   double2* pkA = w.pkA + (size_t)s * n.nnz_lu;
@@ -481,6 +590,10 @@ __global__ void k_prep_bus2(DevNet n, Work w, int n_scen) {
 
 }  // namespace
 
+#ifdef PF_LU_TRACE
+void set_lu_trace(unsigned long long* p) { cudaMemcpyToSymbol(g_lu_trace, &p, sizeof(p)); }
+#endif
+
 int launch_eval(const DevNet& n, const Work& w, int n_scen, const double* v, const double* th,
                 const double* p_g, const double* q_g, const double* p_d, const double* q_d,
                 double* G, double* H, double* s_flow, cudaStream_t st) {
@@ -495,7 +608,7 @@ int launch_jacobian(const DevNet& n, const Work& w, int n_scen, const double* v,
   k_bus_v<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen, v);
   k_jbus<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen);
   k_gather<<<blocks_for((long long)n_scen * (n.nnz_gx + n.nnz_gu + n.nnz_a)), kThreads, 0, st>>>(n, w, n_scen, Gx, Gu, A);
-  const size_t smem = (size_t)(kLuThreads / 32) * n.lu_maxlen * sizeof(double);
+  const size_t smem = (size_t)(kLuThreads / 32) * n.lu_maxlen * sizeof(double) + kLuStageWarps * kLuStageBytes;
   static int CS = 0;
   if (!CS) {  // 16-CTA clusters (non-portable) when the part supports them, else 8
     cudaFuncSetAttribute(k_lu, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

@@ -28,6 +28,9 @@ int launch_chol(const DevNet& n, const Work& w, int n_scen, double* K, const dou
                 double* rhs, int nrhs, int* info, int* info_ws, cudaStream_t st);
 
 int pick_tile_cols(int n_x, int n_scen_x_N);
+#ifdef PF_LU_TRACE
+void set_lu_trace(unsigned long long* p);  // debug builds: per-level k_lu timestamps
+#endif
 size_t chol_tile_doubles(int n_u);  // Cholesky workspaces per scenario (pf_chol.cu)
 size_t chol_flag_ints(int n_u);
 size_t chol_vec_doubles(int n_u);
