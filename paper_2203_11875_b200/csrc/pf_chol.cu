@@ -279,15 +279,26 @@ __device__ void produce(const TaskCtx& t, int kind, Pipe& p, double* sm) {
     // of them runs its triangular kernel on this SM, the other CTA's (non-critical)
     // GEMM stream pauses, so the latency-bound chain does not share the SM's pipes
     const bool critical = t.i <= t.j + 1;
-    const int* crit = t.a->crit + smid();
+    int* crit = t.a->crit + smid();
+    // A critical tile also holds the counter while it streams chunks whose inputs
+    // are ready — never while it waits for a dependency, which the throttled
+    // neighbour may be computing (so the throttle cannot deadlock).
+    bool held = false;
+    auto hold = [&](bool on) {
+      if (on != held) { atomicAdd(crit, on ? 1 : -1); held = on; }
+    };
     for (int k = 0; k < t.j; ++k) {
       if (!critical)
         while (ld_relaxed(crit) > 0) __nanosleep(200);
+      if (critical && (ld_relaxed(t.tflag(t.i, k)) == 0 || (!diag && ld_relaxed(t.tflag(t.j, k)) == 0)))
+        hold(false);
       wait_flag(t.tflag(t.i, k));
       if (!diag) wait_flag(t.tflag(t.j, k));
+      if (critical) hold(true);
       for (int h = 0; h < 2; ++h)
         prod_issue(p, sm, t.tile(t.i, k) + h * HALF_D, diag ? nullptr : t.tile(t.j, k) + h * HALF_D, half);
     }
+    hold(false);
     if (!diag) prod_ljj(t, p, sm + NB * LDC);
   } else if (kind == T_FWD) {
     for (int k = 0; k < t.j; ++k) {
