@@ -180,7 +180,7 @@ def run_reference(args, cfg, rank, world):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "%s (BASELINE.json configs[%d])" % (args.config, cfg["baseline_cfg"]),
                        "grid": cfg["grid"], "n_b": net["n_b"], "n_l": net["n_l"], "n_g": net["n_g"],
-                       "scenarios_per_gpu": cfg["scen"], "directions_per_step": cfg["scen"] * (hv // args.steps),
+                       "scenarios_per_gpu": cfg["scen"], "directions_per_step": hv // args.steps,
                        "parallelism": "CPU oracle, rank 0 only"},
             "cpu_baseline": {"value": value, "unit": "HVP/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "HVP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
