@@ -413,7 +413,8 @@ def main():
     per_dir = {"k_fwd": 8.0 * (2 * r_mean + n_x),             # L sweep writes r rows; U reads them, writes Z
                "k_mu": 8.0 * 2 * n_g,                         # μ_A rows written (Z reads hit L2)
                "k_hvp": 8.0 * (2 * n_x + n_u),                # Z read, H_x write, H_u write
-               "k_adj": 8.0 * (2 * n_x + 2 * a_rows + g_rows + 2 * n_u),  # Uᵀ r+w, Lᵀ r+w on a rows, Ψ at G_u rows, H_u, K̂V
+               "k_adj": 8.0 * (2 * n_x + 2 * a_rows),          # Uᵀ sweep r+w, Lᵀ sweep r+w on a rows
+               "k_proj": 8.0 * (g_rows + 2 * n_u),             # Ψ at G_u rows, H_u read, K̂V write
                "k_lu": None}
     kstats = {}
     for k, v in kern.items():

@@ -211,9 +211,9 @@ int64_t pf_launch_count(const pf_net *net);
  * Instrumentation (bench / profiling only).  pf_profile(net, 1) makes the
  * compute calls record CUDA events on their stream around the hot kernels;
  * pf_kernel_times writes the last calls' per-kernel milliseconds, in the
- * order k_fwd, k_mu, k_hvp, k_adj (pf_reduced_hessian_batch) and k_lu
- * (pf_jacobian), synchronizing on the events; returns how many were written
- * (0 when profiling is off).
+ * order k_fwd, k_mu, k_hvp, k_adj (pf_reduced_hessian_batch), k_lu
+ * (pf_jacobian) and k_proj (pf_reduced_hessian_batch), synchronizing on the
+ * events; returns how many were written (0 when profiling is off; at most 6).
  */
 pf_status pf_profile(pf_net *net, int32_t enable);
 int32_t pf_kernel_times(pf_net *net, float *ms /* [host] cap */, int32_t cap);

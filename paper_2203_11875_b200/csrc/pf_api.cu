@@ -31,7 +31,7 @@ struct pf_net {
   std::vector<int4> u_top, u_bot, ua_top, ua_bot;
   std::vector<int> u_top_ptr, u_bot_ptr, ua_top_ptr, ua_bot_ptr;
   std::vector<int> hvp_order;  // k_hvp bus order (elimination-forest postorder)
-  cudaEvent_t ev[8] = {};    // [0..4] reduction kernels, [5..6] k_lu
+  cudaEvent_t ev[8] = {};    // [0..4] k_fwd/k_mu/k_hvp/k_adj, [5..6] k_lu, [4..7] k_proj
 };
 
 #ifndef PF_P1_IMB
@@ -340,7 +340,7 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
   w.max_tiles = max_scen * ((max_batch + h->C - 1) / h->C);
   const size_t T = w.max_tiles, C = h->C;
   ok = ok && alloc(h, S * d.nnz_jb, &w.jb) && alloc(h, S * d.nnz_gu, &w.gu) && alloc(h, S * d.nnz_lu, &w.lu) &&
-       alloc(h, S * d.nnz_lu, &w.luT) && alloc(h, S * d.nnz_lu, &w.pkA) && alloc(h, S * d.nnz_lu, &w.pkT) && alloc(h, S * d.n_x, &w.rowmax) && alloc(h, S * d.n_x, &w.invd) && alloc(h, S * LS_N * d.n_l, &w.ls) &&
+       alloc(h, S * d.nnz_lu, &w.luT) && alloc(h, S * d.nnz_lu, &w.pkA) && alloc(h, S * d.nnz_lu, &w.pkT) && alloc(h, S * d.nnz_gu, &w.pkG) && alloc(h, S * d.n_x, &w.rowmax) && alloc(h, S * d.n_x, &w.invd) && alloc(h, S * LS_N * d.n_l, &w.ls) &&
        alloc(h, S * BS_N * d.n_b, &w.bs) && alloc(h, S * LB_N * d.n_l, &w.lblk) && alloc(h, S * 4 * d.n_l, &w.sflow) && alloc(h, 2 * S, &w.info) &&
        alloc(h, T * d.n_x * C, &w.slabZ) && alloc(h, T * d.n_x * C, &w.slabW) &&
        alloc(h, T * d.n_u * C, &w.hu) && alloc(h, T * d.n_g * 2 * C, &w.mu) &&
@@ -486,9 +486,9 @@ pf_status pf_profile(pf_net* h, int32_t enable) {
 
 int32_t pf_kernel_times(pf_net* h, float* ms, int32_t cap) {
   if (!h || !h->prof || !ms) return 0;
-  const int pairs[5][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {5, 6}};
+  const int pairs[6][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {5, 6}, {4, 7}};
   int k = 0;
-  for (; k < 5 && k < cap; ++k) {
+  for (; k < 6 && k < cap; ++k) {
     float t = -1.0f;
     if (cudaEventSynchronize(h->ev[pairs[k][1]]) == cudaSuccess &&
         cudaEventElapsedTime(&t, h->ev[pairs[k][0]], h->ev[pairs[k][1]]) != cudaSuccess)

@@ -17,6 +17,7 @@
 // so K̂ is bit-identical across batch sizes.
 #include "pf_launch.h"
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -589,50 +590,98 @@ __global__ void __launch_bounds__(kThreads) k_hvp(DevNet n, Work w, const double
 
 // ---------------------------------------------------------------- d, e
 template <int C>
-__global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_adj(DevNet n, Work w, int N, double* __restrict__ KV) {
-  constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
-  // the sweeps' per-team entry buffers, then (after them) the projection's transpose tile
-  constexpr size_t kEnt = sizeof(double2) * (kThreads / W) * 4 * W, kT = sizeof(double) * C * (kCH + 1);
-  __shared__ __align__(16) unsigned char sm_adj[kEnt > kT ? kEnt : kT];
-  double (*T)[kCH + 1] = reinterpret_cast<double (*)[kCH + 1]>(sm_adj);
+__global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_adj(DevNet n, Work w, int N) {
+  constexpr int W = Geo<C>::W;
+  __shared__ __align__(16) double2 sm_adj[(kThreads / W) * 4 * W];  // the sweeps' per-team entry buffers
   const int ntile = (N + C - 1) / C;
   const int tile = blockIdx.x, s = blockIdx.y;
   const size_t cta = (size_t)s * ntile + tile;
   const int lane = threadIdx.x % W, team = threadIdx.x / W, nteam = blockDim.x / W;
-  const int n_x = n.n_x, n_u = n.n_u;
-  double* Y = w.slabW + cta * n_x * C;
-  const double* Hs = w.hu + cta * n_u * C;
-  const double* gu = w.gu + (size_t)s * n.nnz_gu;
+  double* Y = w.slabW + cta * n.n_x * C;
   const double2* pk = w.pkT + (size_t)s * n.nnz_lu;
-  double2* ent = reinterpret_cast<double2*>(sm_adj) + (size_t)team * 4 * W;
+  double2* ent = sm_adj + (size_t)team * 4 * W;
   sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, Y, true, lane, team, nteam, ent, FromSlab(), nullptr, n.p1_task,
                  n.p1_ptr, n.p1_lev0);                                                  // U^{-T}
   // L^{-T}: only the ancestors of G_u's rows (the projection reads Ψ there)
   sweep<C, false>(n.ua_top, n.ua_top_ptr, n.nlevU, pk, Y, false, lane, team, nteam, ent, FromSlab(), nullptr, n.ua_bot,
                   n.ua_bot_ptr);
-  for (int c0 = 0; c0 < n_u; c0 += kCH) {
-    for (int cc = team; cc < kCH && c0 + cc < n_u; cc += nteam) {
-      const int c = c0 + cc;
-      double acc[CPL];
+}
+
+// G_u of each scenario in column (CSC) order, packed {value, row·C} for the projection
+__global__ void k_pack_gu(DevNet n, Work w, int n_scen) {
+  const long long total = (long long)n_scen * n.nnz_gu;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / n.nnz_gu), e = (int)(t % n.nnz_gu);
+    const double v = w.gu[(size_t)s * n.nnz_gu + __ldg(n.guc_src + e)];
+    w.pkG[t] = make_double2(v, __longlong_as_double((long long)__ldg(n.guc_row + e) * n.C));
+  }
+}
+
+// e. K̂V = H_u − (P G_u)ᵀ Ψ̃ for a chunk of kCH columns of one tile: a column's
+// packed G_u entries are fetched lane-parallel (the next column's while this one
+// is gathered), its Ψ̃ rows gathered kPG at a time; the chunk is transposed in
+// SMEM so every direction's run of kCH outputs is stored contiguously.
+template <int C>
+__global__ void __launch_bounds__(kThreads) k_proj(DevNet n, Work w, int N, double* __restrict__ KV) {
+  constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL, kPG = 4;
+  __shared__ double T[C][kCH + 1];
+  const int ntile = (N + C - 1) / C;
+  const int c0 = blockIdx.x * kCH, tile = blockIdx.y, s = blockIdx.z;
+  const size_t cta = (size_t)s * ntile + tile;
+  const int lane = threadIdx.x % W, team = threadIdx.x / W, nteam = blockDim.x / W;
+  const unsigned mask = team_mask<W>();
+  const int n_u = n.n_u;
+  const double* Y = w.slabW + cta * n.n_x * C;
+  const double* Hs = w.hu + cta * n_u * C;
+  const double2* pg = w.pkG + (size_t)s * n.nnz_gu;
+  const int cend = min(kCH, n_u - c0);
+  int cc = team, e0n = 0, nen = 0;
+  double2 qn = make_double2(0.0, 0.0);
+  if (cc < cend) {
+    e0n = __ldg(n.guc_ptr + c0 + cc); nen = __ldg(n.guc_ptr + c0 + cc + 1) - e0n;
+    if (lane < nen) qn = __ldg(pg + e0n + lane);
+  }
+  for (; cc < cend; cc += nteam) {
+    const int c = c0 + cc, e0 = e0n, ne = nen;
+    const double2 q = qn;
+    if (cc + nteam < cend) {
+      e0n = __ldg(n.guc_ptr + c + nteam); nen = __ldg(n.guc_ptr + c + nteam + 1) - e0n;
+      qn = lane < nen ? __ldg(pg + e0n + lane) : make_double2(0.0, 0.0);
+    }
+    double acc[CPL];
 #pragma unroll
-      for (int j = 0; j < CPL; ++j) acc[j] = Hs[(size_t)c * C + lane + W * j];
-      for (int e = __ldg(n.guc_ptr + c); e < __ldg(n.guc_ptr + c + 1); ++e) {
-        const double gv = gu[__ldg(n.guc_src + e)];
-        const size_t row = (size_t)__ldg(n.guc_row + e) * C;
+    for (int j = 0; j < CPL; ++j) acc[j] = Hs[(size_t)c * C + lane + W * j];
+    for (int b = 0; b < ne; b += kPG) {
+      double gv[kPG], y[kPG][CPL];
 #pragma unroll
-        for (int j = 0; j < CPL; ++j) acc[j] -= gv * Y[row + lane + W * j];
+      for (int t = 0; t < kPG; ++t) {
+        const int ix = (b + t) & (W - 1);
+        double2 qe;
+        if (ne <= W) {
+          qe.x = __shfl_sync(mask, q.x, ix, W);
+          qe.y = __shfl_sync(mask, q.y, ix, W);
+        } else {
+          qe = b + t < ne ? __ldg(pg + e0 + b + t) : make_double2(0.0, 0.0);
+        }
+        const bool on = b + t < ne;
+        gv[t] = on ? qe.x : 0.0;
+        const int rowC = __double2loint(qe.y);
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) y[t][j] = on ? Y[(size_t)rowC + lane + W * j] : 0.0;
       }
 #pragma unroll
-      for (int j = 0; j < CPL; ++j) T[lane + W * j][cc] = acc[j];
+      for (int t = 0; t < kPG; ++t)
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) acc[j] -= gv[t] * y[t][j];
     }
-    __syncthreads();
-    const int w_c = min(kCH, n_u - c0);
-    for (int idx = threadIdx.x; idx < C * kCH; idx += blockDim.x) {
-      const int jl = idx / kCH, cc = idx % kCH;
-      const int jj = tile * C + jl;
-      if (jj < N && cc < w_c) KV[((size_t)s * N + jj) * n_u + c0 + cc] = T[jl][cc];
-    }
-    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) T[lane + W * j][cc] = acc[j];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < C * kCH; idx += blockDim.x) {
+    const int jl = idx / kCH, k = idx % kCH;
+    const int jj = tile * C + jl;
+    if (jj < N && k < cend) KV[((size_t)s * N + jj) * n_u + c0 + k] = T[jl][k];
   }
 }
 
@@ -640,6 +689,8 @@ template <int C>
 void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int col0, int N, double* KV,
                 cudaStream_t st, cudaEvent_t* ev) {
   const int ntile = (N + C - 1) / C;
+  k_pack_gu<<<(int)std::min<long long>(4096, ((long long)n_scen * n.nnz_gu + kThreads - 1) / kThreads), kThreads, 0,
+              st>>>(n, w, n_scen);
   if (ev) cudaEventRecord(ev[0], st);
   const int rt = (V == nullptr && col0 % C == 0) ? col0 / C : -1;  // canonical tile of the call's first tile
   k_fwd<C><<<dim3(ntile, n_scen), kThreads, rt >= 0 ? n.bmw * sizeof(unsigned) : 0, st>>>(n, w, V, col0, N, rt);
@@ -648,8 +699,10 @@ void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int
   if (ev) cudaEventRecord(ev[2], st);
   k_hvp<C><<<dim3((n.n_b + kBusPerCta - 1) / kBusPerCta, ntile, n_scen), kThreads, 0, st>>>(n, w, V, col0, N);
   if (ev) cudaEventRecord(ev[3], st);
-  k_adj<C><<<dim3(ntile, n_scen), kThreads, 0, st>>>(n, w, N, KV);
+  k_adj<C><<<dim3(ntile, n_scen), kThreads, 0, st>>>(n, w, N);
   if (ev) cudaEventRecord(ev[4], st);
+  k_proj<C><<<dim3((n.n_u + kCH - 1) / kCH, ntile, n_scen), kThreads, 0, st>>>(n, w, N, KV);
+  if (ev) cudaEventRecord(ev[7], st);
 }
 
 }  // namespace
@@ -675,7 +728,7 @@ int launch_reduce(const DevNet& n, const Work& w, int C, int n_scen, const doubl
     case 16: launch_all<16>(n, w, n_scen, V, col0, N, KV, st, ev); break;
     default: launch_all<8>(n, w, n_scen, V, col0, N, KV, st, ev); break;
   }
-  return 4;
+  return 6;
 }
 
 }  // namespace pf

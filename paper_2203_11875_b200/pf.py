@@ -182,15 +182,15 @@ class Network:
     def launch_count(self):
         return int(self._lib.pf_launch_count(self._h))
 
-    KERNELS = ("k_fwd", "k_mu", "k_hvp", "k_adj", "k_lu")
+    KERNELS = ("k_fwd", "k_mu", "k_hvp", "k_adj", "k_lu", "k_proj")
 
     def profile(self, enable=True):
         self._check(self._lib.pf_profile(self._h, int(enable)), "pf_profile")
 
     def kernel_times(self):
         """Per-kernel ms of the last reduction / jacobian calls (profiling on)."""
-        ms = (ctypes.c_float * 5)()
-        k = self._lib.pf_kernel_times(self._h, ctypes.cast(ms, ctypes.c_void_p), 5)
+        ms = (ctypes.c_float * 6)()
+        k = self._lib.pf_kernel_times(self._h, ctypes.cast(ms, ctypes.c_void_p), 6)
         return {self.KERNELS[i]: float(ms[i]) for i in range(k)}
 
     # ---------------------------------------------------------------- compute
