@@ -27,7 +27,11 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kCH = 64;        // u-columns per transposed output chunk
-constexpr int kBusPerCta = 64; // buses per k_hvp / k_mu CTA
+#ifndef PF_BUS_PER_CTA
+#define PF_BUS_PER_CTA 128
+#endif
+constexpr int kBusPerCta = 64;              // buses per k_mu CTA
+constexpr int kHvpBusPerCta = PF_BUS_PER_CTA; // buses per k_hvp CTA (a compact run of the postorder)
 #ifndef PF_DOT_W
 #define PF_DOT_W 4
 #endif
@@ -524,9 +528,9 @@ __global__ void __launch_bounds__(kThreads) k_hvp(DevNet n, Work w, const double
   const double* MU = w.mu + cta * n.n_g * 2 * C;
   double* Y = w.slabW + cta * n.n_x * C;
   double* Hs = w.hu + cta * n.n_u * C;
-  const int k1 = min(n_b, (int)(blockIdx.x + 1) * kBusPerCta);
+  const int k1 = min(n_b, (int)(blockIdx.x + 1) * kHvpBusPerCta);
   // buses in elimination order: a chunk's own θ/v rows are contiguous slab rows
-  for (int kb = blockIdx.x * kBusPerCta + team; kb < k1; kb += nteam) {
+  for (int kb = blockIdx.x * kHvpBusPerCta + team; kb < k1; kb += nteam) {
     const int i = __ldg(n.hvp_bus + kb);
     const int pt = __ldg(n.bus_pth + i), pv = __ldg(n.bus_pv + i), uv = __ldg(n.u_v + i);
     double dvi[CPL], dthi[CPL], mPi[CPL], mQi[CPL], hv[CPL], hth[CPL];
@@ -697,7 +701,7 @@ void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int
   if (ev) cudaEventRecord(ev[1], st);
   k_mu<C><<<dim3((n.n_gb + kBusPerCta - 1) / kBusPerCta, ntile, n_scen), kThreads, 0, st>>>(n, w, V, col0, N);
   if (ev) cudaEventRecord(ev[2], st);
-  k_hvp<C><<<dim3((n.n_b + kBusPerCta - 1) / kBusPerCta, ntile, n_scen), kThreads, 0, st>>>(n, w, V, col0, N);
+  k_hvp<C><<<dim3((n.n_b + kHvpBusPerCta - 1) / kHvpBusPerCta, ntile, n_scen), kThreads, 0, st>>>(n, w, V, col0, N);
   if (ev) cudaEventRecord(ev[3], st);
   k_adj<C><<<dim3(ntile, n_scen), kThreads, 0, st>>>(n, w, N);
   if (ev) cudaEventRecord(ev[4], st);
