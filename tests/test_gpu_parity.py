@@ -346,30 +346,38 @@ def test_capacity_and_argument_errors(pfmod):
 @pytest.mark.slow
 @pytest.mark.parametrize("name", ["case2869", "case9241"])
 def test_full_size_sampled_columns(pfmod, name):
-    """Full BASELINE sizes in the bench's launch configuration (all n_u
-    directions of every scenario in one call): sampled columns vs the
-    oracle's adjoint route computed one column at a time (SuperLU solves)."""
+    """Full BASELINE sizes in the bench's launch configuration — case9241: the 8
+    scenarios of config 5 in one call with all n_u directions (64-direction
+    tiles, sparse-RHS reach, subtree schedules), case2869: 2 scenarios —
+    sampled columns vs the oracle's adjoint route computed one column at a time
+    (SuperLU solves) on the first and last scenario, then the condensed-KKT
+    Cholesky + solve of all scenarios at once vs the oracle's on those two."""
     import torch
     net, pt = table1_grid(name)
-    S = 2
-    pts = [pt, make_scenario(net, pt, 1)]
+    S = 8 if name == "case9241" else 2
+    pts = [pt] + [make_scenario(net, pt, s) for s in range(1, S)]
+    checked = [0, S - 1]
     part = O.partition(net)
     n_u = part["n_u"]
     h = pfmod.Network(net, max_batch=n_u, max_scen=S)
+    if name == "case9241":
+        assert h.dims["tile_cols"] == 64  # the bench's tile width
     KV, info = _run_khat(pfmod, h, net, pts)
     assert info.tolist() == [0] * S
+    assert np.all(np.isfinite(KV))
     rng = np.random.default_rng(11)
     cols = np.unique(np.concatenate([[0, n_u - 1, part["n_u"] // 2], rng.choice(n_u, 5, replace=False)]))
-    for s, p in enumerate(pts):
+    for s in checked:
+        p = pts[s]
         Gx, Gu, A = O.jacobians(net, part, p)
         K = O.kkt_K(net, part, p, p["lam"], p["y"], p["sigma_s"], p["sigma_x"])
         ref = O.reduce_columns(K, Gx, Gu, cols)
         got = KV[s][cols].T
         assert rel_err(got, ref) <= TOL, (name, s)
-        assert np.all(np.isfinite(KV[s]))
     # the condensed-KKT Cholesky + solve at full size (bench launch: all scenarios at once)
-    Khs = [0.5 * (KV[s] + KV[s].T) for s in range(S)]
-    delta = max(0.0, -min(np.linalg.eigvalsh(Khs[s] + np.diag(pts[s]["sigma_u"])).min() for s in range(S))) * 1.5 + 1.0
+    Khs = {s: 0.5 * (KV[s] + KV[s].T) for s in checked}
+    delta = max(0.0, -min(np.linalg.eigvalsh(Khs[s] + np.diag(pts[s]["sigma_u"])).min() for s in checked)) * 1.5 + 1.0
+    delta = max(delta, 1e6)  # every scenario PD (the bench's δ_w search lands at 1e6 on these points)
     b = np.random.default_rng(12).standard_normal((S, 1, n_u))
     K, rhs = dev(KV.copy()), dev(b.copy())
     info = torch.empty(S, dtype=torch.int32, device="cuda")
@@ -377,7 +385,7 @@ def test_full_size_sampled_columns(pfmod, name):
     torch.cuda.synchronize()
     assert info.cpu().tolist() == [0] * S
     Lg = K.cpu().numpy()
-    for s in range(S):
+    for s in checked:
         Lo, io = O.cholesky(O.condensed(Khs[s], pts[s]["sigma_u"], delta))
         assert io == 0
         assert rel_err(Lg[s].T, Lo) <= TOL, (name, s)
