@@ -221,6 +221,7 @@ struct FromRhs {
     for (int j = 0; j < CPL; ++j) a[j] = 0.0;
     for (int e = __ldg(gur_ptr + r); e < __ldg(gur_ptr + r + 1); ++e) {
       const int c = __ldg(gur_col + e);
+      if (!Vs && (c < base || c >= base + nvalid)) continue;  // unit directions: only the tile's columns
       const double g = gu[__ldg(gur_src + e)];
 #pragma unroll
       for (int j = 0; j < CPL; ++j) {
