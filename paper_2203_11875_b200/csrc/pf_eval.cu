@@ -248,7 +248,7 @@ constexpr int kLuThreads = 512;
 constexpr int kLuStageMin = 8;    // rows with at least this many pivots stage their working set
 constexpr int kLuMaxPiv = 128;    // … and at most this many
 constexpr int kLuStageCap = 768;  // update entries staged per warp
-constexpr int kLuStageWarps = 4;  // warps of a CTA with a staging area
+constexpr int kLuStageWarps = 6;  // warps of a CTA with a staging area
 
 // A warp's staging area for one long LU row: per pivot a its 1/u_kk and the
 // offset of its update list; the lists' values (pivot U row) and targets.
@@ -326,9 +326,8 @@ __global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int CS) {
   const double* jb = w.jb + (size_t)s * n.nnz_jb;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int gthread = sub * blockDim.x + threadIdx.x, nthread = CS * blockDim.x;
-  // blocks go to the cluster's CTAs round-robin, so a narrow level puts at most a
-  // few rows on each CTA (on its low warps, which own the staging areas)
-  const int gwarp = warp * CS + sub, ngwarp = CS * nwarp;
+  // blocks go to the cluster's CTAs round-robin (below), so a narrow level puts at
+  // most a few rows on each CTA, on its low warps, which own the staging areas
   if (gthread == 0) w.info[s] = INT_MAX;
   for (int r = gthread; r < n.n_x; r += nthread) {
     double mx = 0.0;
@@ -360,59 +359,85 @@ __global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int CS) {
   st.q0 = st.u0 + kLuMaxPiv;
   st.dst = st.q0 + kLuMaxPiv;
   double* invd = w.invd + (size_t)s * n.n_x;
+  // Blocks go to warp PAIRS: the θ row of a bus block on the even warp, its v row on
+  // the odd one.  The v row depends on the θ row only through its last pivot (the
+  // intra-block entry), so both chains run at once; the v row applies that pivot
+  // from the θ row's workspace after a pair barrier.
+  const int pw = warp >> 1, hv = warp & 1;
+  const int gpair = pw * CS + sub, ngpair = CS * (nwarp >> 1);
   for (int lev = 0; lev < n.nlevL; ++lev) {
     const int b0 = __ldg(n.levL_ptr + lev), b1 = __ldg(n.levL_ptr + lev + 1);
-    for (int bi = b0 + gwarp; bi < b1; bi += ngwarp) {
+    for (int bi = b0 + gpair; bi < b1; bi += ngpair) {
       const int p = __ldg(n.levL_blk + bi);
-      for (int r = __ldg(n.blk_ptr + p); r < __ldg(n.blk_ptr + p + 1); ++r) {
-        const int base = __ldg(n.lu_ptr + r), len = __ldg(n.lu_ptr + r + 1) - base;
-        const int dl = __ldg(n.lu_diag + r) - base;
+      const int rb = __ldg(n.blk_ptr + p), nrow = __ldg(n.blk_ptr + p + 1) - rb;
+      const int r = rb + hv;
+      int base = 0, len = 0, dl = 0;
+      bool defer = false;
+      if (hv < nrow) {
+        base = __ldg(n.lu_ptr + r); len = __ldg(n.lu_ptr + r + 1) - base;
+        dl = __ldg(n.lu_diag + r) - base;
+        defer = hv == 1 && dl > 0 && __ldg(n.lu_idx + base + dl - 1) == rb;
+        if (hv == 1 && !defer) asm volatile("bar.sync %0, 64;" ::"r"(1 + pw) : "memory");  // no intra entry: wait
         for (int a = lane; a < len; a += 32) ws[a] = __ldcg(lu + base + a);
         __syncwarp();
-        if (warp < kLuStageWarps && dl >= kLuStageMin && dl <= kLuMaxPiv && stage_row(n, lu, invd, base, dl, lane, st)) {
-          // long (separator) row: its whole IKJ working set is in SMEM, the chain runs there
-          for (int a = 0; a < dl; ++a) {
-            const double l = ws[a] * st.pin[a];
-            const int o = st.off[a], cnt = st.off[a + 1] - o;
-            for (int t = lane; t < cnt; t += 32) ws[st.dst[o + t]] -= l * st.val[o + t];
-            __syncwarp();  // the next pivot's entry may just have been updated
-            if (lane == 0) ws[a] = l;  // (entry a is not read again by the chain)
-          }
-          __syncwarp();
-        } else {
-          // IKJ over the row's L entries; the U row of the next pivot and the
-          // update targets are prefetched into registers while this one runs.
-          double pu[4], pin = 0.0;
-          int pd[4], pq0 = 0, pcnt = 0, pu0 = 0;
-          auto fetch = [&](int a) {
-            const int e = base + a, k = __ldg(n.lu_idx + e);
-            pu0 = __ldg(n.lu_diag + k) + 1;
-            pq0 = __ldg(n.upd_ptr + e);
-            pcnt = __ldg(n.upd_ptr + e + 1) - pq0;
-            pin = __ldcg(invd + k);
-  #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int t = lane + 32 * j;
-              pu[j] = t < pcnt ? __ldcg(lu + pu0 + t) : 0.0;
-              pd[j] = t < pcnt ? __ldg(n.upd_dst + pq0 + t) : 0;
+        const int np = defer ? dl - 1 : dl;  // pivots of this pass
+          if (warp < kLuStageWarps && np >= kLuStageMin && np <= kLuMaxPiv && stage_row(n, lu, invd, base, np, lane, st)) {
+            // long (separator) row: its whole IKJ working set is in SMEM, the chain runs there
+            for (int a = 0; a < np; ++a) {
+              const double l = ws[a] * st.pin[a];
+              const int o = st.off[a], cnt = st.off[a + 1] - o;
+              for (int t = lane; t < cnt; t += 32) ws[st.dst[o + t]] -= l * st.val[o + t];
+              __syncwarp();  // the next pivot's entry may just have been updated
+              if (lane == 0) ws[a] = l;  // (entry a is not read again by the chain)
             }
-          };
-          if (dl > 0) fetch(0);
-          for (int a = 0; a < dl; ++a) {
-            const double cu[4] = {pu[0], pu[1], pu[2], pu[3]};
-            const int cd[4] = {pd[0], pd[1], pd[2], pd[3]};
-            const double cin = pin;
-            const int q0 = pq0, cnt = pcnt, u0 = pu0;
-            if (a + 1 < dl) fetch(a + 1);
-            const double l = ws[a] * cin;
-  #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (lane + 32 * j < cnt) ws[cd[j]] -= l * cu[j];
-            for (int t = lane + 128; t < cnt; t += 32) ws[__ldg(n.upd_dst + q0 + t)] -= l * __ldcg(lu + u0 + t);
             __syncwarp();
-            if (lane == 0) ws[a] = l;
+          } else {
+            // IKJ over the row's L entries; the U row of the next pivot and the
+            // update targets are prefetched into registers while this one runs.
+            double pu[4], pin = 0.0;
+            int pd[4], pq0 = 0, pcnt = 0, pu0 = 0;
+            auto fetch = [&](int a) {
+              const int e = base + a, k = __ldg(n.lu_idx + e);
+              pu0 = __ldg(n.lu_diag + k) + 1;
+              pq0 = __ldg(n.upd_ptr + e);
+              pcnt = __ldg(n.upd_ptr + e + 1) - pq0;
+              pin = __ldcg(invd + k);
+    #pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int t = lane + 32 * j;
+                pu[j] = t < pcnt ? __ldcg(lu + pu0 + t) : 0.0;
+                pd[j] = t < pcnt ? __ldg(n.upd_dst + pq0 + t) : 0;
+              }
+            };
+            if (np > 0) fetch(0);
+            for (int a = 0; a < np; ++a) {
+              const double cu[4] = {pu[0], pu[1], pu[2], pu[3]};
+              const int cd[4] = {pd[0], pd[1], pd[2], pd[3]};
+              const double cin = pin;
+              const int q0 = pq0, cnt = pcnt, u0 = pu0;
+              if (a + 1 < np) fetch(a + 1);
+              const double l = ws[a] * cin;
+    #pragma unroll
+              for (int j = 0; j < 4; ++j)
+                if (lane + 32 * j < cnt) ws[cd[j]] -= l * cu[j];
+              for (int t = lane + 128; t < cnt; t += 32) ws[__ldg(n.upd_dst + q0 + t)] -= l * __ldcg(lu + u0 + t);
+              __syncwarp();
+              if (lane == 0) ws[a] = l;
+            }
           }
-        }
+      }
+      if (nrow == 2 && (hv == 0 || defer)) asm volatile("bar.sync %0, 64;" ::"r"(1 + pw) : "memory");
+      if (defer) {  // the θ row's pivot, from its workspace
+        const double* ws0 = lu_ws + (size_t)(warp - 1) * n.lu_maxlen;
+        const int base0 = __ldg(n.lu_ptr + rb), dl0 = __ldg(n.lu_diag + rb) - base0;
+        const int e = base + dl - 1, q0 = __ldg(n.upd_ptr + e), cnt = __ldg(n.upd_ptr + e + 1) - q0;
+        const int o0 = dl0 + 1;  // U part of the θ row in ws0
+        const double l = ws[dl - 1] * (1.0 / ws0[dl0]);
+        for (int t = lane; t < cnt; t += 32) ws[__ldg(n.upd_dst + q0 + t)] -= l * ws0[o0 + t];
+        __syncwarp();
+        if (lane == 0) ws[dl - 1] = l;
+      }
+      if (hv < nrow) {
         __syncwarp();
         for (int a = lane; a < len; a += 32) __stcg(lu + base + a, ws[a]);
         if (lane == 0) {
@@ -422,6 +447,7 @@ __global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int CS) {
         }
         __syncwarp();
       }
+      if (nrow == 2) asm volatile("bar.sync %0, 64;" ::"r"(1 + pw) : "memory");  // ws0 free for the next block
     }
     cluster.sync();
 #ifdef PF_LU_TRACE
