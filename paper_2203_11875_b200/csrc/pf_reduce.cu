@@ -30,7 +30,18 @@ constexpr int kCH = 64;        // u-columns per transposed output chunk
 #ifndef PF_BUS_PER_CTA
 #define PF_BUS_PER_CTA 128
 #endif
-constexpr int kBusPerCta = 64;              // buses per k_mu CTA
+#ifndef PF_MU_BUS_PER_CTA
+#define PF_MU_BUS_PER_CTA 64
+#endif
+constexpr int kBusPerCta = PF_MU_BUS_PER_CTA;  // generator buses per k_mu CTA
+#ifndef PF_HVP_MIN_BLOCKS
+#define PF_HVP_MIN_BLOCKS 2
+#endif
+constexpr int kHvpMinBlocks = PF_HVP_MIN_BLOCKS;  // CTAs per SM k_hvp is register-capped for
+#ifndef PF_HVP_TILES
+#define PF_HVP_TILES 2
+#endif
+constexpr int kHvpTiles = PF_HVP_TILES;  // direction tiles per k_hvp CTA
 constexpr int kHvpBusPerCta = PF_BUS_PER_CTA; // buses per k_hvp CTA (a compact run of the postorder)
 #ifndef PF_DOT_W
 #define PF_DOT_W 4
@@ -374,15 +385,17 @@ __device__ __forceinline__ void sweep(const int4* __restrict__ tasks, const int*
 }
 
 // ---------------------------------------------------------------- directions in bus space
+// Lane ℓ of a team owns the tile's columns ℓ·CPL … ℓ·CPL+CPL−1 (as in the sweeps),
+// so a slab row's directions are one 16-byte access per lane pair of columns.
 template <int C>
 struct Dir {
   const double* X;   // Z̃ slab of the tile
-  const double* Vs;  // dense directions: V[s][tile*C + lane + W j][·] rows for j = 0 (stride n_u per column)
-  int lane, col, nvalid, n_u;  // col = col0 + tile*C + lane (unit directions); nvalid = directions in the tile
+  const double* Vs;  // dense directions: V[s][tile*C + k][·], column k at Vs + k n_u
+  int lane, col, nvalid, n_u;  // col = col0 + tile*C (unit directions); nvalid = directions in the tile
   __device__ __forceinline__ double vdir(int c, int j) const {
-    constexpr int W = Geo<C>::W;
-    if (lane + W * j >= nvalid) return 0.0;
-    return Vs ? Vs[(size_t)W * j * n_u + c] : (c == col + W * j ? 1.0 : 0.0);
+    const int k = lane * Geo<C>::CPL + j;
+    if (k >= nvalid) return 0.0;
+    return Vs ? Vs[(size_t)k * n_u + c] : (c == col + k ? 1.0 : 0.0);
   }
 };
 
@@ -391,24 +404,54 @@ __device__ __forceinline__ Dir<C> make_dir(const DevNet& n, const Work& w, const
                                            int tile, size_t cta, int lane) {
   Dir<C> d;
   d.lane = lane;
-  d.col = col0 + tile * C + lane;
+  d.col = col0 + tile * C;
   d.nvalid = min(C, N - tile * C);
   d.n_u = n.n_u;
   d.X = w.slabZ + cta * n.n_x * C;
-  d.Vs = V ? V + ((size_t)s * N + tile * C + lane) * n.n_u : nullptr;
+  d.Vs = V ? V + ((size_t)s * N + tile * C) * n.n_u : nullptr;
   return d;
+}
+
+// this lane's CPL columns of row r of a C-wide slab (load / store)
+template <int C>
+__device__ __forceinline__ void row_ld(const double* S, int r, int lane, double* o) {
+  constexpr int CPL = Geo<C>::CPL;
+  const double* p = S + (size_t)r * C + lane * CPL;
+  if constexpr (CPL == 1) {
+    o[0] = *p;
+  } else {
+#pragma unroll
+    for (int q = 0; q < CPL / 2; ++q) {
+      const double2 v = reinterpret_cast<const double2*>(p)[q];
+      o[2 * q] = v.x; o[2 * q + 1] = v.y;
+    }
+  }
+}
+template <int C>
+__device__ __forceinline__ void row_st(double* S, int r, int lane, const double* o) {
+  constexpr int CPL = Geo<C>::CPL;
+  double* p = S + (size_t)r * C + lane * CPL;
+  if constexpr (CPL == 1) {
+    *p = o[0];
+  } else {
+#pragma unroll
+    for (int q = 0; q < CPL / 2; ++q) reinterpret_cast<double2*>(p)[q] = make_double2(o[2 * q], o[2 * q + 1]);
+  }
 }
 
 // dθ, dv at a bus (own rows) and at the far end of an incidence record
 // {line, θ row, v row or −1−(u index), 1·from | 2·(gen + 1)} (pf_api.cu).
 template <int C>
 __device__ __forceinline__ void dirs_at(const Dir<C>& d, int pth, int pv, double* dth, double* dv) {
-  constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
+  constexpr int CPL = Geo<C>::CPL;
+  if (pth >= 0) row_ld<C>(d.X, pth, d.lane, dth);
+  else
 #pragma unroll
-  for (int j = 0; j < CPL; ++j) {
-    dth[j] = pth >= 0 ? d.X[(size_t)pth * C + d.lane + W * j] : 0.0;
-    dv[j] = pv >= 0 ? d.X[(size_t)pv * C + d.lane + W * j] : d.vdir(-1 - pv, j);
-  }
+    for (int j = 0; j < CPL; ++j) dth[j] = 0.0;
+  if (pv >= 0) row_ld<C>(d.X, pv, d.lane, dv);
+  else
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) dv[j] = d.vdir(-1 - pv, j);
 }
 
 // Line block of K (pf_eval.cu k_prep_line): H (3×3 sym) and J (4×3) on the
@@ -466,130 +509,186 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
 // ---------------------------------------------------------------- c1
 // μ_A at the generator buses: dG = R_r M dψ = Σ_{ends at i} J_end · d_loc plus
 // the shunt part of G_ii ψ^d; μ_A = Σ_r dG (+ 2c1 dG on P_r0, folded into Σ_rP).
-template <int C>
+template <int C, int NT>
 __global__ void __launch_bounds__(kThreads) k_mu(DevNet n, Work w, const double* __restrict__ V, int col0, int N) {
-  constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
+  constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL, D = NT * CPL;  // NT tiles per CTA, as in k_hvp
   const int ntile = (N + C - 1) / C;
-  const int tile = blockIdx.y, s = blockIdx.z;
-  const size_t cta = (size_t)s * ntile + tile;
+  const int s = blockIdx.z;
   const int lane = threadIdx.x % W, team = threadIdx.x / W, nteam = blockDim.x / W;
-  const Dir<C> d = make_dir<C>(n, w, V, col0, N, s, tile, cta, lane);
+  Dir<C> d[NT];
+  double* MU[NT];
+  bool on[NT];
+#pragma unroll
+  for (int u = 0; u < NT; ++u) {
+    const int t = blockIdx.y * NT + u, tile = min(t, ntile - 1);
+    const size_t cta = (size_t)s * ntile + tile;
+    on[u] = t < ntile;
+    d[u] = make_dir<C>(n, w, V, col0, N, s, tile, cta, lane);
+    MU[u] = w.mu + cta * n.n_g * 2 * C;
+  }
   const int n_b = n.n_b;
   const double* lb = w.lblk + (size_t)s * n.n_l * LB_N;
   const double* bs = w.bs + (size_t)s * BS_N * n_b;
-  double* MU = w.mu + cta * n.n_g * 2 * C;
   const int g1 = min(n.n_gb, (int)(blockIdx.x + 1) * kBusPerCta);
   for (int gi = blockIdx.x * kBusPerCta + team; gi < g1; gi += nteam) {
     const int i = __ldg(n.gbus + gi);
-    double dvi[CPL], dthi[CPL], dP[CPL], dQ[CPL];
-    dirs_at<C>(d, __ldg(n.bus_pth + i), __ldg(n.bus_pv + i) >= 0 ? __ldg(n.bus_pv + i) : -1 - __ldg(n.u_v + i), dthi, dvi);
+    const int pth = __ldg(n.bus_pth + i), pvi = __ldg(n.bus_pv + i) >= 0 ? __ldg(n.bus_pv + i) : -1 - __ldg(n.u_v + i);
+    double dvi[D], dthi[D], dP[D], dQ[D];
 #pragma unroll
-    for (int j = 0; j < CPL; ++j) { dP[j] = 0.0; dQ[j] = 0.0; }
+    for (int u = 0; u < NT; ++u) dirs_at<C>(d[u], pth, pvi, dthi + u * CPL, dvi + u * CPL);
+#pragma unroll
+    for (int k = 0; k < D; ++k) { dP[k] = 0.0; dQ[k] = 0.0; }
     for (int e = __ldg(n.inc_ptr + i); e < __ldg(n.inc_ptr + i + 1); ++e) {
       const int4 rec = __ldg(n.inc_rec + e);
       const bool from = rec.w & 1;
-      double dvo[CPL], dtho[CPL], J[12];
-      dirs_at<C>(d, rec.y, rec.z, dtho, dvo);
+      double dvo[D], dtho[D], J[12];
+#pragma unroll
+      for (int u = 0; u < NT; ++u) dirs_at<C>(d[u], rec.y, rec.z, dtho + u * CPL, dvo + u * CPL);
       load_j(lb + (size_t)rec.x * LB_N, J);
 #pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        const double dvf = from ? dvi[j] : dvo[j], dvt = from ? dvo[j] : dvi[j];
-        const double dD = from ? dthi[j] - dtho[j] : dtho[j] - dthi[j];
+      for (int k = 0; k < D; ++k) {
+        const double dvf = from ? dvi[k] : dvo[k], dvt = from ? dvo[k] : dvi[k];
+        const double dD = from ? dthi[k] - dtho[k] : dtho[k] - dthi[k];
         // rows (s_p, s_q) of this end
-        dP[j] += from ? J[0] * dvf + J[1] * dvt + J[2] * dD : J[6] * dvf + J[7] * dvt + J[8] * dD;
-        dQ[j] += from ? J[3] * dvf + J[4] * dvt + J[5] * dD : J[9] * dvf + J[10] * dvt + J[11] * dD;
+        dP[k] += from ? J[0] * dvf + J[1] * dvt + J[2] * dD : J[6] * dvf + J[7] * dvt + J[8] * dD;
+        dQ[k] += from ? J[3] * dvf + J[4] * dvt + J[5] * dD : J[9] * dvf + J[10] * dvt + J[11] * dD;
       }
     }
     const double vi = bs[BS_V * n_b + i], gsh = __ldg(n.gsh + i), bsh = __ldg(n.bsh + i);
     const double srp = bs[BS_SRP * n_b + i], srq = bs[BS_SRQ * n_b + i];
     const int g = __ldg(n.bus_gen + i);
 #pragma unroll
-    for (int j = 0; j < CPL; ++j) {
-      MU[(2 * g) * C + lane + W * j] = srp * (dP[j] + 2.0 * gsh * vi * dvi[j]);
-      MU[(2 * g + 1) * C + lane + W * j] = srq * (dQ[j] - 2.0 * bsh * vi * dvi[j]);
+    for (int k = 0; k < D; ++k) {
+      dP[k] = srp * (dP[k] + 2.0 * gsh * vi * dvi[k]);
+      dQ[k] = srq * (dQ[k] - 2.0 * bsh * vi * dvi[k]);
     }
+#pragma unroll
+    for (int u = 0; u < NT; ++u)
+      if (on[u]) {
+        row_st<C>(MU[u], 2 * g, lane, dP + u * CPL);
+        row_st<C>(MU[u], 2 * g + 1, lane, dQ + u * CPL);
+      }
   }
+  (void)W;
 }
 
 // ---------------------------------------------------------------- c2
 // [H_u; H_x] = K [V; Z]: per bus, Σ over incident lines of the line block
 // (H d_loc + Jᵀ μ_A(ends)) restricted to the bus's own (v, θ), plus the bus
 // terms 2w̄^d dv (ψ^d curvature), the shunt part of Mᵀμ_A, and Σ_x.
-template <int C>
-__global__ void __launch_bounds__(kThreads) k_hvp(DevNet n, Work w, const double* __restrict__ V, int col0, int N) {
-  constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
+template <int C, int NT>
+__global__ void __launch_bounds__(kThreads, kHvpMinBlocks) k_hvp(DevNet n, Work w, const double* __restrict__ V, int col0, int N) {
+  // NT direction tiles per CTA: the per-bus and per-line work (records, line
+  // blocks, index arithmetic) is shared by NT·C directions
+  constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL, D = NT * CPL;
   const int ntile = (N + C - 1) / C;
-  const int tile = blockIdx.y, s = blockIdx.z;
-  const size_t cta = (size_t)s * ntile + tile;
+  const int s = blockIdx.z;
   const int lane = threadIdx.x % W, team = threadIdx.x / W, nteam = blockDim.x / W;
-  const Dir<C> d = make_dir<C>(n, w, V, col0, N, s, tile, cta, lane);
   const int n_b = n.n_b;
+  Dir<C> d[NT];
+  const double* MU[NT];
+  double *Y[NT], *Hs[NT];
+  bool on[NT];
+#pragma unroll
+  for (int u = 0; u < NT; ++u) {
+    const int t = blockIdx.y * NT + u, tile = min(t, ntile - 1);  // a missing last tile repeats the previous one
+    const size_t cta = (size_t)s * ntile + tile;
+    on[u] = t < ntile;
+    d[u] = make_dir<C>(n, w, V, col0, N, s, tile, cta, lane);
+    MU[u] = w.mu + cta * n.n_g * 2 * C;
+    Y[u] = w.slabW + cta * n.n_x * C;
+    Hs[u] = w.hu + cta * n.n_u * C;
+  }
   const double* lb = w.lblk + (size_t)s * n.n_l * LB_N;
   const double* bs = w.bs + (size_t)s * BS_N * n_b;
-  const double* MU = w.mu + cta * n.n_g * 2 * C;
-  double* Y = w.slabW + cta * n.n_x * C;
-  double* Hs = w.hu + cta * n.n_u * C;
   const int k1 = min(n_b, (int)(blockIdx.x + 1) * kHvpBusPerCta);
   // buses in elimination order: a chunk's own θ/v rows are contiguous slab rows
   for (int kb = blockIdx.x * kHvpBusPerCta + team; kb < k1; kb += nteam) {
     const int i = __ldg(n.hvp_bus + kb);
     const int pt = __ldg(n.bus_pth + i), pv = __ldg(n.bus_pv + i), uv = __ldg(n.u_v + i);
-    double dvi[CPL], dthi[CPL], mPi[CPL], mQi[CPL], hv[CPL], hth[CPL];
-    dirs_at<C>(d, pt, pv >= 0 ? pv : -1 - uv, dthi, dvi);
+    double dvi[D], dthi[D], mPi[D], mQi[D], hv[D], hth[D];
     const int gi_own = __ldg(n.bus_gen + i);
 #pragma unroll
-    for (int j = 0; j < CPL; ++j) {
-      mPi[j] = gi_own >= 0 ? MU[(2 * gi_own) * C + lane + W * j] : 0.0;
-      mQi[j] = gi_own >= 0 ? MU[(2 * gi_own + 1) * C + lane + W * j] : 0.0;
-      hv[j] = 0.0; hth[j] = 0.0;
+    for (int u = 0; u < NT; ++u) {
+      dirs_at<C>(d[u], pt, pv >= 0 ? pv : -1 - uv, dthi + u * CPL, dvi + u * CPL);
+      if (gi_own >= 0) {
+        row_ld<C>(MU[u], 2 * gi_own, lane, mPi + u * CPL);
+        row_ld<C>(MU[u], 2 * gi_own + 1, lane, mQi + u * CPL);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      if (gi_own < 0) { mPi[k] = 0.0; mQi[k] = 0.0; }
+      hv[k] = 0.0; hth[k] = 0.0;
     }
     for (int e = __ldg(n.inc_ptr + i); e < __ldg(n.inc_ptr + i + 1); ++e) {
       const int4 rec = __ldg(n.inc_rec + e);
       const bool from = rec.w & 1;
       const int go = (rec.w >> 1) - 1;
-      double dvo[CPL], dtho[CPL], h[6];
-      dirs_at<C>(d, rec.y, rec.z, dtho, dvo);
+      double dvo[D], dtho[D], h[6];
+#pragma unroll
+      for (int u = 0; u < NT; ++u) dirs_at<C>(d[u], rec.y, rec.z, dtho + u * CPL, dvo + u * CPL);
       const double* p = lb + (size_t)rec.x * LB_N;
       load_h(p, h);
       const bool coupled = gi_own >= 0 || go >= 0;  // Jᵀ μ_A: only lines touching an r bus
-      double J[12];
-      if (coupled) load_j(p, J);
+      double J[12], mPo[D], mQo[D];
+      if (coupled) {
+        load_j(p, J);
 #pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        const double dvf = from ? dvi[j] : dvo[j], dvt = from ? dvo[j] : dvi[j];
-        const double dD = from ? dthi[j] - dtho[j] : dtho[j] - dthi[j];
+        for (int u = 0; u < NT; ++u) {
+          if (go >= 0) {
+            row_ld<C>(MU[u], 2 * go, lane, mPo + u * CPL);
+            row_ld<C>(MU[u], 2 * go + 1, lane, mQo + u * CPL);
+          } else {
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) { mPo[u * CPL + j] = 0.0; mQo[u * CPL + j] = 0.0; }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const double dvf = from ? dvi[k] : dvo[k], dvt = from ? dvo[k] : dvi[k];
+        const double dD = from ? dthi[k] - dtho[k] : dtho[k] - dthi[k];
         double hvo = from ? h[0] * dvf + h[1] * dvt + h[2] * dD : h[1] * dvf + h[3] * dvt + h[4] * dD;
         double hD = h[2] * dvf + h[4] * dvt + h[5] * dD;
         if (coupled) {
-          const double mPo = go >= 0 ? MU[(2 * go) * C + lane + W * j] : 0.0;
-          const double mQo = go >= 0 ? MU[(2 * go + 1) * C + lane + W * j] : 0.0;
-          const double mpf = from ? mPi[j] : mPo, mqf = from ? mQi[j] : mQo;
-          const double mpt = from ? mPo : mPi[j], mqt = from ? mQo : mQi[j];
+          const double mpf = from ? mPi[k] : mPo[k], mqf = from ? mQi[k] : mQo[k];
+          const double mpt = from ? mPo[k] : mPi[k], mqt = from ? mQo[k] : mQi[k];
           hvo += from ? J[0] * mpf + J[3] * mqf + J[6] * mpt + J[9] * mqt
                       : J[1] * mpf + J[4] * mqf + J[7] * mpt + J[10] * mqt;
           hD += J[2] * mpf + J[5] * mqf + J[8] * mpt + J[11] * mqt;
         }
-        hv[j] += hvo;
-        hth[j] += from ? hD : -hD;
+        hv[k] += hvo;
+        hth[k] += from ? hD : -hD;
       }
     }
     const double vi = bs[BS_V * n_b + i], gsh = __ldg(n.gsh + i), bsh = __ldg(n.bsh + i);
     const double wd2 = bs[BS_WD2 * n_b + i], sxv = bs[BS_SXV * n_b + i], sxt = bs[BS_SXT * n_b + i];
 #pragma unroll
-    for (int j = 0; j < CPL; ++j) {
-      const double v_ = hv[j] + wd2 * dvi[j] + 2.0 * vi * (gsh * mPi[j] - bsh * mQi[j]) + sxv * dvi[j];
-      const double t_ = hth[j] + sxt * dthi[j];
-      if (pt >= 0) Y[(size_t)pt * C + lane + W * j] = t_;
-      if (pv >= 0) Y[(size_t)pv * C + lane + W * j] = v_;
-      else Hs[(size_t)uv * C + lane + W * j] = v_;
+    for (int k = 0; k < D; ++k) {
+      hv[k] += wd2 * dvi[k] + 2.0 * vi * (gsh * mPi[k] - bsh * mQi[k]) + sxv * dvi[k];
+      hth[k] += sxt * dthi[k];
     }
+#pragma unroll
+    for (int u = 0; u < NT; ++u)
+      if (on[u]) {
+        if (pt >= 0) row_st<C>(Y[u], pt, lane, hth + u * CPL);
+        if (pv >= 0) row_st<C>(Y[u], pv, lane, hv + u * CPL);
+        else row_st<C>(Hs[u], uv, lane, hv + u * CPL);
+      }
   }
   if (blockIdx.x == 0)  // objective curvature on explicit p_g
     for (int g = team; g < n.n_g; g += nteam) {
       const int up = __ldg(n.u_p + g);
       if (up >= 0)
 #pragma unroll
-        for (int j = 0; j < CPL; ++j) Hs[(size_t)up * C + lane + W * j] = 2.0 * __ldg(n.c_quad + g) * d.vdir(up, j);
+        for (int u = 0; u < NT; ++u)
+          if (on[u]) {
+            double o[CPL];
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) o[j] = 2.0 * __ldg(n.c_quad + g) * d[u].vdir(up, j);
+            row_st<C>(Hs[u], up, lane, o);
+          }
     }
 }
 
@@ -654,8 +753,7 @@ __global__ void __launch_bounds__(kThreads) k_proj(DevNet n, Work w, int N, doub
       qn = lane < nen ? __ldg(pg + e0n + lane) : make_double2(0.0, 0.0);
     }
     double acc[CPL];
-#pragma unroll
-    for (int j = 0; j < CPL; ++j) acc[j] = Hs[(size_t)c * C + lane + W * j];
+    row_ld<C>(Hs, c, lane, acc);
     for (int b = 0; b < ne; b += kPG) {
       double gv[kPG], y[kPG][CPL];
 #pragma unroll
@@ -671,8 +769,10 @@ __global__ void __launch_bounds__(kThreads) k_proj(DevNet n, Work w, int N, doub
         const bool on = b + t < ne;
         gv[t] = on ? qe.x : 0.0;
         const int rowC = __double2loint(qe.y);
+        if (on) row_ld<C>(Y + rowC, 0, lane, y[t]);
+        else
 #pragma unroll
-        for (int j = 0; j < CPL; ++j) y[t][j] = on ? Y[(size_t)rowC + lane + W * j] : 0.0;
+          for (int j = 0; j < CPL; ++j) y[t][j] = 0.0;
       }
 #pragma unroll
       for (int t = 0; t < kPG; ++t)
@@ -680,7 +780,7 @@ __global__ void __launch_bounds__(kThreads) k_proj(DevNet n, Work w, int N, doub
         for (int j = 0; j < CPL; ++j) acc[j] -= gv[t] * y[t][j];
     }
 #pragma unroll
-    for (int j = 0; j < CPL; ++j) T[lane + W * j][cc] = acc[j];
+    for (int j = 0; j < CPL; ++j) T[lane * CPL + j][cc] = acc[j];
   }
   __syncthreads();
   for (int idx = threadIdx.x; idx < C * kCH; idx += blockDim.x) {
@@ -700,9 +800,11 @@ void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int
   const int rt = (V == nullptr && col0 % C == 0) ? col0 / C : -1;  // canonical tile of the call's first tile
   k_fwd<C><<<dim3(ntile, n_scen), kThreads, rt >= 0 ? n.bmw * sizeof(unsigned) : 0, st>>>(n, w, V, col0, N, rt);
   if (ev) cudaEventRecord(ev[1], st);
-  k_mu<C><<<dim3((n.n_gb + kBusPerCta - 1) / kBusPerCta, ntile, n_scen), kThreads, 0, st>>>(n, w, V, col0, N);
+  k_mu<C, kHvpTiles><<<dim3((n.n_gb + kBusPerCta - 1) / kBusPerCta, (ntile + kHvpTiles - 1) / kHvpTiles, n_scen), kThreads,
+                       0, st>>>(n, w, V, col0, N);
   if (ev) cudaEventRecord(ev[2], st);
-  k_hvp<C><<<dim3((n.n_b + kHvpBusPerCta - 1) / kHvpBusPerCta, ntile, n_scen), kThreads, 0, st>>>(n, w, V, col0, N);
+  k_hvp<C, kHvpTiles><<<dim3((n.n_b + kHvpBusPerCta - 1) / kHvpBusPerCta, (ntile + kHvpTiles - 1) / kHvpTiles, n_scen),
+                        kThreads, 0, st>>>(n, w, V, col0, N);
   if (ev) cudaEventRecord(ev[3], st);
   k_adj<C><<<dim3(ntile, n_scen), kThreads, 0, st>>>(n, w, N);
   if (ev) cudaEventRecord(ev[4], st);
