@@ -64,8 +64,8 @@ struct Work {
   double* gu;      // [max_scen][nnz_gu]  G_u values (internal copy)
   double* lu;      // [max_scen][nnz_lu]  LU values (row-wise)
   double* luT;     // [max_scen][nnz_lu]  transposed values: luT[e] = lu[tpos[e]]
-  double2* pkA;    // [max_scen][nnz_lu]  packed {lu[e], bits(idx[e]*C)} for the L / U sweeps
-  double2* pkT;    // [max_scen][nnz_lu]  packed {luT[e], bits(idx[e]*C)} for the Uᵀ / Lᵀ sweeps
+  double2* pkA;    // [max_scen][nnz_lu]  packed {lu[e] (1/u_rr on the diagonal), bits(idx[e]*C)} for the L / U sweeps
+  double2* pkT;    // [max_scen][nnz_lu]  packed {luT[e] (1/u_rr on the diagonal), bits(idx[e]*C)} for the Uᵀ / Lᵀ sweeps
   double2* pkG;    // [max_scen][nnz_gu]  G_u by column (CSC): {value, bits(row*C)} for the projection
   double* rowmax;  // [max_scen][n_x]     pivot threshold scale (R18)
   double* invd;    // [max_scen][n_x]     1 / u_rr of the factorized rows

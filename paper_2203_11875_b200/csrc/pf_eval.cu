@@ -461,12 +461,16 @@ __global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int CS) {
   double* luT = w.luT + (size_t)s * n.nnz_lu;
   double2* pkA = w.pkA + (size_t)s * n.nnz_lu;
   double2* pkT = w.pkT + (size_t)s * n.nnz_lu;
+  // packed sweep entries {value, column·C}; a diagonal entry (its own transpose
+  // position) is packed as 1/u_rr, so the sweeps that divide multiply instead
   for (int e = gthread; e < n.nnz_lu; e += nthread) {
-    const double t = __ldcg(lu + __ldg(n.lu_tpos + e));
+    const int tp = __ldg(n.lu_tpos + e);
+    const double t = __ldcg(lu + tp);
     const double c = __longlong_as_double((long long)__ldg(n.lu_idx + e) * n.C);
     luT[e] = t;
-    pkA[e] = make_double2(__ldcg(lu + e), c);
-    pkT[e] = make_double2(t, c);
+    const double a = tp == e ? 1.0 / t : __ldcg(lu + e);
+    pkA[e] = make_double2(a, c);
+    pkT[e] = make_double2(tp == e ? a : t, c);
   }
 }
 

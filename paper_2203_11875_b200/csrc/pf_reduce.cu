@@ -312,11 +312,11 @@ __device__ __forceinline__ void run_seq(const int4* __restrict__ tasks, int firs
 #pragma unroll
       for (int j = 0; j < CPL; ++j) {
         double x0 = a0[j];
-        if (divide) x0 /= d0;
+        if (divide) x0 *= d0;
         x0p[j] = x0;
         if (k.two) {
           double x1 = a1[j] - intra * x0;
-          if (divide) x1 /= d1;
+          if (divide) x1 *= d1;
           x1p[j] = x1;
         }
       }
@@ -341,11 +341,11 @@ __device__ __forceinline__ void run_seq(const int4* __restrict__ tasks, int firs
         double x1 = 0.0;
         if (k.two) {
           x1 = a1[j];
-          if (divide) x1 /= d1;
+          if (divide) x1 *= d1;
           x1p[j] = x1;
         }
         double x0 = a0[j] - intra * x1;
-        if (divide) x0 /= d0;
+        if (divide) x0 *= d0;
         x0p[j] = x0;
       }
     }
