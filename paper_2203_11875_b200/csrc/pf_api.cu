@@ -311,6 +311,14 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
                              (from ? 1 : 0) | ((P.bus_gen[o] + 1) << 1));
     }
 
+  const std::vector<int>& hvp_order = h->hvp_order.size() == (size_t)n_b ? h->hvp_order : P.hvp_bus;
+  std::vector<int4> hvp_meta(n_b);
+  std::vector<int2> hvp_inc(n_b);
+  for (int kb = 0; kb < n_b; ++kb) {
+    const int i = hvp_order[kb];
+    hvp_meta[kb] = make_int4(i, P.bus_pth[i], P.bus_pv[i] >= 0 ? P.bus_pv[i] : -1 - P.u_v[i], P.bus_gen[i]);
+    hvp_inc[kb] = make_int2(P.inc_ptr[i], P.inc_ptr[i + 1] - P.inc_ptr[i]);
+  }
   bool ok = up(h, lf, &d.lf) && up(h, lt, &d.lt) && up(h, coef, &d.coef) && up(h, gsh, &d.gsh) &&
             up(h, bsh, &d.bsh) && up(h, gb, &d.gen_bus) && up(h, P.bus_gen, &d.bus_gen) &&
             up(h, cq, &d.c_quad) && up(h, cl, &d.c_lin) && up(h, pd, &d.p_d0) && up(h, qd, &d.q_d0) &&
@@ -328,7 +336,7 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
             up(h, P.levU_blk, &d.levU_blk) && up(h, P.guc_ptr, &d.guc_ptr) && up(h, P.guc_row, &d.guc_row) &&
             up(h, P.guc_src, &d.guc_src) && up(h, P.gur_ptr, &d.gur_ptr) && up(h, P.gur_col, &d.gur_col) &&
             up(h, P.gur_src, &d.gur_src) && up(h, P.bus_pth, &d.bus_pth) && up(h, P.bus_pv, &d.bus_pv) &&
-            up(h, gbus, &d.gbus) && up(h, rowmeta, &d.rowmeta) && up(h, h->hvp_order.size() == (size_t)n_b ? h->hvp_order : P.hvp_bus, &d.hvp_bus) &&
+            up(h, gbus, &d.gbus) && up(h, rowmeta, &d.rowmeta) && up(h, hvp_order, &d.hvp_bus) && up(h, hvp_meta, &d.hvp_meta) && up(h, hvp_inc, &d.hvp_inc) &&
             up(h, inc_rec, &d.inc_rec) && up(h, taskL, &d.taskL) && up(h, taskU, &d.taskU) &&
             up(h, taskLr, &d.taskLr) && up(h, levLr_ptr, &d.levLr_ptr) && up(h, rowbm, &d.rowbm) &&
             up(h, taskUa, &d.taskUa) && up(h, levUa_ptr, &d.levUa_ptr) && up(h, h->p1_task, &d.p1_task) &&

@@ -27,6 +27,8 @@ struct DevNet {
   const int *gbus;              // [n_gb] generator buses ascending (the r buses)
   const int4 *rowmeta;          // [n_x] {lu_ptr[r], lu_diag[r], lu_ptr[r+1], block of r}
   const int *hvp_bus;           // [n_b] buses in elimination order, the reference bus last
+  const int4 *hvp_meta;         // [n_b] per hvp_bus position: {bus, θ row, v row or −1−(u index), gen or −1}
+  const int2 *hvp_inc;          // [n_b] per hvp_bus position: {first incidence record, degree}
   const int4 *taskL, *taskU;    // [n_blocks] sweep tasks in level order (pf_reduce.cu sweep())
   // Sparse right-hand sides (Gilbert–Peierls reach): for unit directions the L sweep of
   // canonical column tile t (columns [tC, tC+C)) only visits the blocks on the

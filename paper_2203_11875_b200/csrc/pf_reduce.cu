@@ -39,10 +39,11 @@ constexpr int kBusPerCta = PF_MU_BUS_PER_CTA;  // generator buses per k_mu CTA
 #endif
 constexpr int kHvpMinBlocks = PF_HVP_MIN_BLOCKS;  // CTAs per SM k_hvp is register-capped for
 #ifndef PF_HVP_TILES
-#define PF_HVP_TILES 2
+#define PF_HVP_TILES 1
 #endif
 constexpr int kHvpTiles = PF_HVP_TILES;  // direction tiles per k_hvp CTA
 constexpr int kHvpBusPerCta = PF_BUS_PER_CTA; // buses per k_hvp CTA (a compact run of the postorder)
+static_assert(kHvpBusPerCta <= kThreads, "k_hvp: a team's buses must fit its lanes");
 #ifndef PF_DOT_W
 #define PF_DOT_W 4
 #endif
@@ -602,15 +603,39 @@ __global__ void __launch_bounds__(kThreads, kHvpMinBlocks) k_hvp(DevNet n, Work 
   const double* lb = w.lblk + (size_t)s * n.n_l * LB_N;
   const double* bs = w.bs + (size_t)s * BS_N * n_b;
   const int k1 = min(n_b, (int)(blockIdx.x + 1) * kHvpBusPerCta);
-  // buses in elimination order: a chunk's own θ/v rows are contiguous slab rows
-  for (int kb = blockIdx.x * kHvpBusPerCta + team; kb < k1; kb += nteam) {
-    const int i = __ldg(n.hvp_bus + kb);
-    const int pt = __ldg(n.bus_pth + i), pv = __ldg(n.bus_pv + i), uv = __ldg(n.u_v + i);
+  // buses in elimination order: a chunk's own θ/v rows are contiguous slab rows.
+  // Lane j holds the metadata of the team's j-th bus (one load for all of them),
+  // and the next bus's incidence records are fetched lane-parallel while this
+  // bus runs, so a line costs one round trip (its slab rows and line block).
+  const unsigned mask = team_mask<W>();
+  const int kb0 = blockIdx.x * kHvpBusPerCta + team;
+  const int nb = k1 > kb0 ? (k1 - kb0 + nteam - 1) / nteam : 0;  // ≤ W (kHvpBusPerCta ≤ W·nteam)
+  int4 mym = make_int4(0, 0, 0, 0);
+  int2 mye = make_int2(0, 0);
+  if (lane < nb) { mym = __ldg(n.hvp_meta + kb0 + lane * nteam); mye = __ldg(n.hvp_inc + kb0 + lane * nteam); }
+  auto shfl4 = [&](int4 v, int src) {
+    return make_int4(__shfl_sync(mask, v.x, src, W), __shfl_sync(mask, v.y, src, W), __shfl_sync(mask, v.z, src, W),
+                     __shfl_sync(mask, v.w, src, W));
+  };
+  int4 recn = make_int4(0, 0, 0, 0);
+  if (nb > 0) {
+    const int e0 = __shfl_sync(mask, mye.x, 0, W), dg = __shfl_sync(mask, mye.y, 0, W);
+    if (lane < dg) recn = __ldg(n.inc_rec + e0 + lane);
+  }
+  for (int jb = 0; jb < nb; ++jb) {
+    const int4 m = shfl4(mym, jb);
+    const int i = m.x, pt = m.y, pvc = m.z, gi_own = m.w;
+    const int e0 = __shfl_sync(mask, mye.x, jb, W), dg = __shfl_sync(mask, mye.y, jb, W);
+    const int pv = pvc >= 0 ? pvc : -1, uv = pvc >= 0 ? -1 : -1 - pvc;
+    const int4 recc = recn;
+    if (jb + 1 < nb) {  // next bus's records
+      const int e0n = __shfl_sync(mask, mye.x, jb + 1, W), dgn = __shfl_sync(mask, mye.y, jb + 1, W);
+      recn = lane < dgn ? __ldg(n.inc_rec + e0n + lane) : make_int4(0, 0, 0, 0);
+    }
     double dvi[D], dthi[D], mPi[D], mQi[D], hv[D], hth[D];
-    const int gi_own = __ldg(n.bus_gen + i);
 #pragma unroll
     for (int u = 0; u < NT; ++u) {
-      dirs_at<C>(d[u], pt, pv >= 0 ? pv : -1 - uv, dthi + u * CPL, dvi + u * CPL);
+      dirs_at<C>(d[u], pt, pvc, dthi + u * CPL, dvi + u * CPL);
       if (gi_own >= 0) {
         row_ld<C>(MU[u], 2 * gi_own, lane, mPi + u * CPL);
         row_ld<C>(MU[u], 2 * gi_own + 1, lane, mQi + u * CPL);
@@ -621,8 +646,8 @@ __global__ void __launch_bounds__(kThreads, kHvpMinBlocks) k_hvp(DevNet n, Work 
       if (gi_own < 0) { mPi[k] = 0.0; mQi[k] = 0.0; }
       hv[k] = 0.0; hth[k] = 0.0;
     }
-    for (int e = __ldg(n.inc_ptr + i); e < __ldg(n.inc_ptr + i + 1); ++e) {
-      const int4 rec = __ldg(n.inc_rec + e);
+    for (int e = 0; e < dg; ++e) {
+      const int4 rec = e < W ? shfl4(recc, e) : __ldg(n.inc_rec + e0 + e);
       const bool from = rec.w & 1;
       const int go = (rec.w >> 1) - 1;
       double dvo[D], dtho[D], h[6];
