@@ -42,7 +42,9 @@ int main(int argc, char** argv) {
   for (int r = 0; r < reps; ++r) {
     cudaMemcpy(dK, dK0, K.size() * 8, cudaMemcpyDeviceToDevice);
     cudaMemcpy(drhs, b.data(), b.size() * 8, cudaMemcpyHostToDevice);
+#ifdef PF_CHOL_TRACE
     if (r == reps - 1 && trace) cudaMemcpyToSymbol(pf::g_chol_trace, &dtr, sizeof(dtr));
+#endif
     cudaEventRecord(e0);
     pf::launch_chol(net, w, S, dK, nullptr, 0.0, drhs, 1, dinfo, dws, 0);
     cudaEventRecord(e1);
