@@ -222,6 +222,8 @@ __device__ __forceinline__ void dot_long(const double2* __restrict__ pk, const d
 struct FromSlab {};
 // U sweep after a reach-restricted L sweep: rows outside the reach start at 0
 struct FromSlabReach { const unsigned* bm; };
+// L sweep after the RHS scatter: rows marked in bm start from the slab, the rest at 0
+struct FromSlabMarked { const unsigned* bm; };
 template <int C>
 struct FromRhs {
   const int* gur_ptr; const int* gur_col; const int* gur_src; const double* gu;
@@ -277,7 +279,7 @@ __device__ __forceinline__ void run_seq(const int4* __restrict__ tasks, int firs
     if constexpr (std::is_same<Init, FromSlab>::value) {
 #pragma unroll
       for (int j = 0; j < CPL; ++j) { a0[j] = x0p[j]; a1[j] = k.two ? x1p[j] : 0.0; }
-    } else if constexpr (std::is_same<Init, FromSlabReach>::value) {
+    } else if constexpr (std::is_same<Init, FromSlabReach>::value || std::is_same<Init, FromSlabMarked>::value) {
       const bool in0 = (init.bm[k.r0 >> 5] >> (k.r0 & 31)) & 1u;
       const bool in1 = k.two && ((init.bm[(k.r0 + 1) >> 5] >> ((k.r0 + 1) & 31)) & 1u);
 #pragma unroll
@@ -493,10 +495,26 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
   if (rt >= 0) {
     // sparse RHS: only the tile's reach (tree paths of its columns' G_u rows) is nonzero
     const unsigned* bmg = n.rowbm + (size_t)(rt + tile) * n.bmw;
-    for (int i = threadIdx.x; i < n.bmw; i += blockDim.x) bm_sm[i] = __ldg(bmg + i);
+    unsigned* rhs_sm = bm_sm + n.bmw;  // rows of B with a nonzero in this tile
+    for (int i = threadIdx.x; i < n.bmw; i += blockDim.x) { bm_sm[i] = __ldg(bmg + i); rhs_sm[i] = 0u; }
+    __syncthreads();
+    // B(r, j) = −G_u(r, base + j) scattered from the tile's G_u columns (off the sweep's
+    // latency chain): mark and zero the rows, then drop the entries in
+    const int base = col0 + tile * C;
+    const int e0 = __ldg(n.guc_ptr + base), e1 = __ldg(n.guc_ptr + base + nvalid);
+    for (int e = e0 + team; e < e1; e += nteam) {
+      const int r = __ldg(n.guc_row + e);
+      if (lane == 0) atomicOr(rhs_sm + (r >> 5), 1u << (r & 31));
+      double z[Geo<C>::CPL] = {};
+      row_st<C>(X, r, lane, z);
+    }
+    __syncthreads();
+    for (int c = team; c < nvalid; c += nteam)
+      for (int e = __ldg(n.guc_ptr + base + c) + lane; e < __ldg(n.guc_ptr + base + c + 1); e += W)
+        X[(size_t)__ldg(n.guc_row + e) * C + c] = -gu[__ldg(n.guc_src + e)];
     __syncthreads();
     sweep<C, true>(n.taskLr, n.levLr_ptr + (size_t)(rt + tile) * (n.nlevL + 1), n.nlevL, pk, X, false, lane, team,
-                   nteam, ent, rhs, bm_sm);                                                       // L^{-1} B
+                   nteam, ent, FromSlabMarked{rhs_sm}, bm_sm);                                   // L^{-1} B
     sweep<C, false>(n.u_top, n.u_top_ptr, n.nlevU, pk, X, true, lane, team, nteam, ent, FromSlabReach{bm_sm}, nullptr,
                     n.u_bot, n.u_bot_ptr);                                                 // U^{-1}
   } else {
@@ -823,7 +841,7 @@ void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int
               st>>>(n, w, n_scen);
   if (ev) cudaEventRecord(ev[0], st);
   const int rt = (V == nullptr && col0 % C == 0) ? col0 / C : -1;  // canonical tile of the call's first tile
-  k_fwd<C><<<dim3(ntile, n_scen), kThreads, rt >= 0 ? n.bmw * sizeof(unsigned) : 0, st>>>(n, w, V, col0, N, rt);
+  k_fwd<C><<<dim3(ntile, n_scen), kThreads, rt >= 0 ? 2 * n.bmw * sizeof(unsigned) : 0, st>>>(n, w, V, col0, N, rt);
   if (ev) cudaEventRecord(ev[1], st);
   k_mu<C, kHvpTiles><<<dim3((n.n_gb + kBusPerCta - 1) / kBusPerCta, (ntile + kHvpTiles - 1) / kHvpTiles, n_scen), kThreads,
                        0, st>>>(n, w, V, col0, N);
