@@ -39,9 +39,13 @@ constexpr int kBusPerCta = PF_MU_BUS_PER_CTA;  // generator buses per k_mu CTA
 #endif
 constexpr int kHvpMinBlocks = PF_HVP_MIN_BLOCKS;  // CTAs per SM k_hvp is register-capped for
 #ifndef PF_HVP_TILES
-#define PF_HVP_TILES 1
+#define PF_HVP_TILES 2
 #endif
 constexpr int kHvpTiles = PF_HVP_TILES;  // direction tiles per k_hvp CTA
+#ifndef PF_MU_TILES
+#define PF_MU_TILES 1
+#endif
+constexpr int kMuTiles = PF_MU_TILES;    // … per k_mu CTA
 constexpr int kHvpBusPerCta = PF_BUS_PER_CTA; // buses per k_hvp CTA (a compact run of the postorder)
 static_assert(kHvpBusPerCta <= kThreads, "k_hvp: a team's buses must fit its lanes");
 #ifndef PF_DOT_W
@@ -673,36 +677,42 @@ __global__ void __launch_bounds__(kThreads, kHvpMinBlocks) k_hvp(DevNet n, Work 
       for (int u = 0; u < NT; ++u) dirs_at<C>(d[u], rec.y, rec.z, dtho + u * CPL, dvo + u * CPL);
       const double* p = lb + (size_t)rec.x * LB_N;
       load_h(p, h);
-      const bool coupled = gi_own >= 0 || go >= 0;  // Jᵀ μ_A: only lines touching an r bus
-      double J[12], mPo[D], mQo[D];
-      if (coupled) {
-        load_j(p, J);
-#pragma unroll
-        for (int u = 0; u < NT; ++u) {
-          if (go >= 0) {
-            row_ld<C>(MU[u], 2 * go, lane, mPo + u * CPL);
-            row_ld<C>(MU[u], 2 * go + 1, lane, mQo + u * CPL);
-          } else {
-#pragma unroll
-            for (int j = 0; j < CPL; ++j) { mPo[u * CPL + j] = 0.0; mQo[u * CPL + j] = 0.0; }
-          }
-        }
-      }
 #pragma unroll
       for (int k = 0; k < D; ++k) {
         const double dvf = from ? dvi[k] : dvo[k], dvt = from ? dvo[k] : dvi[k];
         const double dD = from ? dthi[k] - dtho[k] : dtho[k] - dthi[k];
-        double hvo = from ? h[0] * dvf + h[1] * dvt + h[2] * dD : h[1] * dvf + h[3] * dvt + h[4] * dD;
-        double hD = h[2] * dvf + h[4] * dvt + h[5] * dD;
-        if (coupled) {
-          const double mpf = from ? mPi[k] : mPo[k], mqf = from ? mQi[k] : mQo[k];
-          const double mpt = from ? mPo[k] : mPi[k], mqt = from ? mQo[k] : mQi[k];
-          hvo += from ? J[0] * mpf + J[3] * mqf + J[6] * mpt + J[9] * mqt
-                      : J[1] * mpf + J[4] * mqf + J[7] * mpt + J[10] * mqt;
-          hD += J[2] * mpf + J[5] * mqf + J[8] * mpt + J[11] * mqt;
-        }
-        hv[k] += hvo;
+        hv[k] += from ? h[0] * dvf + h[1] * dvt + h[2] * dD : h[1] * dvf + h[3] * dvt + h[4] * dD;
+        const double hD = h[2] * dvf + h[4] * dvt + h[5] * dD;
         hth[k] += from ? hD : -hD;
+      }
+    }
+    // Jᵀ μ_A, only on lines touching an r bus — a second pass, so its line block and
+    // far-end μ do not hold registers alongside the first pass's slab rows
+    for (int e = 0; e < dg; ++e) {
+      const int4 rec = e < W ? shfl4(recc, e) : __ldg(n.inc_rec + e0 + e);
+      const bool from = rec.w & 1;
+      const int go = (rec.w >> 1) - 1;
+      if (gi_own < 0 && go < 0) continue;
+      double J[12], mPo[D], mQo[D];
+      load_j(lb + (size_t)rec.x * LB_N, J);
+#pragma unroll
+      for (int u = 0; u < NT; ++u) {
+        if (go >= 0) {
+          row_ld<C>(MU[u], 2 * go, lane, mPo + u * CPL);
+          row_ld<C>(MU[u], 2 * go + 1, lane, mQo + u * CPL);
+        } else {
+#pragma unroll
+          for (int j = 0; j < CPL; ++j) { mPo[u * CPL + j] = 0.0; mQo[u * CPL + j] = 0.0; }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const double mpf = from ? mPi[k] : mPo[k], mqf = from ? mQi[k] : mQo[k];
+        const double mpt = from ? mPo[k] : mPi[k], mqt = from ? mQo[k] : mQi[k];
+        hv[k] += from ? J[0] * mpf + J[3] * mqf + J[6] * mpt + J[9] * mqt
+                      : J[1] * mpf + J[4] * mqf + J[7] * mpt + J[10] * mqt;
+        const double jD = J[2] * mpf + J[5] * mqf + J[8] * mpt + J[11] * mqt;
+        hth[k] += from ? jD : -jD;
       }
     }
     const double vi = bs[BS_V * n_b + i], gsh = __ldg(n.gsh + i), bsh = __ldg(n.bsh + i);
@@ -843,7 +853,7 @@ void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int
   const int rt = (V == nullptr && col0 % C == 0) ? col0 / C : -1;  // canonical tile of the call's first tile
   k_fwd<C><<<dim3(ntile, n_scen), kThreads, rt >= 0 ? 2 * n.bmw * sizeof(unsigned) : 0, st>>>(n, w, V, col0, N, rt);
   if (ev) cudaEventRecord(ev[1], st);
-  k_mu<C, kHvpTiles><<<dim3((n.n_gb + kBusPerCta - 1) / kBusPerCta, (ntile + kHvpTiles - 1) / kHvpTiles, n_scen), kThreads,
+  k_mu<C, kMuTiles><<<dim3((n.n_gb + kBusPerCta - 1) / kBusPerCta, (ntile + kMuTiles - 1) / kMuTiles, n_scen), kThreads,
                        0, st>>>(n, w, V, col0, N);
   if (ev) cudaEventRecord(ev[2], st);
   k_hvp<C, kHvpTiles><<<dim3((n.n_b + kHvpBusPerCta - 1) / kHvpBusPerCta, (ntile + kHvpTiles - 1) / kHvpTiles, n_scen),
