@@ -217,13 +217,18 @@ def main():
     tmp = Network(net, max_batch=1, max_scen=1, device=-1)
     n_u, n_x, m = tmp.dims["n_u"], tmp.dims["n_x"], tmp.dims["m"]
     tmp.close()
-    col0, ncols, cpad = column_partition(n_u, world, rank) if directions else (0, n_u, n_u)
+    # direction mode: tile-aligned column slabs, so every rank keeps the sparse-RHS reach lists
+    tmp = Network(net, max_batch=-(-n_u // world), max_scen=S, device=-1)
+    tile = tmp.dims["tile_cols"]
+    tmp.close()
+    col0, ncols, cpad = column_partition(n_u, world, rank, tile) if directions else (0, n_u, n_u)
     # P independent pipelines (one handle + one stream each) over contiguous scenario
     # groups: the latency-bound phases of one group (LU refactor, Cholesky chain)
     # overlap the bandwidth-bound reduction of the other.
     P = args.pipelines if (not directions and S % max(args.pipelines, 1) == 0) else 1
     Sg = S // P
-    hs = [Network(net, max_batch=max(cpad, 1), max_scen=Sg, device=local) for _ in range(P)]
+    hs = [Network(net, max_batch=max(cpad, 1), max_scen=Sg, device=local, tile_cols=tile if directions else 0)
+          for _ in range(P)]
     h = hs[0]
     h.profile(True)
     d = h.dims

@@ -118,6 +118,25 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g,
                            int32_t max_batch, int32_t max_scen, int32_t device,
                            pf_net **out);
 
+/*
+ * pf_build_network_ex — pf_build_network with an explicit direction-tile
+ * width of the reduction kernels: tile_cols ∈ {8, 16, 32, 64} directions per
+ * CTA tile, or 0 = automatic (what pf_build_network does: the widest tile that
+ * still gives ≥ 2 CTAs per SM for max_batch × max_scen directions).  Results
+ * are bit-identical for every tile width.  PF_ERR_ARG for any
+ * other value.
+ */
+pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g,
+                              const int32_t *line_from, const int32_t *line_to,
+                              const double *Y_ff, const double *Y_ft,
+                              const double *Y_tf, const double *Y_tt,
+                              const double *Y_sh, const int32_t *gen_bus,
+                              int32_t ref_bus, const double *p_d,
+                              const double *q_d, const double *F_max,
+                              const double *c_quad, const double *c_lin,
+                              int32_t max_batch, int32_t max_scen, int32_t device,
+                              int32_t tile_cols, pf_net **out);
+
 void pf_destroy(pf_net *net);
 pf_status pf_query(const pf_net *net, pf_dims *out /* [host] */);
 /* Copy one integer structure array (sizes in pf_structure) to [host] out. */
@@ -167,9 +186,13 @@ pf_status pf_jacobian(pf_net *net, int32_t n_scen, const double *v,
  *   K̂ V = H_u − G_uᵀ Ψ,
  * K = ∇²ℒ + AᵀΣ_sA + blkdiag(0, Σ_x) (R14), ℒ = f + λᵀg
  * + yᵀ[r; h], f with the implicit p_ref (R8).  K is never formed: K·[V;Z]
- * is evaluated matrix-free through ψ.  Uses the LU of the last pf_jacobian
- * (same v, theta).
- *   v, theta: [n_scen][n_b];  p_d: [n_scen][n_b] or NULL = base loads
+ * is evaluated matrix-free through ψ.  Uses the point and the LU factors of
+ * the last successful pf_jacobian (factorize once per
+ * iteration, reuse for every right-hand side).
+ *   v, theta: the SAME device arrays passed to that pf_jacobian (contents
+ *   unchanged since), or NULL = that point; other pointers → PF_ERR_STATE,
+ *   as is a call with more scenarios than that pf_jacobian factorized;
+ *   p_d: [n_scen][n_b] or NULL = base loads
  *   (only p_d[ref] enters, through p_ref);
  *   lambda: [n_scen][n_x];  y: [n_scen][m];
  *   sigma_s: [n_scen][m] or NULL (= 0);  sigma_x: [n_scen][n_x] or NULL;
@@ -203,6 +226,79 @@ pf_status pf_condensed_kkt_solve(pf_net *net, int32_t n_scen, double *K,
                                  const double *sigma_u, double delta_w,
                                  double *rhs, int32_t nrhs, int32_t *info,
                                  void *stream);
+
+/*
+ * ---- NEXT-1: condensed right-hand side and step recovery ----
+ * One LinRed iteration's remaining linear algebra (Algorithm 1)
+ * around pf_condensed_kkt_solve, at the point of the last pf_jacobian (v,
+ * theta as in pf_reduced_hessian_batch) with the multipliers and barrier
+ * diagonals of the reduction (lambda, y, sigma_s, sigma_x, p_d as there).
+ *   r: [n_scen][n_u + n_x + m + n_x + m] device — the right-hand side
+ *   (r₁, r₂, r₃, r₄, r₅) of eq. kktmatrix:normal, blocks
+ *   ordered like the unknowns (p_u, p_x, p_s, p_λ, p_y); K_aug p = −r.
+ *
+ * pf_condensed_rhs — Theorem 1's r̂₁, r̂₂, r̂₃ and Theorem 2's
+ * right-hand side with reading R10 (sign of the r̂₂ terms):
+ *   b = −(r̂₁ + Â_uᵀ Σ_s r̂₃ + Â_uᵀ r̂₂),   K_cond p_u = b;
+ * computed matrix-free as ONE direction of the HVP pipeline per scenario
+ * (DESIGN.md §"Step recovery"), never forming Â_u.
+ *   out b: [n_scen][n_u] (pass it as pf_condensed_kkt_solve's rhs).
+ *
+ * pf_recover_step — Algorithm 1's dual, slack, state and adjoint steps:
+ *   p_y = Σ_s(Â_u p_u + r̂₃ + Σ_s⁻¹ r̂₂),  p_s = Σ_s⁻¹(p_y − r̂₂),
+ *   p_x = −G_x⁻¹(r₄ + G_u p_u),
+ *   p_λ = −G_x⁻ᵀ(r₂ + A_xᵀ p_y + W_xu p_u + (W_xx + Σ_x) p_x).
+ *   p_u: [n_scen][n_u] (the condensed solve's solution);
+ *   out p: [n_scen][n_u + n_x + m + n_x + m] = (p_u, p_x, p_s, p_λ, p_y).
+ * sigma_s must be non-NULL for the recovery when m > 0 (Theorem 2 needs Σ_s
+ * nonsingular); NULL is read as 0 elsewhere.
+ */
+pf_status pf_condensed_rhs(pf_net *net, int32_t n_scen, const double *v,
+                           const double *theta, const double *p_d,
+                           const double *lambda, const double *y,
+                           const double *sigma_s, const double *sigma_x,
+                           const double *r, double *b, void *stream);
+pf_status pf_recover_step(pf_net *net, int32_t n_scen, const double *v,
+                          const double *theta, const double *p_d,
+                          const double *lambda, const double *y,
+                          const double *sigma_s, const double *sigma_x,
+                          const double *r, const double *p_u, double *p,
+                          void *stream);
+
+/*
+ * ---- NEXT-2: power flow, first-order adjoint, reduced gradient ----
+ * pf_power_flow — the RedLin projection step (Algorithm 2):
+ * Newton–Raphson on g(x, u) = 0 for every scenario at once, x ← x − G_x⁻¹g
+ * with the A4/A5 Jacobian and LU and the k_fwd sweeps (N = 1), until
+ * ‖g‖∞ ≤ tol (the paper's 1e-10) or max_iter steps.
+ *   v, theta: [n_scen][n_b] device, IN the start point (u = v at generator
+ *   buses and p_g fixed), OUT the solution (state entries updated in place);
+ *   p_g, q_g, p_d, q_d as pf_eval_constraints (q_g may be NULL: it enters no
+ *   g row); out [host] iters, resid (final ‖g‖∞), info: 0 converged, −1 no
+ *   convergence in max_iter (or NaN), k+1 singular Jacobian (R18 pivot k).
+ *   Each may be NULL.  Synchronizes the stream once per iteration (host
+ *   convergence test; not graph-capturable).  Ends with a factorization at
+ *   the final point: pf_reduced_hessian_batch / pf_reduced_gradient /
+ *   pf_condensed_rhs may follow with these v, theta arrays.
+ *
+ * pf_reduced_gradient — the adjoint step and the reduced gradient
+ * (Algorithm 2; Theorem "Reduced derivatives"):
+ *   ∇_z ℓ = ∇_z(f + yᵀ[r; h]) (f with the implicit p_ref, R8),
+ *   λ = −G_x⁻ᵀ ∇_x ℓ,   ∇_u ℓ_r = ∇_u ℓ − G_uᵀ G_x⁻ᵀ ∇_x ℓ.
+ * At the point of the last pf_jacobian / pf_power_flow (v, theta as in
+ * pf_reduced_hessian_batch).
+ *   p_g: [n_scen][n_g]; p_d: [n_scen][n_b] or NULL; y: [n_scen][m];
+ *   out lambda: [n_scen][n_x] or NULL; out grad: [n_scen][n_u].
+ */
+pf_status pf_power_flow(pf_net *net, int32_t n_scen, double *v, double *theta,
+                        const double *p_g, const double *q_g,
+                        const double *p_d, const double *q_d, double tol,
+                        int32_t max_iter, int32_t *iters, double *resid,
+                        int32_t *info, void *stream);
+pf_status pf_reduced_gradient(pf_net *net, int32_t n_scen, const double *v,
+                              const double *theta, const double *p_g,
+                              const double *p_d, const double *y,
+                              double *lambda, double *grad, void *stream);
 
 /* Number of kernels this handle has launched so far (bench evidence). */
 int64_t pf_launch_count(const pf_net *net);

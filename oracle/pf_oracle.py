@@ -119,16 +119,18 @@ def ybus(net):
     return Cf.T @ Yf + Ct.T @ Yt + np.diag(net["Y_sh"])
 
 
-def ybus_entries(net):
+def ybus_entries(net, dense_max=3000):
     """Nonzero entries (i, j, Y_ij) of Y_bus in row-major order, topological
     pattern (an entry exists iff i = j or a line joins i and j; R19), values
-    summed over parallel lines exactly as the dense product above."""
+    summed over parallel lines exactly as the dense product above.  Above
+    dense_max buses the same product runs in sparse storage (pinned against
+    the dense branch by tests/test_oracle_pins.py)."""
     n_b = int(net["n_b"])
     f = np.asarray(net["line_from"], dtype=np.int64)
     t = np.asarray(net["line_to"], dtype=np.int64)
     key = np.unique(np.concatenate([np.arange(n_b) * n_b + np.arange(n_b), f * n_b + t, t * n_b + f]))
     ii, jj = key // n_b, key % n_b
-    if n_b <= 3000:
+    if n_b <= dense_max:
         Y = ybus(net)
         return ii, jj, Y[ii, jj]
     # same formula with sparse storage (the dense product does not fit in memory at 9k buses)
@@ -453,6 +455,16 @@ def kkt_K(net, part, point, lam, y, sigma_s=None, sigma_x=None):
     return K.tocsr()
 
 
+def kkt_K_from(W, A, sigma_s, sigma_x, n_u):
+    """K = W + AᵀΣ_sA + blkdiag(0_u, Σ_x) from given W and A (same as kkt_K)."""
+    K = sp.csr_matrix(W)
+    if sigma_s is not None:
+        K = K + sp.csr_matrix(A).T @ sp.diags(sigma_s) @ sp.csr_matrix(A)
+    if sigma_x is not None:
+        K = K + sp.diags(np.concatenate([np.zeros(n_u), sigma_x]))
+    return K.tocsr()
+
+
 # ----------------------------------------------------------------------------
 # O7 / O7' reductions (PAPER.md eq. algo:reduction L1156–1172; L1180–1235)
 # ----------------------------------------------------------------------------
@@ -615,6 +627,18 @@ def adjoint_multipliers(net, part, point, y):
     return np.linalg.solve(Gx.toarray().T, -grad[n_u:])
 
 
+def reduced_gradient(net, part, point, y):
+    """Algorithm 2's adjoint step and the reduced gradient (Theorem 'Reduced
+    derivatives', P:L976): with ∇ℓ = ∇_z(f + y_rᵀr + y_hᵀh),
+    λ = −G_x⁻ᵀ∇_xℓ and ∇_uℓ_r = ∇_uℓ − G_uᵀG_x⁻ᵀ∇_xℓ = ∇_uℓ + G_uᵀλ.
+    Returns (λ, ∇_uℓ_r)."""
+    Gx, Gu, A = jacobians(net, part, point)
+    n_u = part["n_u"]
+    grad = objective_gradient(net, part, point) + A.T @ y
+    lam = -np.linalg.solve(Gx.toarray().T, grad[n_u:])
+    return lam, grad[:n_u] + Gu.T @ lam
+
+
 def reduced_value(net, part, point, y, u):
     """φ(u) = f(x(u),u) + yᵀ[r; h](x(u),u), x(u) by Newton (the reduced
     Lagrangian's smooth part, Theorem 'Reduced derivatives' L967–990)."""
@@ -658,6 +682,63 @@ def kaug(W, Gx, Gu, A, sigma_u, sigma_x, sigma_s):
     K[iy:, iu:ix] = Au
     K[iy:, ix:is_] = Ax
     return K
+
+
+# ----------------------------------------------------------------------------
+# NEXT-1: condensed right-hand side and step recovery (Theorem 1 P:L671–719,
+# Theorem 2, Algorithm 1), dense, in the paper's order
+# and notation, with reading R10 (the signs of the r̂₂ terms).
+# W is the Lagrangian Hessian ∇²ℒ (lagrangian_hessian: no Σ, no AᵀΣ_sA).
+# The right-hand side r = (r₁, r₂, r₃, r₄, r₅) of eq. kktmatrix:normal is
+# ordered like kaug's blocks (p_u, p_x, p_s, p_λ, p_y): K_aug p = −r.
+# ----------------------------------------------------------------------------
+def split_kkt(vec, n_u, n_x, m):
+    o = np.cumsum([0, n_u, n_x, m, n_x, m])
+    return [np.asarray(vec[o[k]:o[k + 1]], dtype=np.float64) for k in range(5)]
+
+
+def condensed_rhs(W, Gx, Gu, A, sigma_x, sigma_s, r):
+    """Theorem 1: r̂₁ = r₁ − G_uᵀG_x⁻ᵀr₂ − (W_ux − G_uᵀG_x⁻ᵀ(W_xx+Σ_x))G_x⁻¹r₄,
+    r̂₂ = r₃, r̂₃ = r₅ − A_xG_x⁻¹r₄, Â_u = A_u − A_xG_x⁻¹G_u; Theorem 2 (R10):
+    K_cond p_u = −(r̂₁ + Â_uᵀΣ_s r̂₃ + Â_uᵀ r̂₂).  Returns (b, (r̂₁, r̂₂, r̂₃), Â_u)."""
+    Gx = np.asarray(sp.csr_matrix(Gx).toarray())
+    Gu = np.asarray(sp.csr_matrix(Gu).toarray())
+    A = np.asarray(sp.csr_matrix(A).toarray())
+    W = np.asarray(sp.csr_matrix(W).toarray())
+    n_x, n_u = Gu.shape
+    m = A.shape[0]
+    r1, r2, r3, r4, r5 = split_kkt(r, n_u, n_x, m)
+    Wux, Wxx = W[:n_u, n_u:], W[n_u:, n_u:] + np.diag(sigma_x)
+    Au, Ax = A[:, :n_u], A[:, n_u:]
+    Gx_inv_r4 = np.linalg.solve(Gx, r4)
+    rh1 = r1 - Gu.T @ np.linalg.solve(Gx.T, r2) - (Wux - Gu.T @ np.linalg.solve(Gx.T, Wxx)) @ Gx_inv_r4
+    rh2 = r3
+    rh3 = r5 - Ax @ Gx_inv_r4
+    Ahat = Au - Ax @ np.linalg.solve(Gx, Gu)
+    b = -(rh1 + Ahat.T @ (sigma_s * rh3) + Ahat.T @ rh2)
+    return b, (rh1, rh2, rh3), Ahat
+
+
+def recover_step(W, Gx, Gu, A, sigma_x, sigma_s, r, p_u):
+    """Algorithm 1's dual, slack, state and adjoint steps (Theorem 1 recovery,
+    Theorem 2 with R10): p_y = Σ_s(Â_u p_u + r̂₃ + Σ_s⁻¹r̂₂), p_s = Σ_s⁻¹(p_y − r̂₂),
+    p_x = −G_x⁻¹(r₄ + G_u p_u), p_λ = −G_x⁻ᵀ(r₂ + A_xᵀp_y + W_xu p_u + (W_xx+Σ_x)p_x).
+    Returns the step ordered (p_u, p_x, p_s, p_λ, p_y)."""
+    _, (rh1, rh2, rh3), Ahat = condensed_rhs(W, Gx, Gu, A, sigma_x, sigma_s, r)
+    Gx = np.asarray(sp.csr_matrix(Gx).toarray())
+    Gu = np.asarray(sp.csr_matrix(Gu).toarray())
+    A = np.asarray(sp.csr_matrix(A).toarray())
+    W = np.asarray(sp.csr_matrix(W).toarray())
+    n_x, n_u = Gu.shape
+    m = A.shape[0]
+    r1, r2, r3, r4, r5 = split_kkt(r, n_u, n_x, m)
+    Wxu, Wxx = W[n_u:, :n_u], W[n_u:, n_u:] + np.diag(sigma_x)
+    Ax = A[:, n_u:]
+    p_y = sigma_s * (Ahat @ p_u + rh3 + rh2 / sigma_s)
+    p_s = (p_y - rh2) / sigma_s
+    p_x = -np.linalg.solve(Gx, r4 + Gu @ p_u)
+    p_l = -np.linalg.solve(Gx.T, r2 + Ax.T @ p_y + Wxu @ p_u + Wxx @ p_x)
+    return np.concatenate([p_u, p_x, p_s, p_l, p_y])
 
 
 def gauss_jordan_inverse(M):
@@ -886,6 +967,24 @@ def a_pattern(net, part):
     return ptr, np.array([c for r in rows for c in r], dtype=np.int32)
 
 
+def static_lu(Gx, perm, rel=1e-12):
+    """R18 numeric refactorization rule, written out: dense LU of P G_x Pᵀ
+    (P from the R18 ordering) with NO pivoting, right-looking.  Pivot k fails
+    iff u_kk is non-finite, zero, or |u_kk| < rel · max_j |(P G_x Pᵀ)_kj|; the
+    first failure stops the factorization.  Returns (info, LU): info = 0 or
+    k+1; LU holds L (unit, strict lower) and U (upper) of the rows done."""
+    A = np.asarray(sp.csr_matrix(Gx).toarray(), dtype=np.float64)[np.ix_(perm, perm)]
+    n = A.shape[0]
+    rowmax = np.abs(A).max(axis=1) if n else np.zeros(0)
+    for k in range(n):
+        d = A[k, k]
+        if not np.isfinite(d) or d == 0.0 or abs(d) < rel * rowmax[k]:
+            return k + 1, A
+        A[k + 1:, k] /= d
+        A[k + 1:, k + 1:] -= np.outer(A[k + 1:, k], A[k, k + 1:])
+    return 0, A
+
+
 def filled_csr(F):
     """CSR (ptr, idx) of a boolean filled pattern."""
     ptr = np.zeros(F.shape[0] + 1, dtype=np.int32)
@@ -897,14 +996,50 @@ def filled_csr(F):
     return ptr, np.concatenate(idx).astype(np.int32) if idx else np.zeros(0, np.int32)
 
 
-def reduce_columns(K, Gx, Gu, cols):
-    """O7' for selected unit directions (sampled full-size parity): the three
-    steps of PAPER.md L1203–1222 with R11 for V = I[:, cols], using a sparse
-    LU (SuperLU) of G_x as the solve primitive."""
+class SparseLU:
+    """A sparse LU of G_x used as a solve primitive (SuperLU), in one of three
+    independent variants (for the measured noise floor of R20):
+      "colamd": SuperLU defaults — COLAMD column ordering, partial pivoting;
+      "mmd":    minimum degree on AᵀA+A, static diagonal pivots;
+      "static": the R18 rule itself — P G_x Pᵀ with the given bus-level
+                ordering perm, natural order inside SuperLU, diagonal pivots
+                (no numerical pivoting), i.e. the algorithm the GPU runs."""
+
+    def __init__(self, Gx, kind="colamd", perm=None):
+        A = sp.csc_matrix(Gx)
+        self.perm = None
+        if kind == "colamd":
+            self.lu = spla.splu(A)
+        elif kind == "mmd":
+            self.lu = spla.splu(A, permc_spec="MMD_AT_PLUS_A", diag_pivot_thresh=0.0,
+                                options=dict(SymmetricMode=True))
+        elif kind == "static":
+            self.perm = np.asarray(perm)
+            Ap = sp.csc_matrix(A[self.perm][:, self.perm])
+            self.lu = spla.splu(Ap, permc_spec="NATURAL", diag_pivot_thresh=0.0,
+                                options=dict(SymmetricMode=True))
+            n = len(self.perm)
+            assert np.array_equal(self.lu.perm_r, np.arange(n)) and np.array_equal(self.lu.perm_c, np.arange(n))
+        else:
+            raise ValueError(kind)
+
+    def solve(self, B, trans="N"):
+        B = np.asarray(B, dtype=np.float64)
+        if self.perm is None:
+            return self.lu.solve(B, trans=trans)
+        X = np.empty_like(B)
+        X[self.perm] = self.lu.solve(B[self.perm], trans=trans)   # (P G_x Pᵀ)⁻¹ and its transpose
+        return X
+
+
+def reduce_columns(K, Gx, Gu, cols, kind="colamd", perm=None):
+    """O7' for selected unit directions (full-size parity): the three steps of
+    PAPER.md L1203–1222 with R11 for V = I[:, cols], with a sparse LU of G_x
+    (SparseLU `kind`) as the solve primitive."""
     n_u = Gu.shape[1]
     V = np.zeros((n_u, len(cols)))
     V[cols, np.arange(len(cols))] = 1.0
-    lu = spla.splu(sp.csc_matrix(Gx))
+    lu = SparseLU(Gx, kind, perm)
     Gu = sp.csr_matrix(Gu)
     Z = -lu.solve(np.asarray((Gu @ V)))
     H = sp.csr_matrix(K) @ np.vstack([V, Z])

@@ -20,7 +20,10 @@ struct pf_net {
   int device = 0;
   int C = 8;
   int max_batch = 0, max_scen = 0;
-  int lu_scen = 0;  // scenarios factorized by the last pf_jacobian (0 = none)
+  int lu_scen = 0;  // scenarios factorized by the last successful pf_jacobian (0 = none)
+  const double *lu_v = nullptr, *lu_th = nullptr;  // … and the point it was called with
+  int lu_cs = 0;     // k_lu cluster size on this handle's device (set at build)
+  int chol_grid = 0; // k_chol_dag resident CTAs on this handle's device (set at build)
   std::vector<void*> allocs;
   std::string err;
   long long launches = 0;
@@ -89,6 +92,17 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
                            const double* q_d, const double* F_max, const double* c_quad,
                            const double* c_lin, int32_t max_batch, int32_t max_scen,
                            int32_t device, pf_net** out) {
+  return pf_build_network_ex(n_b, n_l, n_g, line_from, line_to, Y_ff, Y_ft, Y_tf, Y_tt, Y_sh, gen_bus, ref_bus, p_d,
+                             q_d, F_max, c_quad, c_lin, max_batch, max_scen, device, 0, out);
+}
+
+pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t* line_from,
+                              const int32_t* line_to, const double* Y_ff, const double* Y_ft,
+                              const double* Y_tf, const double* Y_tt, const double* Y_sh,
+                              const int32_t* gen_bus, int32_t ref_bus, const double* p_d,
+                              const double* q_d, const double* F_max, const double* c_quad,
+                              const double* c_lin, int32_t max_batch, int32_t max_scen,
+                              int32_t device, int32_t tile_cols, pf_net** out) {
   g_build_err.clear();
   if (!out || !line_from || !line_to || !Y_ff || !Y_ft || !Y_tf || !Y_tt || !Y_sh || !gen_bus || !p_d ||
       !q_d || !F_max || !c_quad || !c_lin) {
@@ -97,6 +111,10 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
   }
   *out = nullptr;
   if (max_batch < 1 || max_scen < 1) { g_build_err = "max_batch and max_scen must be >= 1"; return PF_ERR_ARG; }
+  if (tile_cols != 0 && tile_cols != 8 && tile_cols != 16 && tile_cols != 32 && tile_cols != 64) {
+    g_build_err = "tile_cols must be 0 (automatic), 8, 16, 32 or 64";
+    return PF_ERR_ARG;
+  }
   pf_net* h = new pf_net();
   bool topo = false;
   std::string e = build_plan(n_b, n_l, n_g, line_from, line_to, gen_bus, ref_bus, F_max, h->P, &topo);
@@ -109,7 +127,7 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
   const Plan& P = h->P;
   h->max_batch = max_batch;
   h->max_scen = max_scen;
-  h->C = pick_tile_cols(P.n_x, max_batch * max_scen);
+  h->C = tile_cols ? tile_cols : pick_tile_cols(P.n_x, max_batch * max_scen);
   if (device < 0) {  // host analysis only: structure queries work, compute calls return PF_ERR_STATE
     *out = h;
     return PF_OK;
@@ -319,6 +337,27 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
     hvp_meta[kb] = make_int4(i, P.bus_pth[i], P.bus_pv[i] >= 0 ? P.bus_pv[i] : -1 - P.u_v[i], P.bus_gen[i]);
     hvp_inc[kb] = make_int2(P.inc_ptr[i], P.inc_ptr[i + 1] - P.inc_ptr[i]);
   }
+  // step recovery / Newton maps: G row of each permuted row, A by columns
+  std::vector<int> row_g(P.n_x);
+  for (int r = 0; r < P.n_x; ++r) row_g[r] = -1;
+  for (int i = 0; i < n_b; ++i) {
+    if (P.x_th[i] >= 0) row_g[P.iperm[P.x_th[i]]] = i;
+    if (P.x_v[i] >= 0) row_g[P.iperm[P.x_v[i]]] = n_b + i;
+  }
+  const int n_z = P.n_u + P.n_x;
+  std::vector<int> a_cptr(n_z + 1, 0), a_crow(P.a_idx.size()), a_cpos(P.a_idx.size());
+  for (int c : P.a_idx) ++a_cptr[c + 1];
+  for (int z = 0; z < n_z; ++z) a_cptr[z + 1] += a_cptr[z];
+  {
+    std::vector<int> fill(a_cptr.begin(), a_cptr.end() - 1);
+    for (int k = 0; k < P.m; ++k)
+      for (int e = P.a_ptr[k]; e < P.a_ptr[k + 1]; ++e) {
+        const int q = fill[P.a_idx[e]]++;
+        a_crow[q] = k; a_cpos[q] = e;   // ascending rows within a column (deterministic sums)
+      }
+  }
+  std::vector<int> u_gen(P.n_u, -1);
+  for (int g = 0; g < n_g; ++g) if (P.u_p[g] >= 0) u_gen[P.u_p[g]] = g;
   bool ok = up(h, lf, &d.lf) && up(h, lt, &d.lt) && up(h, coef, &d.coef) && up(h, gsh, &d.gsh) &&
             up(h, bsh, &d.bsh) && up(h, gb, &d.gen_bus) && up(h, P.bus_gen, &d.bus_gen) &&
             up(h, cq, &d.c_quad) && up(h, cl, &d.c_lin) && up(h, pd, &d.p_d0) && up(h, qd, &d.q_d0) &&
@@ -342,7 +381,10 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
             up(h, taskUa, &d.taskUa) && up(h, levUa_ptr, &d.levUa_ptr) && up(h, h->p1_task, &d.p1_task) &&
             up(h, h->p1_ptr, &d.p1_ptr) && up(h, h->u_top, &d.u_top) && up(h, h->u_top_ptr, &d.u_top_ptr) &&
             up(h, h->u_bot, &d.u_bot) && up(h, h->u_bot_ptr, &d.u_bot_ptr) && up(h, h->ua_top, &d.ua_top) &&
-            up(h, h->ua_top_ptr, &d.ua_top_ptr) && up(h, h->ua_bot, &d.ua_bot) && up(h, h->ua_bot_ptr, &d.ua_bot_ptr);
+            up(h, h->ua_top_ptr, &d.ua_top_ptr) && up(h, h->ua_bot, &d.ua_bot) && up(h, h->ua_bot_ptr, &d.ua_bot_ptr) &&
+            up(h, P.perm, &d.perm) && up(h, P.iperm, &d.iperm) && up(h, row_g, &d.row_g) &&
+            up(h, a_cptr, &d.a_cptr) && up(h, P.a_idx, &d.a_idx) && up(h, a_crow, &d.a_crow) && up(h, a_cpos, &d.a_cpos) &&
+            up(h, u_gen, &d.u_gen);
   Work& w = h->w;
   const size_t S = max_scen;
   w.max_tiles = max_scen * ((max_batch + h->C - 1) / h->C);
@@ -353,12 +395,18 @@ pf_status pf_build_network(int32_t n_b, int32_t n_l, int32_t n_g, const int32_t*
        alloc(h, T * d.n_x * C, &w.slabZ) && alloc(h, T * d.n_x * C, &w.slabW) &&
        alloc(h, T * d.n_u * C, &w.hu) && alloc(h, T * d.n_g * 2 * C, &w.mu) &&
        alloc(h, S * chol_tile_doubles(d.n_u), &w.ctile) && alloc(h, S * chol_flag_ints(d.n_u), &w.cflag) &&
-       alloc(h, 1 + 1024, &w.cticket) && alloc(h, S * chol_vec_doubles(d.n_u), &w.cy);
+       alloc(h, 1 + 1024, &w.cticket) && alloc(h, S * chol_vec_doubles(d.n_u), &w.cy) &&
+       alloc(h, S * d.nnz_a, &w.aval) && alloc(h, S * (d.n_u + d.n_x + d.m), &w.zero) &&
+       alloc(h, S * 2 * d.n_b, &w.gbuf) && alloc(h, S, &w.res) && alloc(h, S, &w.active);
+  ok = ok && cudaMemset(w.zero, 0, S * (d.n_u + d.n_x + d.m) * sizeof(double)) == cudaSuccess;
   if (!ok) {
     g_build_err = std::string("device allocation/upload failed: ") + cudaGetErrorString(cudaGetLastError());
     pf_destroy(h);
     return PF_ERR_CUDA;
   }
+  // launch geometry that depends on the device (cluster support, SM count): per handle
+  h->lu_cs = lu_cluster_size(d);
+  h->chol_grid = chol_grid_max();
   if (cudaDeviceSynchronize() != cudaSuccess) {
     g_build_err = std::string("build sync: ") + cudaGetErrorString(cudaGetLastError());
     pf_destroy(h);
@@ -440,10 +488,12 @@ pf_status pf_jacobian(pf_net* h, int32_t n_scen, const double* v, const double* 
   if (!v || !theta || n_scen < 1) { h->err = "pf_jacobian: bad argument"; return PF_ERR_ARG; }
   if (n_scen > h->max_scen) { h->err = "pf_jacobian: n_scen > max_scen"; return PF_ERR_CAPACITY; }
   if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
+  h->lu_scen = 0;  // the factors are being overwritten
   h->launches += launch_jacobian(h->dn, h->w, n_scen, v, theta, Gx_val, Gu_val, A_val, info, (cudaStream_t)stream,
-                                 h->prof ? h->ev + 5 : nullptr);
-  h->lu_scen = n_scen;
-  return cuda_check(h, "pf_jacobian");
+                                 h->lu_cs, h->prof ? h->ev + 5 : nullptr);
+  const pf_status st = cuda_check(h, "pf_jacobian");
+  if (st == PF_OK) { h->lu_scen = n_scen; h->lu_v = v; h->lu_th = theta; }
+  return st;
 }
 
 pf_status pf_reduced_hessian_batch(pf_net* h, int32_t n_scen, const double* v, const double* theta,
@@ -451,11 +501,14 @@ pf_status pf_reduced_hessian_batch(pf_net* h, int32_t n_scen, const double* v, c
                                    const double* sigma_s, const double* sigma_x, const double* V,
                                    int32_t col0, int32_t N, double* KV, void* stream) {
   if (!h) return PF_ERR_ARG;
-  (void)v; (void)theta;  // the point's state was cached by pf_jacobian (same v, theta)
   if (!lambda || !y || (!KV && N > 0) || n_scen < 1 || N < 0) { h->err = "pf_reduced_hessian_batch: bad argument"; return PF_ERR_ARG; }
   if (n_scen > h->max_scen || N > h->max_batch) { h->err = "pf_reduced_hessian_batch: capacity"; return PF_ERR_CAPACITY; }
   if (!V && (col0 < 0 || col0 + N > h->P.n_u)) { h->err = "pf_reduced_hessian_batch: columns out of range"; return PF_ERR_ARG; }
   if (h->lu_scen < n_scen) { h->err = "pf_reduced_hessian_batch: call pf_jacobian first"; return PF_ERR_STATE; }
+  if ((v && v != h->lu_v) || (theta && theta != h->lu_th)) {
+    h->err = "pf_reduced_hessian_batch: v/theta are not the arrays of the last pf_jacobian (its point and LU are used)";
+    return PF_ERR_STATE;
+  }
   if (N == 0) return PF_OK;
   if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
   cudaStream_t st = (cudaStream_t)stream;
@@ -471,8 +524,118 @@ pf_status pf_condensed_kkt_solve(pf_net* h, int32_t n_scen, double* K, const dou
   if (n_scen > h->max_scen) { h->err = "pf_condensed_kkt_solve: n_scen > max_scen"; return PF_ERR_CAPACITY; }
   if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
   h->launches += launch_chol(h->dn, h->w, n_scen, K, sigma_u, delta_w, rhs, nrhs, info, h->w.info + h->max_scen,
-                             (cudaStream_t)stream);
+                             (cudaStream_t)stream, h->chol_grid);
   return cuda_check(h, "pf_condensed_kkt_solve");
+}
+
+// ---------------------------------------------------------------- NEXT-1 / NEXT-2
+namespace {
+pf_status point_check(pf_net* h, const char* who, int n_scen, const double* v, const double* theta) {
+  if (h->lu_scen < n_scen) { h->err = std::string(who) + ": call pf_jacobian first (for these scenarios)"; return PF_ERR_STATE; }
+  if ((v && v != h->lu_v) || (theta && theta != h->lu_th)) {
+    h->err = std::string(who) + ": v/theta are not the arrays of the last pf_jacobian (its point and LU are used)";
+    return PF_ERR_STATE;
+  }
+  return PF_OK;
+}
+}  // namespace
+
+pf_status pf_condensed_rhs(pf_net* h, int32_t n_scen, const double* v, const double* theta, const double* p_d,
+                           const double* lambda, const double* y, const double* sigma_s, const double* sigma_x,
+                           const double* r, double* b, void* stream) {
+  if (!h) return PF_ERR_ARG;
+  if (!lambda || !y || !r || !b || n_scen < 1) { h->err = "pf_condensed_rhs: bad argument"; return PF_ERR_ARG; }
+  if (n_scen > h->max_scen) { h->err = "pf_condensed_rhs: n_scen > max_scen"; return PF_ERR_CAPACITY; }
+  if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
+  if (pf_status st = point_check(h, "pf_condensed_rhs", n_scen, v, theta)) return st;
+  cudaStream_t st = (cudaStream_t)stream;
+  h->launches += launch_prep(h->dn, h->w, n_scen, p_d, lambda, y, sigma_s, sigma_x, st);
+  h->launches += launch_step(0, h->dn, h->w, h->C, n_scen, r, sigma_s, nullptr, nullptr, nullptr, b, nullptr, st);
+  return cuda_check(h, "pf_condensed_rhs");
+}
+
+pf_status pf_recover_step(pf_net* h, int32_t n_scen, const double* v, const double* theta, const double* p_d,
+                          const double* lambda, const double* y, const double* sigma_s, const double* sigma_x,
+                          const double* r, const double* p_u, double* p, void* stream) {
+  if (!h) return PF_ERR_ARG;
+  if (!lambda || !y || !r || !p_u || !p || n_scen < 1) { h->err = "pf_recover_step: bad argument"; return PF_ERR_ARG; }
+  if (n_scen > h->max_scen) { h->err = "pf_recover_step: n_scen > max_scen"; return PF_ERR_CAPACITY; }
+  if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
+  if (pf_status st = point_check(h, "pf_recover_step", n_scen, v, theta)) return st;
+  cudaStream_t st = (cudaStream_t)stream;
+  h->launches += launch_prep(h->dn, h->w, n_scen, p_d, lambda, y, sigma_s, sigma_x, st);
+  h->launches += launch_step(1, h->dn, h->w, h->C, n_scen, r, sigma_s, nullptr, nullptr, p_u, p, nullptr, st);
+  return cuda_check(h, "pf_recover_step");
+}
+
+pf_status pf_reduced_gradient(pf_net* h, int32_t n_scen, const double* v, const double* theta, const double* p_g,
+                              const double* p_d, const double* y, double* lambda, double* grad, void* stream) {
+  if (!h) return PF_ERR_ARG;
+  if (!p_g || !y || !grad || n_scen < 1) { h->err = "pf_reduced_gradient: bad argument"; return PF_ERR_ARG; }
+  if (n_scen > h->max_scen) { h->err = "pf_reduced_gradient: n_scen > max_scen"; return PF_ERR_CAPACITY; }
+  if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
+  if (pf_status st = point_check(h, "pf_reduced_gradient", n_scen, v, theta)) return st;
+  cudaStream_t st = (cudaStream_t)stream;
+  // μ̃^P_r0 = y_0 + (2c₁p_ref + c₂) is the only prep output used (λ = 0, no Σ)
+  h->launches += launch_prep(h->dn, h->w, n_scen, p_d, h->w.zero, y, nullptr, nullptr, st);
+  h->launches += launch_step(2, h->dn, h->w, h->C, n_scen, nullptr, nullptr, y, p_g, nullptr, grad, lambda, st);
+  return cuda_check(h, "pf_reduced_gradient");
+}
+
+pf_status pf_power_flow(pf_net* h, int32_t n_scen, double* v, double* theta, const double* p_g, const double* q_g,
+                        const double* p_d, const double* q_d, double tol, int32_t max_iter, int32_t* iters,
+                        double* resid, int32_t* info, void* stream) {
+  if (!h) return PF_ERR_ARG;
+  if (!v || !theta || !p_g || n_scen < 1 || max_iter < 0 || !(tol >= 0.0)) {
+    h->err = "pf_power_flow: bad argument";
+    return PF_ERR_ARG;
+  }
+  if (n_scen > h->max_scen) { h->err = "pf_power_flow: n_scen > max_scen"; return PF_ERR_CAPACITY; }
+  if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  const Work& w = h->w;
+  std::vector<double> res(n_scen);
+  std::vector<int> act(n_scen, 1), it(n_scen, 0), inf(n_scen, 0), lui(n_scen, 0);
+  h->lu_scen = 0;
+  for (int k = 0;; ++k) {
+    h->launches += launch_eval(h->dn, w, n_scen, v, theta, p_g, q_g ? q_g : w.zero, p_d, q_d, w.gbuf, nullptr,
+                               nullptr, st);
+    h->launches += launch_pf_resid(h->dn, w, n_scen, st);
+    if (cudaMemcpyAsync(res.data(), w.res, n_scen * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return cuda_check(h, "pf_power_flow");
+    int n_act = 0;
+    for (int s = 0; s < n_scen; ++s) {
+      if (!act[s]) continue;
+      if (res[s] <= tol) act[s] = 0;                                  // converged
+      else if (!(res[s] == res[s]) || k == max_iter) { act[s] = 0; inf[s] = -1; }  // diverged / no convergence
+      n_act += act[s];
+    }
+    if (!n_act) break;
+    if (cudaMemcpyAsync(w.active, act.data(), n_scen * sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return cuda_check(h, "pf_power_flow");
+    h->launches += launch_jacobian(h->dn, w, n_scen, v, theta, nullptr, nullptr, nullptr, nullptr, st, h->lu_cs);
+    if (cudaMemcpyAsync(lui.data(), w.info, n_scen * sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return cuda_check(h, "pf_power_flow");
+    for (int s = 0; s < n_scen; ++s)
+      if (act[s] && lui[s]) { act[s] = 0; inf[s] = lui[s]; }          // singular Jacobian (R18 pivot k+1)
+    if (cudaMemcpyAsync(w.active, act.data(), n_scen * sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return cuda_check(h, "pf_power_flow");
+    h->launches += launch_newton_step(h->dn, w, h->C, n_scen, v, theta, st);
+    for (int s = 0; s < n_scen; ++s) it[s] += act[s];
+  }
+  // factorize at the final point, so a reduction / gradient / recovery can follow (RedLin, Algorithm 2)
+  h->launches += launch_jacobian(h->dn, w, n_scen, v, theta, nullptr, nullptr, nullptr, nullptr, st, h->lu_cs);
+  if (pf_status e = cuda_check(h, "pf_power_flow")) return e;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check(h, "pf_power_flow");
+  h->lu_scen = n_scen; h->lu_v = v; h->lu_th = theta;
+  for (int s = 0; s < n_scen; ++s) {
+    if (iters) iters[s] = it[s];
+    if (resid) resid[s] = res[s];
+    if (info) info[s] = inf[s];
+  }
+  return PF_OK;
 }
 
 #ifdef PF_LU_TRACE  // debug builds only (tools/lu_trace.py)

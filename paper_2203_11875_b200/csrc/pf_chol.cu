@@ -760,18 +760,20 @@ size_t chol_flag_ints(int n_u) {
 }
 size_t chol_vec_doubles(int n_u) { return 2 * (size_t)kRhsCap * ((n_u + NB - 1) / NB) * NB; }
 
+int chol_grid_max() {
+  cudaFuncSetAttribute(k_chol_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDagSmem);
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_dag, kDagThreads, kDagSmem);
+  cudaGetLastError();
+  return std::max(1, sms * std::max(per, 1));
+}
+
 int launch_chol(const DevNet& net, const Work& w, int n_scen, double* K, const double* sigma_u, double delta_w,
-                double* rhs, int nrhs, int* info, int* info_ws, cudaStream_t st) {
+                double* rhs, int nrhs, int* info, int* info_ws, cudaStream_t st, int grid_max) {
   const int n = net.n_u, nt = (n + NB - 1) / NB, ntri = nt * (nt + 1) / 2;
-  static int grid_max = 0;
-  if (!grid_max) {
-    cudaFuncSetAttribute(k_chol_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDagSmem);
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_chol_dag, kDagThreads, kDagSmem);
-    grid_max = std::max(1, sms * std::max(per, 1));
-  }
+  cudaFuncSetAttribute(k_chol_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDagSmem);  // per device, idempotent
   int launches = 0;
   k_chol_pack<<<dim3(ntri, n_scen), 256, 0, st>>>(n, nt, K, sigma_u, delta_w, w.ctile, w.cflag, w.cticket, info_ws,
                                                    w.cticket + 1);

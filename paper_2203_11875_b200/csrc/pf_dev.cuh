@@ -49,6 +49,12 @@ struct DevNet {
   const int4 *u_top, *u_bot, *ua_top, *ua_bot;
   const int *u_top_ptr, *u_bot_ptr, *ua_top_ptr, *ua_bot_ptr;
   const int4 *inc_rec;          // [2 n_l] per incidence: {line, far θ row, far v row | −1−u, from | 2(gen+1)}
+  // step recovery / Newton (pf_step): permuted slab row <-> x index, the G row
+  // (P_i = i, Q_i = n_b + i) of each permuted row, and A by columns (CSC over
+  // z = [u; x]: rows and positions in the CSR value array)
+  const int *perm, *iperm, *row_g;
+  const int *a_cptr, *a_crow, *a_cpos, *a_idx;
+  const int *u_gen;             // [n_u] generator of a p_g control, −1 for v controls
   int C;                        // directions per tile (slab row width)
   int lu_maxlen;                // longest row of the filled LU pattern
 };
@@ -76,6 +82,11 @@ struct Work {
   double* lblk;    // [max_scen][n_l][LB_N]  line-local K blocks
   double* sflow;   // [max_scen][4][n_l]
   int* info;       // [max_scen] internal pivot info
+  double* aval;    // [max_scen][nnz_a]   A values (CSR of pf_get_structure) of the last pf_jacobian
+  double* zero;    // [max_scen][n_u + n_x + m]  zeros (V = 0 directions, λ = 0)
+  double* gbuf;    // [max_scen][2 n_b]   G of the Newton iterations
+  double* res;     // [max_scen]          ‖g‖∞ per scenario (Newton)
+  int* active;     // [max_scen]          Newton: 1 while the scenario iterates
   double* slabZ;   // [max_tiles][n_x][C]
   double* slabW;   // [max_tiles][n_x][C]
   double* hu;      // [max_tiles][n_u][C]

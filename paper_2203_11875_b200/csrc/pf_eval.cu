@@ -218,9 +218,13 @@ __global__ void k_gather(DevNet n, Work w, int n_scen, double* __restrict__ Gx,
       continue;
     }
     k -= n.nnz_gu;
-    if (!A) continue;
+    double* Aw = w.aval + (size_t)s * n.nnz_a;  // kept for the step recovery / reduced gradient
     const int src = __ldg(n.a_src + k);
-    if (src >= 0) { A[(size_t)s * n.nnz_a + k] = jb[src]; continue; }
+    if (src >= 0) {
+      Aw[k] = jb[src];
+      if (A) A[(size_t)s * n.nnz_a + k] = jb[src];
+      continue;
+    }
     // h row owning position k: binary search in a_ptr over rows [n_r, m)
     int lo = n.n_r, hi = n.m - 1;
     while (lo < hi) { int mid = (lo + hi + 1) >> 1; if (__ldg(n.a_ptr + mid) <= k) lo = mid; else hi = mid - 1; }
@@ -232,7 +236,11 @@ __global__ void k_gather(DevNet n, Work w, int n_scen, double* __restrict__ Gx,
     const double sp = e == 0 ? ls[LS_SPF * n.n_l + l] : ls[LS_SPT * n.n_l + l];
     const double sq = e == 0 ? ls[LS_SQF * n.n_l + l] : ls[LS_SQT * n.n_l + l];
     for (int a = 0; a < 4; ++a)
-      if (__ldg(n.ah_off + 4 * h + a) == k - base) A[(size_t)s * n.nnz_a + k] = 2.0 * (sp * g.p[a] + sq * g.q[a]);
+      if (__ldg(n.ah_off + 4 * h + a) == k - base) {
+        const double val = 2.0 * (sp * g.p[a] + sq * g.q[a]);
+        Aw[k] = val;
+        if (A) A[(size_t)s * n.nnz_a + k] = val;
+      }
   }
 }
 
@@ -632,30 +640,38 @@ int launch_eval(const DevNet& n, const Work& w, int n_scen, const double* v, con
   return 2;
 }
 
+static size_t lu_smem(const DevNet& n) {
+  return (size_t)(kLuThreads / 32) * n.lu_maxlen * sizeof(double) + kLuStageWarps * kLuStageBytes;
+}
+
+int lu_cluster_size(const DevNet& n) {
+  // 16-CTA clusters (non-portable) when the part supports them, else 8, 4, …
+  const size_t smem = lu_smem(n);
+  cudaFuncSetAttribute(k_lu, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int CS = 0;
+  for (int cs : {16, 8, 4, 2, 1}) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cs); cfg.blockDim = dim3(kLuThreads); cfg.dynamicSmemBytes = smem;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, (void*)k_lu, &cfg) == cudaSuccess && nc > 0) { CS = cs; break; }
+  }
+  cudaGetLastError();
+  return CS ? CS : 1;
+}
+
 int launch_jacobian(const DevNet& n, const Work& w, int n_scen, const double* v, const double* th,
-                    double* Gx, double* Gu, double* A, int* info, cudaStream_t st, cudaEvent_t* ev) {
+                    double* Gx, double* Gu, double* A, int* info, cudaStream_t st, int lu_cs, cudaEvent_t* ev) {
   k_line_state<<<blocks_for((long long)n_scen * n.n_l), kThreads, 0, st>>>(n, w, n_scen, v, th);
   k_bus_v<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen, v);
   k_jbus<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen);
   k_gather<<<blocks_for((long long)n_scen * (n.nnz_gx + n.nnz_gu + n.nnz_a)), kThreads, 0, st>>>(n, w, n_scen, Gx, Gu, A);
-  const size_t smem = (size_t)(kLuThreads / 32) * n.lu_maxlen * sizeof(double) + kLuStageWarps * kLuStageBytes;
-  static int CS = 0;
-  if (!CS) {  // 16-CTA clusters (non-portable) when the part supports them, else 8
-    cudaFuncSetAttribute(k_lu, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    for (int cs : {16, 8, 4, 2, 1}) {
-      cudaLaunchConfig_t cfg = {};
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-      cfg.gridDim = dim3(cs); cfg.blockDim = dim3(kLuThreads); cfg.dynamicSmemBytes = smem;
-      cfg.attrs = at; cfg.numAttrs = 1;
-      int nc = 0;
-      if (cudaOccupancyMaxActiveClusters(&nc, (void*)k_lu, &cfg) == cudaSuccess && nc > 0) { CS = cs; break; }
-    }
-    cudaGetLastError();
-    if (!CS) CS = 1;
-  }
+  const size_t smem = lu_smem(n);
+  const int CS = lu_cs;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];

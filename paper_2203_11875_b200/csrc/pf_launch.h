@@ -11,8 +11,10 @@ int launch_eval(const DevNet& n, const Work& w, int n_scen, const double* v, con
 
 // A4/A5: line state, J_bus values, gathers into G_x/G_u/A, numeric LU + transposed values.
 int launch_jacobian(const DevNet& n, const Work& w, int n_scen, const double* v, const double* th,
-                    double* Gx, double* Gu, double* A, int* info, cudaStream_t st,
+                    double* Gx, double* Gu, double* A, int* info, cudaStream_t st, int lu_cs,
                     cudaEvent_t* ev = nullptr /* optional: [2] around k_lu */);
+// k_lu cluster size supported on the current device (sets k_lu's function attributes there)
+int lu_cluster_size(const DevNet& n);
 
 // A6: per-scenario ψ weights w̄ and bus/line state for the HVP.
 int launch_prep(const DevNet& n, const Work& w, int n_scen, const double* p_d, const double* lam,
@@ -25,7 +27,17 @@ int launch_reduce(const DevNet& n, const Work& w, int C, int n_scen, const doubl
 
 // A9: symmetrize + shift + pack, tile-DAG FP64 Cholesky (DMMA updates) with the solves fused in.
 int launch_chol(const DevNet& n, const Work& w, int n_scen, double* K, const double* sigma_u, double delta_w,
-                double* rhs, int nrhs, int* info, int* info_ws, cudaStream_t st);
+                double* rhs, int nrhs, int* info, int* info_ws, cudaStream_t st, int grid_max);
+// resident k_chol_dag CTAs on the current device (sets its SMEM attribute there)
+int chol_grid_max();
+
+// NEXT-1 / NEXT-2 single-direction passes (pf_reduce.cu): what = 0 condensed rhs (out = b),
+// 1 step recovery (out = p), 2 reduced gradient (out = ∇f_r, out2 = λ).
+int launch_step(int what, const DevNet& n, const Work& w, int C, int n_scen, const double* r, const double* sig_s,
+                const double* y, const double* p_g, const double* p_u, double* out, double* out2, cudaStream_t st);
+// Newton: ‖g‖∞ of w.gbuf per scenario into w.res; one step x −= G_x⁻¹ g on the active scenarios.
+int launch_pf_resid(const DevNet& n, const Work& w, int n_scen, cudaStream_t st);
+int launch_newton_step(const DevNet& n, const Work& w, int C, int n_scen, double* v, double* th, cudaStream_t st);
 
 int pick_tile_cols(int n_x, int n_scen_x_N);
 #ifdef PF_LU_TRACE

@@ -232,11 +232,14 @@ template <int C>
 struct FromRhs {
   const int* gur_ptr; const int* gur_col; const int* gur_src; const double* gu;
   const double* Vs;  // dense V row of this lane's first direction (the next ones follow at stride n_u), or null = unit
+  const double* X4;  // optional extra right-hand side of direction 0 (step recovery, Newton): B −= P X4
+  const int* x4map;  //   … X4 entry of permuted row r: X4[x4map[r]]
   int base, nvalid, n_u, lane;  // base = col0 + tile*C: the u column of direction 0 of the tile
   __device__ __forceinline__ void operator()(int r, double* a) const {
     constexpr int CPL = Geo<C>::CPL;
 #pragma unroll
     for (int j = 0; j < CPL; ++j) a[j] = 0.0;
+    if (X4 && lane == 0) a[0] = -X4[__ldg(x4map + r)];
     for (int e = __ldg(gur_ptr + r); e < __ldg(gur_ptr + r + 1); ++e) {
       const int c = __ldg(gur_col + e);
       if (!Vs && (c < base || c >= base + nvalid)) continue;  // unit directions: only the tile's columns
@@ -477,7 +480,8 @@ __device__ __forceinline__ void load_j(const double* p, double* j) {
 // ---------------------------------------------------------------- a, b
 template <int C>
 __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Work w, const double* __restrict__ V, int col0,
-                                                                   int N, int rt) {
+                                                                   int N, int rt, const double* __restrict__ X4 = nullptr,
+                                                                   const int* __restrict__ x4map = nullptr, int x4ld = 0) {
   constexpr int W = Geo<C>::W;
   extern __shared__ unsigned bm_sm[];  // reach bitmap of this tile (rt ≥ 0)
   __shared__ __align__(16) double2 ent_sm[kThreads / Geo<C>::W][2][2][Geo<C>::W];  // per-team entry buffers
@@ -496,6 +500,7 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
   rhs.gur_ptr = n.gur_ptr; rhs.gur_col = n.gur_col; rhs.gur_src = n.gur_src; rhs.gu = gu;
   rhs.Vs = V ? V + ((size_t)s * N + tile * C + lane * Geo<C>::CPL) * n_u : nullptr;
   rhs.base = col0 + tile * C; rhs.nvalid = nvalid; rhs.n_u = n_u; rhs.lane = lane;
+  rhs.X4 = X4 ? X4 + (size_t)s * x4ld : nullptr; rhs.x4map = x4map;
   if (rt >= 0) {
     // sparse RHS: only the tile's reach (tree paths of its columns' G_u rows) is nonzero
     const unsigned* bmg = n.rowbm + (size_t)(rt + tile) * n.bmw;
@@ -747,7 +752,7 @@ __global__ void __launch_bounds__(kThreads, kHvpMinBlocks) k_hvp(DevNet n, Work 
 
 // ---------------------------------------------------------------- d, e
 template <int C>
-__global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_adj(DevNet n, Work w, int N) {
+__global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_adj(DevNet n, Work w, int N, bool full = false) {
   constexpr int W = Geo<C>::W;
   __shared__ __align__(16) double2 sm_adj[(kThreads / W) * 4 * W];  // the sweeps' per-team entry buffers
   const int ntile = (N + C - 1) / C;
@@ -759,9 +764,14 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_adj(DevNet n, Wor
   double2* ent = sm_adj + (size_t)team * 4 * W;
   sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, Y, true, lane, team, nteam, ent, FromSlab(), nullptr, n.p1_task,
                  n.p1_ptr, n.p1_lev0);                                                  // U^{-T}
-  // L^{-T}: only the ancestors of G_u's rows (the projection reads Ψ there)
-  sweep<C, false>(n.ua_top, n.ua_top_ptr, n.nlevU, pk, Y, false, lane, team, nteam, ent, FromSlab(), nullptr, n.ua_bot,
-                  n.ua_bot_ptr);
+  // L^{-T}: only the ancestors of G_u's rows (the projection reads Ψ there), or every row
+  // when the whole Ψ is an output (adjoint step / multipliers)
+  if (full)
+    sweep<C, false>(n.u_top, n.u_top_ptr, n.nlevU, pk, Y, false, lane, team, nteam, ent, FromSlab(), nullptr, n.u_bot,
+                    n.u_bot_ptr);
+  else
+    sweep<C, false>(n.ua_top, n.ua_top_ptr, n.nlevU, pk, Y, false, lane, team, nteam, ent, FromSlab(), nullptr, n.ua_bot,
+                    n.ua_bot_ptr);
 }
 
 // G_u of each scenario in column (CSC) order, packed {value, row·C} for the projection
@@ -843,6 +853,169 @@ __global__ void __launch_bounds__(kThreads) k_proj(DevNet n, Work w, int N, doub
   }
 }
 
+// ---------------------------------------------------------------- NEXT-1 / NEXT-2 single-direction passes
+// One direction per scenario: the tile of scenario s is CTA s (ntile = 1) and the
+// direction is column 0 of its slabs.  DESIGN.md §"Step recovery" derives the passes:
+// with q = [r₁; r₂] + Aᵀ(Σ_s r₅ + r₃) and d = [V; Z], Z = −G_x⁻¹(G_u V + r₄), the HVP
+// pipeline runs on H := −(K d + q):
+//   condensed rhs   (V = 0):   b = H_u − G_uᵀG_x⁻ᵀH_x  (= −(r̂₁ + Â_uᵀΣ_s r̂₃ + Â_uᵀ r̂₂), R10);
+//   recovery (V = p_u):        p_x = Z, p_λ = G_x⁻ᵀH_x, p_s = A[p_u; p_x] + r₅, p_y = Σ_s p_s + r₃;
+//   reduced gradient:          H := ∇_z(f + yᵀ[r; h]) = Aᵀỹ + ∂f/∂p_g, λ = −G_x⁻ᵀH_x, ∇f_r = H_u − G_uᵀG_x⁻ᵀH_x.
+enum { KV_RHS = 0, KV_GRAD = 1 };
+
+template <int C>
+__global__ void k_kkt_vec(DevNet n, Work w, int n_scen, int mode, const double* __restrict__ r,
+                          const double* __restrict__ sig_s, const double* __restrict__ y,
+                          const double* __restrict__ p_g) {
+  const int n_u = n.n_u, n_x = n.n_x, m = n.m, nz = n_u + n_x;
+  const size_t ld = 2 * (size_t)n_x + n_u + 2 * (size_t)m;
+  const long long total = (long long)n_scen * nz;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / nz), z = (int)(t % nz);
+    const double* A = w.aval + (size_t)s * n.nnz_a;
+    const double* rs = r ? r + s * ld : nullptr;
+    double q = 0.0;
+    for (int e = __ldg(n.a_cptr + z); e < __ldg(n.a_cptr + z + 1); ++e) {
+      const int k = __ldg(n.a_crow + e);
+      double om;
+      if (mode == KV_RHS) {
+        om = rs[n_u + n_x + k];                                                   // r₃
+        if (sig_s) om += sig_s[(size_t)s * m + k] * rs[n_u + n_x + m + n_x + k];  // Σ_s r₅
+      } else {
+        // ỹ: y, and on row P_r0 (r row 0) the implicit p_ref's (2c₁p_ref + c₂) (R8), which
+        // k_prep_bus1 folded into μ̃^P_r0 = y_0 + (2c₁p_ref + c₂) (λ has no P_r0 row)
+        om = k == 0 ? w.bs[(size_t)s * BS_N * n.n_b + BS_MUP * n.n_b + n.r0] : y[(size_t)s * m + k];
+      }
+      q += A[__ldg(n.a_cpos + e)] * om;
+    }
+    double* H = z < n_u ? w.hu + (size_t)s * n_u * C + (size_t)z * C
+                        : w.slabW + (size_t)s * n_x * C + (size_t)__ldg(n.iperm + z - n_u) * C;
+    if (mode == KV_RHS) {
+      q += rs[z];  // [r₁; r₂]
+      *H = -(*H + q);
+    } else {
+      if (z < n_u) {
+        const int g = __ldg(n.u_gen + z);
+        if (g >= 0) q += 2.0 * __ldg(n.c_quad + g) * p_g[(size_t)s * n.n_g + g] + __ldg(n.c_lin + g);
+      }
+      *H = q;
+    }
+  }
+}
+
+// Step recovery output, ordered (p_u, p_x, p_s, p_λ, p_y) like eq. kktmatrix:normal's blocks.
+template <int C>
+__global__ void k_step_out(DevNet n, Work w, int n_scen, const double* __restrict__ r, const double* __restrict__ sig_s,
+                           const double* __restrict__ p_u, double* __restrict__ p) {
+  const int n_u = n.n_u, n_x = n.n_x, m = n.m;
+  const int ld = 2 * n_x + n_u + 2 * m;
+  const long long total = (long long)n_scen * ld;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / ld);
+    int k = (int)(t % ld);
+    const double* Z = w.slabZ + (size_t)s * n_x * C;
+    const double* Y = w.slabW + (size_t)s * n_x * C;
+    const double* pu = p_u + (size_t)s * n_u;
+    const double* rs = r + (size_t)s * ld;
+    double* ps = p + (size_t)s * ld;
+    if (k < n_u) { ps[k] = pu[k]; continue; }
+    k -= n_u;
+    if (k < n_x) { ps[n_u + k] = Z[(size_t)__ldg(n.iperm + k) * C]; continue; }
+    k -= n_x;
+    if (k < m) {  // p_s = A [p_u; p_x] + r₅ (row 5 of K_aug), p_y = Σ_s p_s + r₃ (row 3)
+      double a = rs[n_u + n_x + m + n_x + k];
+      const double* A = w.aval + (size_t)s * n.nnz_a;
+      for (int e = __ldg(n.a_ptr + k); e < __ldg(n.a_ptr + k + 1); ++e) {
+        const int z = __ldg(n.a_idx + e);
+        a += A[e] * (z < n_u ? pu[z] : Z[(size_t)__ldg(n.iperm + z - n_u) * C]);
+      }
+      ps[n_u + n_x + k] = a;
+      ps[n_u + n_x + m + n_x + k] = (sig_s ? sig_s[(size_t)s * m + k] : 0.0) * a + rs[n_u + n_x + k];
+      continue;
+    }
+    k -= m;
+    if (k < n_x) { ps[n_u + n_x + m + k] = Y[(size_t)__ldg(n.iperm + k) * C]; continue; }
+  }
+}
+
+// λ = −Ψ (the adjoint step of Algorithm 2: λ = −G_x⁻ᵀ∇_xℒ), x order
+template <int C>
+__global__ void k_lam_out(DevNet n, Work w, int n_scen, double* __restrict__ lam) {
+  const long long total = (long long)n_scen * n.n_x;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / n.n_x), x = (int)(t % n.n_x);
+    lam[t] = -w.slabW[(size_t)s * n.n_x * C + (size_t)__ldg(n.iperm + x) * C];
+  }
+}
+
+// Newton: x += Z (Z = −G_x⁻¹ g) for the scenarios still iterating
+template <int C>
+__global__ void k_pf_update(DevNet n, Work w, int n_scen, double* __restrict__ v, double* __restrict__ th) {
+  const long long total = (long long)n_scen * n.n_b;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / n.n_b), i = (int)(t % n.n_b);
+    if (!w.active[s]) continue;
+    const double* Z = w.slabZ + (size_t)s * n.n_x * C;
+    const int pt = __ldg(n.bus_pth + i), pv = __ldg(n.bus_pv + i);
+    if (pt >= 0) th[t] += Z[(size_t)pt * C];
+    if (pv >= 0) v[t] += Z[(size_t)pv * C];
+  }
+}
+
+inline int grid_for(long long n) { return (int)std::max<long long>(1, std::min<long long>(148LL * 16, (n + kThreads - 1) / kThreads)); }
+
+template <int C>
+void one_dir_fwd_hvp(const DevNet& n, const Work& w, int n_scen, const double* V, const double* X4, const int* map,
+                     int x4ld, bool hvp, cudaStream_t st) {
+  k_fwd<C><<<dim3(1, n_scen), kThreads, 0, st>>>(n, w, V, 0, 1, -1, X4, map, x4ld);
+  if (!hvp) return;
+  k_mu<C, kMuTiles><<<dim3((n.n_gb + kBusPerCta - 1) / kBusPerCta, 1, n_scen), kThreads, 0, st>>>(n, w, V, 0, 1);
+  k_hvp<C, kHvpTiles><<<dim3((n.n_b + kHvpBusPerCta - 1) / kHvpBusPerCta, 1, n_scen), kThreads, 0, st>>>(n, w, V, 0, 1);
+}
+
+template <int C>
+int step_all(int what, const DevNet& n, const Work& w, int n_scen, const double* r, const double* sig_s,
+             const double* y, const double* p_g, const double* p_u, double* out, double* out2, cudaStream_t st) {
+  const int ld = 2 * n.n_x + n.n_u + 2 * n.m;
+  const int nz = n.n_u + n.n_x;
+  int launches = 0;
+  if (what == 0 || what == 2) {  // the projection needs G_u packed by columns
+    k_pack_gu<<<(int)std::min<long long>(4096, ((long long)n_scen * n.nnz_gu + kThreads - 1) / kThreads), kThreads, 0,
+                st>>>(n, w, n_scen);
+    ++launches;
+  }
+  if (what == 0 || what == 1) {  // condensed rhs / recovery: forward pass with r₄, K·d
+    one_dir_fwd_hvp<C>(n, w, n_scen, what == 0 ? w.zero : p_u, r + n.n_u + n.n_x + n.m, n.perm, ld, true, st);
+    k_kkt_vec<C><<<grid_for((long long)n_scen * nz), kThreads, 0, st>>>(n, w, n_scen, KV_RHS, r, sig_s, nullptr, nullptr);
+    k_adj<C><<<dim3(1, n_scen), kThreads, 0, st>>>(n, w, 1, what == 1);
+    launches += 6;
+  } else {  // reduced gradient
+    k_kkt_vec<C><<<grid_for((long long)n_scen * nz), kThreads, 0, st>>>(n, w, n_scen, KV_GRAD, nullptr, nullptr, y, p_g);
+    k_adj<C><<<dim3(1, n_scen), kThreads, 0, st>>>(n, w, 1, true);
+    launches += 2;
+  }
+  if (what == 0 || what == 2) {
+    k_proj<C><<<dim3((n.n_u + kCH - 1) / kCH, 1, n_scen), kThreads, 0, st>>>(n, w, 1, out);
+    ++launches;
+  }
+  if (what == 1) {
+    k_step_out<C><<<grid_for((long long)n_scen * ld), kThreads, 0, st>>>(n, w, n_scen, r, sig_s, p_u, out);
+    ++launches;
+  }
+  if (what == 2 && out2) {
+    k_lam_out<C><<<grid_for((long long)n_scen * n.n_x), kThreads, 0, st>>>(n, w, n_scen, out2);
+    ++launches;
+  }
+  return launches;
+}
+
+template <int C>
+int newton_step(const DevNet& n, const Work& w, int n_scen, double* v, double* th, cudaStream_t st) {
+  one_dir_fwd_hvp<C>(n, w, n_scen, w.zero, w.gbuf, n.row_g, 2 * n.n_b, false, st);  // Z = −G_x⁻¹ g
+  k_pf_update<C><<<grid_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen, v, th);
+  return 2;
+}
+
 template <int C>
 void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int col0, int N, double* KV,
                 cudaStream_t st, cudaEvent_t* ev) {
@@ -868,16 +1041,56 @@ void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int
 }  // namespace
 
 int pick_tile_cols(int n_x, int total_cols) {
-  if (const char* e = getenv("PF_TILE_COLS")) {  // experiments: force 8 / 16 / 32 / 64
-    const int c = atoi(e);
-    if (c == 8 || c == 16 || c == 32 || c == 64) return c;
-  }
+  (void)n_x;
   // Wide tiles carry more directions per memory round trip of the latency-
   // bound sweeps; narrow ones keep ≥ 2 CTAs per SM when the work is small.
   if (total_cols >= 64 * 296) return 64;
   if (total_cols >= 32 * 296) return 32;
   if (total_cols >= 16 * 296) return 16;
   return 8;
+}
+
+// ‖g‖∞ over the x rows of G (w.gbuf) per scenario
+__global__ void k_pf_resid(DevNet n, Work w, int n_scen) {
+  __shared__ double red[kThreads / 32];
+  const int s = blockIdx.x;
+  double mx = 0.0;
+  for (int r = threadIdx.x; r < n.n_x; r += blockDim.x) {
+    const double g = w.gbuf[(size_t)s * 2 * n.n_b + __ldg(n.row_g + r)];
+    mx = (g != g) ? g : fmax(mx, fabs(g));  // NaN propagates
+  }
+  for (int o = 16; o > 0; o >>= 1) { const double t = __shfl_xor_sync(0xffffffffu, mx, o); mx = (t != t) ? t : fmax(mx, t); }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int k = 0; k < kThreads / 32; ++k) a = (red[k] != red[k]) ? red[k] : fmax(a, red[k]);
+    w.res[s] = a;
+  }
+}
+
+int launch_step(int what, const DevNet& n, const Work& w, int C, int n_scen, const double* r, const double* sig_s,
+                const double* y, const double* p_g, const double* p_u, double* out, double* out2, cudaStream_t st) {
+  switch (C) {
+    case 64: return step_all<64>(what, n, w, n_scen, r, sig_s, y, p_g, p_u, out, out2, st);
+    case 32: return step_all<32>(what, n, w, n_scen, r, sig_s, y, p_g, p_u, out, out2, st);
+    case 16: return step_all<16>(what, n, w, n_scen, r, sig_s, y, p_g, p_u, out, out2, st);
+    default: return step_all<8>(what, n, w, n_scen, r, sig_s, y, p_g, p_u, out, out2, st);
+  }
+}
+
+int launch_pf_resid(const DevNet& n, const Work& w, int n_scen, cudaStream_t st) {
+  k_pf_resid<<<n_scen, kThreads, 0, st>>>(n, w, n_scen);
+  return 1;
+}
+
+int launch_newton_step(const DevNet& n, const Work& w, int C, int n_scen, double* v, double* th, cudaStream_t st) {
+  switch (C) {
+    case 64: return newton_step<64>(n, w, n_scen, v, th, st);
+    case 32: return newton_step<32>(n, w, n_scen, v, th, st);
+    case 16: return newton_step<16>(n, w, n_scen, v, th, st);
+    default: return newton_step<8>(n, w, n_scen, v, th, st);
+  }
 }
 
 int launch_reduce(const DevNet& n, const Work& w, int C, int n_scen, const double* V, int col0,

@@ -23,9 +23,10 @@ STRUCTURE = dict(x_theta=0, x_v=1, u_v=2, u_p=3, gx_ptr=4, gx_idx=5, gu_ptr=6, g
                  level_u_ptr=17, level_u_blk=18)
 
 # exported symbols declared in include/pf.h
-SYMBOLS = ["pf_build_network", "pf_destroy", "pf_query", "pf_get_structure", "pf_last_error", "pf_build_error",
+SYMBOLS = ["pf_build_network", "pf_build_network_ex", "pf_destroy", "pf_query", "pf_get_structure", "pf_last_error", "pf_build_error",
            "pf_eval_constraints", "pf_jacobian", "pf_reduced_hessian_batch", "pf_condensed_kkt_solve",
-           "pf_launch_count", "pf_profile", "pf_kernel_times"]
+           "pf_launch_count", "pf_profile", "pf_kernel_times", "pf_condensed_rhs", "pf_recover_step",
+           "pf_power_flow", "pf_reduced_gradient"]
 
 
 class PFError(RuntimeError):
@@ -56,6 +57,9 @@ def load_library():
     P, I32, D, VP = ctypes.c_void_p, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
     lib.pf_build_network.argtypes = [I32, I32, I32] + [P] * 8 + [I32] + [P] * 5 + [I32, I32, I32, ctypes.POINTER(P)]
     lib.pf_build_network.restype = ctypes.c_int
+    lib.pf_build_network_ex.argtypes = [I32, I32, I32] + [P] * 8 + [I32] + [P] * 5 + [I32, I32, I32, I32,
+                                                                                ctypes.POINTER(P)]
+    lib.pf_build_network_ex.restype = ctypes.c_int
     lib.pf_destroy.argtypes = [P]
     lib.pf_destroy.restype = None
     lib.pf_query.argtypes = [P, ctypes.POINTER(pf_dims)]
@@ -74,6 +78,14 @@ def load_library():
     lib.pf_reduced_hessian_batch.restype = ctypes.c_int
     lib.pf_condensed_kkt_solve.argtypes = [P, I32, P, P, D, P, I32, P, VP]
     lib.pf_condensed_kkt_solve.restype = ctypes.c_int
+    lib.pf_condensed_rhs.argtypes = [P, I32] + [P] * 9 + [VP]
+    lib.pf_condensed_rhs.restype = ctypes.c_int
+    lib.pf_recover_step.argtypes = [P, I32] + [P] * 10 + [VP]
+    lib.pf_recover_step.restype = ctypes.c_int
+    lib.pf_power_flow.argtypes = [P, I32] + [P] * 6 + [D, I32, P, P, P, VP]
+    lib.pf_power_flow.restype = ctypes.c_int
+    lib.pf_reduced_gradient.argtypes = [P, I32] + [P] * 7 + [VP]
+    lib.pf_reduced_gradient.restype = ctypes.c_int
     lib.pf_launch_count.argtypes = [P]
     lib.pf_launch_count.restype = ctypes.c_int64
     lib.pf_profile.argtypes = [P, I32]
@@ -120,7 +132,7 @@ class Network:
     """A built network handle (pf_build_network) plus typed wrappers of the
     compute entry points.  All tensors are CUDA float64 / int32."""
 
-    def __init__(self, net, max_batch, max_scen=1, device=0):
+    def __init__(self, net, max_batch, max_scen=1, device=0, tile_cols=0):
         lib = load_library()
         self._lib = lib
         keep = []
@@ -136,14 +148,14 @@ class Network:
             return arr.ctypes.data_as(ctypes.c_void_p)
 
         h = ctypes.c_void_p()
-        st = lib.pf_build_network(
+        st = lib.pf_build_network_ex(
             int(net["n_b"]), int(net["n_l"]), int(net["n_g"]),
             hp(net["line_from"], np.int32), hp(net["line_to"], np.int32),
             hc(net["Y_ff"]), hc(net["Y_ft"]), hc(net["Y_tf"]), hc(net["Y_tt"]), hc(net["Y_sh"]),
             hp(net["gen_bus"], np.int32), int(net["ref_bus"]),
             hp(net["p_d"], np.float64), hp(net["q_d"], np.float64), hp(net["F_max"], np.float64),
             hp(net["c_quad"], np.float64), hp(net["c_lin"], np.float64),
-            int(max_batch), int(max_scen), int(device), ctypes.byref(h))
+            int(max_batch), int(max_scen), int(device), int(tile_cols), ctypes.byref(h))
         if st != PF_OK:
             raise PFError(st, lib.pf_build_error().decode())
         self._h = h
@@ -251,3 +263,72 @@ class Network:
             _dev(info, "info", torch.int32, n_scen), _stream(stream))
         self._check(st, "pf_condensed_kkt_solve")
         return K, rhs, info
+
+    # ---------------------------------------------------------------- NEXT-1 / NEXT-2
+    def kkt_len(self):
+        d = self.dims
+        return 2 * d["n_x"] + d["n_u"] + 2 * d["m"]
+
+    def pf_condensed_rhs(self, n_scen, v, theta, lam, y, r, b=None, sigma_s=None, sigma_x=None, p_d=None,
+                         stream=None):
+        import torch
+        d = self.dims
+        f64 = torch.float64
+        if b is None:
+            b = torch.empty(n_scen, d["n_u"], dtype=f64, device=r.device)
+        st = self._lib.pf_condensed_rhs(
+            self._h, n_scen, _dev(v, "v", f64, n_scen * d["n_b"]), _dev(theta, "theta", f64, n_scen * d["n_b"]),
+            _dev(p_d, "p_d", f64, n_scen * d["n_b"]), _dev(lam, "lambda", f64, n_scen * d["n_x"]),
+            _dev(y, "y", f64, n_scen * d["m"]), _dev(sigma_s, "sigma_s", f64, n_scen * d["m"]),
+            _dev(sigma_x, "sigma_x", f64, n_scen * d["n_x"]), _dev(r, "r", f64, n_scen * self.kkt_len()),
+            _dev(b, "b", f64, n_scen * d["n_u"]), _stream(stream))
+        self._check(st, "pf_condensed_rhs")
+        return b
+
+    def pf_recover_step(self, n_scen, v, theta, lam, y, r, p_u, p=None, sigma_s=None, sigma_x=None, p_d=None,
+                        stream=None):
+        import torch
+        d = self.dims
+        f64 = torch.float64
+        if p is None:
+            p = torch.empty(n_scen, self.kkt_len(), dtype=f64, device=r.device)
+        st = self._lib.pf_recover_step(
+            self._h, n_scen, _dev(v, "v", f64, n_scen * d["n_b"]), _dev(theta, "theta", f64, n_scen * d["n_b"]),
+            _dev(p_d, "p_d", f64, n_scen * d["n_b"]), _dev(lam, "lambda", f64, n_scen * d["n_x"]),
+            _dev(y, "y", f64, n_scen * d["m"]), _dev(sigma_s, "sigma_s", f64, n_scen * d["m"]),
+            _dev(sigma_x, "sigma_x", f64, n_scen * d["n_x"]), _dev(r, "r", f64, n_scen * self.kkt_len()),
+            _dev(p_u, "p_u", f64, n_scen * d["n_u"]), _dev(p, "p", f64, n_scen * self.kkt_len()), _stream(stream))
+        self._check(st, "pf_recover_step")
+        return p
+
+    def pf_power_flow(self, n_scen, v, theta, p_g, q_g=None, p_d=None, q_d=None, tol=1e-10, max_iter=20,
+                      stream=None):
+        """Newton power flow in place on (v, theta); returns (iters, resid, info) host arrays."""
+        import torch
+        d = self.dims
+        f64 = torch.float64
+        iters = np.zeros(n_scen, dtype=np.int32)
+        resid = np.zeros(n_scen, dtype=np.float64)
+        info = np.zeros(n_scen, dtype=np.int32)
+        st = self._lib.pf_power_flow(
+            self._h, n_scen, _dev(v, "v", f64, n_scen * d["n_b"]), _dev(theta, "theta", f64, n_scen * d["n_b"]),
+            _dev(p_g, "p_g", f64, n_scen * d["n_g"]), _dev(q_g, "q_g", f64, n_scen * d["n_g"]),
+            _dev(p_d, "p_d", f64, n_scen * d["n_b"]), _dev(q_d, "q_d", f64, n_scen * d["n_b"]), float(tol),
+            int(max_iter), iters.ctypes.data_as(ctypes.c_void_p), resid.ctypes.data_as(ctypes.c_void_p),
+            info.ctypes.data_as(ctypes.c_void_p), _stream(stream))
+        self._check(st, "pf_power_flow")
+        return iters, resid, info
+
+    def pf_reduced_gradient(self, n_scen, v, theta, p_g, y, lam=None, grad=None, p_d=None, stream=None):
+        import torch
+        d = self.dims
+        f64 = torch.float64
+        if grad is None:
+            grad = torch.empty(n_scen, d["n_u"], dtype=f64, device=y.device)
+        st = self._lib.pf_reduced_gradient(
+            self._h, n_scen, _dev(v, "v", f64, n_scen * d["n_b"]), _dev(theta, "theta", f64, n_scen * d["n_b"]),
+            _dev(p_g, "p_g", f64, n_scen * d["n_g"]), _dev(p_d, "p_d", f64, n_scen * d["n_b"]),
+            _dev(y, "y", f64, n_scen * d["m"]), _dev(lam, "lambda", f64, n_scen * d["n_x"]),
+            _dev(grad, "grad", f64, n_scen * d["n_u"]), _stream(stream))
+        self._check(st, "pf_reduced_gradient")
+        return lam, grad

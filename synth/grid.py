@@ -104,8 +104,10 @@ def _multipliers(rng, n_b, n_g, cnt, n_l_lim):
     return dict(lam=lam, y=y, sigma_s=sigma_s, sigma_x=sigma_x, sigma_u=sigma_u)
 
 
-def make_grid(n_b, n_l, n_g, seed, parallel_frac=0.02, tr_frac=0.15, ps_frac=0.01, shunt_frac=0.05):
-    """Build one seeded synthetic network + operating point + multipliers."""
+def make_grid(n_b, n_l, n_g, seed, parallel_frac=0.02, tr_frac=0.15, ps_frac=0.01, shunt_frac=0.05,
+              nolimit_frac=0.0):
+    """Build one seeded synthetic network + operating point + multipliers.
+    nolimit_frac: fraction of lines given F_max = 0 (no limit, no h rows: R23)."""
     rng = np.random.default_rng(seed)
     pts = rng.uniform(size=(n_b, 2))
     tri = Delaunay(pts)
@@ -160,6 +162,8 @@ def make_grid(n_b, n_l, n_g, seed, parallel_frac=0.02, tr_frac=0.15, ps_frac=0.0
     c_quad = rng.uniform(0.01, 0.1, size=n_g) * 100.0 ** 2
     c_lin = rng.uniform(10, 40, size=n_g) * 100.0
     F_max = rng.uniform(2.0, 6.0, size=n_l)
+    if nolimit_frac > 0:
+        F_max[rng.uniform(size=n_l) < nolimit_frac] = 0.0
 
     v, theta = _point(rng, pts, line_from, line_to, gen_bus, ref_bus, n_b)
     p_d = rng.uniform(0.0, 0.6, size=n_b)

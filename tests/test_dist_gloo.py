@@ -58,12 +58,14 @@ def test_allgather_columns_assembles_khat(world, n_u):
 def test_partitions_cover_exactly_once():
     for n_u in (1, 5, 107, 519, 1019, 2889):
         for world in (1, 2, 3, 4, 8):
-            cols = []
-            for r in range(world):
-                c0, n, c = column_partition(n_u, world, r)
-                assert n <= c
-                cols += list(range(c0, c0 + n))
-            assert cols == list(range(n_u))
+            for align in (8, 16, 64):
+                cols = []
+                for r in range(world):
+                    c0, n, c = column_partition(n_u, world, r, align)
+                    assert n <= c and c % align == 0
+                    assert n == 0 or c0 % align == 0   # every rank starts a canonical tile
+                    cols += list(range(c0, c0 + n))
+                assert cols == list(range(n_u))
     for tot in (8, 64, 10):
         for world in (1, 2, 4, 8):
             got = []

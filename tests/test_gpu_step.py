@@ -1,0 +1,237 @@
+"""GPU parity of the NEXT rows through the C-ABI:
+
+* NEXT-1 — pf_condensed_rhs (Theorem 1's r̂ and Theorem 2's right-hand side,
+  R10) and pf_recover_step (Algorithm 1's dual / slack / state / adjoint
+  steps) against the oracle's dense step-by-step formulas (themselves pinned
+  against a direct K_aug solve, tests/test_oracle_pins.py), plus the GPU step's
+  own K_aug residual on the small cases;
+* NEXT-2 — pf_power_flow (Newton–Raphson, Algorithm 2's projection) against
+  the oracle's dense Newton, the 2-bus closed form (P2), the WSCC textbook
+  solution (P17) and constructive exact points of the Table-1 shapes from a
+  flat start; pf_reduced_gradient (λ and ∇f_r) against the oracle.
+Tolerance: 1e-10 relative, normwise per output block (R20); the condensed
+solve's blocks carry cond(K_cond)·ε on top, stated per test."""
+import numpy as np
+import pytest
+
+from oracle import pf_oracle as O
+from synth import case9, make_scenario
+from synth.case9 import case9_multipliers
+from synth.grid import table1_grid
+from tests.gpu_common import TOL, cond2_spd, dev, record, rel_err, stack
+from tests.nets import rich_small, two_bus
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pfmod():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2203_11875_b200 import _build
+    _build.build()
+    import paper_2203_11875_b200 as m
+    return m
+
+
+def _case9_point():
+    net, pt = case9()
+    part = O.partition(net)
+    pt, _, _ = O.newton(net, part, pt)
+    pt.update(case9_multipliers())
+    return net, pt
+
+
+def _cases(name):
+    if name == "case9":
+        net, pt = _case9_point()
+        return net, [pt]
+    if name == "rich8":
+        return rich_small()[0], [rich_small()[1]]
+    net, pt = table1_grid(name)
+    return net, [pt, make_scenario(net, pt, 1)]
+
+
+@pytest.mark.parametrize("name", ["case9", "rich8", "case118", "case1354"])
+def test_condensed_rhs_and_step_recovery(pfmod, name):
+    """NEXT-1 end to end on the device: K̂ (pf_reduced_hessian_batch), b
+    (pf_condensed_rhs), p_u (pf_condensed_kkt_solve), the full step
+    (pf_recover_step) — each vs the oracle's Theorem 1/2 route; on the small
+    cases the GPU step also solves K_aug p = −r to round-off."""
+    import torch
+    net, pts = _cases(name)
+    S = len(pts)
+    part = O.partition(net)
+    n_u, n_x, m = part["n_u"], part["n_x"], part["m"]
+    h = pfmod.Network(net, max_batch=n_u, max_scen=S)
+    L = h.kkt_len()
+    assert L == 2 * n_x + n_u + 2 * m
+    rng = np.random.default_rng(31)
+    r = rng.standard_normal((S, L))
+    v, th = dev(stack(pts, "v")), dev(stack(pts, "theta"))
+    lam, y, ss, sx = (dev(stack(pts, k)) for k in ("lam", "y", "sigma_s", "sigma_x"))
+    pd = dev(stack(pts, "p_d"))
+    info = torch.empty(S, dtype=torch.int32, device="cuda")
+    h.pf_jacobian(S, v, th, info=info)
+    KV = torch.empty(S, n_u, n_u, dtype=torch.float64, device="cuda")
+    h.pf_reduced_hessian_batch(S, v, th, lam, y, KV, sigma_s=ss, sigma_x=sx, p_d=pd)
+    rd = dev(r)
+    b = h.pf_condensed_rhs(S, v, th, lam, y, rd, sigma_s=ss, sigma_x=sx, p_d=pd)
+    torch.cuda.synchronize()
+    Kh = KV.cpu().numpy()
+    bg = b.cpu().numpy()
+    delta = 0.0
+    oracle = []
+    for s, pt in enumerate(pts):
+        Gx, Gu, A = O.jacobians(net, part, pt)
+        W = O.lagrangian_hessian(net, part, pt, pt["lam"], pt["y"])
+        bo, _, _ = O.condensed_rhs(W, Gx, Gu, A, pt["sigma_x"], pt["sigma_s"], r[s])
+        assert rel_err(bg[s], bo) <= TOL, (name, s, rel_err(bg[s], bo))
+        Ksym = 0.5 * (Kh[s] + Kh[s].T)
+        lmin = np.linalg.eigvalsh(Ksym + np.diag(pt["sigma_u"])).min()
+        delta = max(delta, 0.0 if lmin > 0 else -1.5 * lmin + 1.0)
+        oracle.append((W, Gx, Gu, A, bo))
+    K = KV.clone()
+    p_u = b.clone()
+    h.pf_condensed_kkt_solve(S, K, dev(stack(pts, "sigma_u")), delta, p_u, 1, info)
+    p = h.pf_recover_step(S, v, th, lam, y, rd, p_u, sigma_s=ss, sigma_x=sx, p_d=pd)
+    torch.cuda.synchronize()
+    assert info.cpu().tolist() == [0] * S
+    pg = p.cpu().numpy()
+    pug = p_u.cpu().numpy()
+    for s, pt in enumerate(pts):
+        W, Gx, Gu, A, bo = oracle[s]
+        Kc = O.condensed(0.5 * (Kh[s] + Kh[s].T), pt["sigma_u"], delta)
+        c2 = cond2_spd(Kc)
+        puo = np.linalg.solve(Kc, bo)
+        po = O.recover_step(W, Gx, Gu, A, pt["sigma_x"], pt["sigma_s"], r[s], puo)
+        tol = max(TOL, 10 * c2 * np.finfo(float).eps)
+        errs = [rel_err(a, o) for a, o in zip(O.split_kkt(pg[s], n_u, n_x, m), O.split_kkt(po, n_u, n_x, m))]
+        assert np.array_equal(pg[s, :n_u], pug[s])
+        assert max(errs) <= tol, (name, s, errs, tol)
+        rec = dict(case=name, scenario=s, b_rel_err=float(rel_err(bg[s], bo)), cond2_Kcond=c2, tol=tol,
+                   block_rel_err=dict(zip(("p_u", "p_x", "p_s", "p_lambda", "p_y"), map(float, errs))))
+        if n_x <= 300:  # brute force: the GPU step solves K_aug p = −r (δ_w on the uu block)
+            Ka = O.kaug(W, Gx, Gu, A, pt["sigma_u"] + delta, pt["sigma_x"], pt["sigma_s"])
+            res = np.abs(Ka @ pg[s] + r[s]).max() / (np.abs(Ka).max() * np.abs(pg[s]).max() + np.abs(r[s]).max())
+            assert res <= 1e-12, res
+            rec["kaug_backward_err"] = float(res)
+        record("next1_step", **rec)
+    h.close()
+
+
+def test_step_recovery_state_errors(pfmod):
+    """The NEXT-1 calls refuse a point other than the last pf_jacobian's."""
+    import torch
+    net, pts = _cases("case118")
+    h = pfmod.Network(net, max_batch=8, max_scen=1)
+    pt = pts[0]
+    v, th = dev(pt["v"][None]), dev(pt["theta"][None])
+    r = torch.zeros(1, h.kkt_len(), dtype=torch.float64, device="cuda")
+    with pytest.raises(pfmod.PFError) as e:
+        h.pf_condensed_rhs(1, v, th, dev(pt["lam"][None]), dev(pt["y"][None]), r)
+    assert e.value.status == 5
+    h.pf_jacobian(1, v, th)
+    with pytest.raises(pfmod.PFError) as e:
+        h.pf_recover_step(1, v.clone(), th, dev(pt["lam"][None]), dev(pt["y"][None]), r,
+                          torch.zeros(1, h.dims["n_u"], dtype=torch.float64, device="cuda"))
+    assert e.value.status == 5
+    h.close()
+
+
+# ---------------------------------------------------------------------------- NEXT-2
+def test_power_flow_two_bus_closed_form(pfmod):
+    """P2: θ₂ = −½ asin(0.1), v₂ = cos(½ asin 0.1) from a flat start."""
+    import math
+    net, pt = two_bus()
+    pt = dict(pt, p_g=np.array([0.5]))
+    h = pfmod.Network(net, max_batch=1, max_scen=1)
+    v, th = dev(pt["v"][None]), dev(pt["theta"][None])
+    it, res, info = h.pf_power_flow(1, v, th, dev(pt["p_g"][None]), dev(pt["q_g"][None]), dev(pt["p_d"][None]),
+                                    dev(pt["q_d"][None]), tol=1e-12)
+    assert info.tolist() == [0] and res[0] <= 1e-12
+    a = 0.5 * math.asin(0.1)
+    assert abs(th[0, 1].item() + a) <= 1e-12 and abs(v[0, 1].item() - math.cos(a)) <= 1e-12
+    h.close()
+
+
+def test_power_flow_case9_textbook(pfmod):
+    """P17 + O6: from case9's start (generator set points, flat elsewhere) the
+    GPU Newton converges (‖g‖∞ ≤ 1e-10) in the oracle's iteration
+    count to the oracle's solution (1e-10) and to the WSCC textbook values."""
+    net, pt = case9()
+    part = O.partition(net)
+    ref, it_o, _ = O.newton(net, part, pt, tol=1e-10)
+    h = pfmod.Network(net, max_batch=1, max_scen=1)
+    v, th = dev(pt["v"][None]), dev(pt["theta"][None])
+    it, res, info = h.pf_power_flow(1, v, th, dev(pt["p_g"][None]), dev(pt["q_g"][None]), dev(pt["p_d"][None]),
+                                    dev(pt["q_d"][None]), tol=1e-10)
+    assert info.tolist() == [0] and res[0] <= 1e-10
+    assert it[0] == it_o
+    assert rel_err(v[0].cpu().numpy(), ref["v"]) <= 1e-9
+    assert np.abs(th[0].cpu().numpy() - ref["theta"]).max() <= 1e-9
+    thdeg = np.degrees(th[0].cpu().numpy())
+    assert np.allclose(thdeg[1:], [9.280, 4.665, -2.217, -3.687, 1.967, 0.728, 3.720, -3.989], atol=2e-3)
+    assert np.allclose(v[0].cpu().numpy()[3:], [1.0258, 1.0127, 1.0324, 1.0159, 1.0258, 0.9956], atol=2e-4)
+    record("power_flow", case="case9", iters=int(it[0]), oracle_iters=int(it_o), resid=float(res[0]))
+    h.close()
+
+
+@pytest.mark.parametrize("name", ["case118", "case1354", "case2869"])
+def test_power_flow_constructive_points(pfmod, name):
+    """SURVEY §8(d) constructive operating points: loads and dispatch set from
+    the point by the oracle (p_d = −P_i at PQ buses, p_g = P_i at generator
+    buses), so the point x* is an exact power-flow solution; two scenarios
+    from a flat start (θ = 0, v = 1 at PQ buses) converge together to their
+    own x* (1e-9) with ‖g‖∞ ≤ 1e-10, in the oracle's iteration count."""
+    import torch
+    net, base = table1_grid(name)
+    part = O.partition(net)
+    pts, starts = [], []
+    for s, pt in enumerate([base, make_scenario(net, base, 1)]):
+        p, q = O.injections(net, pt["v"], pt["theta"])
+        gb = net["gen_bus"]
+        pd = np.where(part["is_gen"], 0.0, -p)
+        qd = np.where(part["is_gen"], 0.0, -q)
+        pt = dict(pt, p_d=pd, q_d=qd, p_g=p[gb].copy(), q_g=q[gb].copy())
+        assert np.abs(O.g_residual(net, part, pt)).max() <= 1e-12
+        st = dict(pt, v=np.where(part["is_gen"], pt["v"], 1.0), theta=np.zeros(net["n_b"]))
+        pts.append(pt)
+        starts.append(st)
+    h = pfmod.Network(net, max_batch=1, max_scen=2)
+    v, th = dev(stack(starts, "v")), dev(stack(starts, "theta"))
+    it, res, info = h.pf_power_flow(2, v, th, dev(stack(pts, "p_g")), dev(stack(pts, "q_g")), dev(stack(pts, "p_d")),
+                                    dev(stack(pts, "q_d")), tol=1e-10, max_iter=20)
+    torch.cuda.synchronize()
+    assert info.tolist() == [0, 0], (info, res)
+    for s in range(2):
+        _, it_o, _ = O.newton(net, part, starts[s], tol=1e-10)
+        assert res[s] <= 1e-10
+        assert abs(int(it[s]) - it_o) <= 1, (it, it_o)
+        assert np.abs(v[s].cpu().numpy() - pts[s]["v"]).max() <= 1e-9
+        assert np.abs(th[s].cpu().numpy() - pts[s]["theta"]).max() <= 1e-9
+        record("power_flow", case=name, scenario=s, iters=int(it[s]), oracle_iters=int(it_o), resid=float(res[s]))
+    h.close()
+
+
+@pytest.mark.parametrize("name", ["case9", "case118", "case1354"])
+def test_reduced_gradient(pfmod, name):
+    """NEXT-2 adjoint step and reduced gradient vs the oracle (R8)."""
+    import torch
+    net, pts = _cases(name)
+    S = len(pts)
+    part = O.partition(net)
+    h = pfmod.Network(net, max_batch=8, max_scen=S)
+    v, th = dev(stack(pts, "v")), dev(stack(pts, "theta"))
+    h.pf_jacobian(S, v, th)
+    lam = torch.empty(S, part["n_x"], dtype=torch.float64, device="cuda")
+    _, g = h.pf_reduced_gradient(S, v, th, dev(stack(pts, "p_g")), dev(stack(pts, "y")), lam=lam,
+                                 p_d=dev(stack(pts, "p_d")))
+    torch.cuda.synchronize()
+    for s, pt in enumerate(pts):
+        lo, go = O.reduced_gradient(net, part, pt, pt["y"])
+        assert rel_err(lam[s].cpu().numpy(), lo) <= TOL
+        assert rel_err(g[s].cpu().numpy(), go) <= TOL
+        record("reduced_gradient", case=name, scenario=s, lam_rel_err=float(rel_err(lam[s].cpu().numpy(), lo)),
+               grad_rel_err=float(rel_err(g[s].cpu().numpy(), go)))
+    h.close()

@@ -40,6 +40,8 @@ def _nets():
     out.append(("case118",) + table1_grid("case118"))
     out.append(("case300",) + table1_grid("case300"))
     out.append(("case1354",) + table1_grid("case1354"))
+    out.append(("case2869",) + table1_grid("case2869"))   # the benchmarked shapes (configs 3 and 4/5)
+    out.append(("case9241",) + table1_grid("case9241"))
     return out
 
 

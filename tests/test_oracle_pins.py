@@ -223,6 +223,23 @@ def test_reduced_hessian_fd_through_newton():
     assert np.max(np.abs(Kh - Kh.T)) <= 1e-12 * np.abs(Kh).max()   # P12
 
 
+def test_reduced_gradient_fd_through_newton():
+    """NEXT-2 pin: the adjoint-based reduced gradient equals the central
+    finite difference of φ(u) = f + yᵀ[r; h] at x(u) from Newton (the reduced
+    objective + constraint term), and λ satisfies the adjoint
+    equation G_xᵀλ = −∇_x(f + yᵀ[r;h]) (Algorithm 2)."""
+    net, part, pt, lam0, y, _ = _case9_solved()
+    lam, g = O.reduced_gradient(net, part, pt, y)
+    assert np.abs(lam - lam0).max() <= 1e-12 * np.abs(lam0).max()
+    u0 = O.get_u(part, pt)
+    h = 1e-5
+    fd = np.zeros_like(u0)
+    for i in range(len(u0)):
+        e = np.zeros_like(u0); e[i] = h
+        fd[i] = (O.reduced_value(net, part, pt, y, u0 + e) - O.reduced_value(net, part, pt, y, u0 - e)) / (2 * h)
+    assert np.abs(g - fd).max() <= 1e-6 * np.abs(g).max()
+
+
 def test_reduced_jacobian_term_fd():
     """P9 second part: K̂(σ_s) − K̂(0) = Â_uᵀΣ_sÂ_u with Â_u = ∂[r;h](x(u),u)/∂u by FD through Newton."""
     net, part, pt, lam, y, mult = _case9_solved()
@@ -254,6 +271,53 @@ def test_schur_pin_case9():
     n_u = part["n_u"]
     ref = np.linalg.inv(Kc)
     assert np.max(np.abs(inv[:n_u, :n_u] - ref)) <= 1e-9 * np.abs(ref).max()
+
+
+def _next1_problem(name, seed=0):
+    """A LinRed iteration's linear algebra on a small instance: W, G_x, G_u, A,
+    Σ's, a random right-hand side r and the condensed matrix (δ_w making it PD)."""
+    if name == "case9":
+        net, part, pt, lam, y, mult = _case9_solved()
+    else:
+        net, pt = rich_small(seed=5 + seed) if name == "rich8" else table1_grid(name)
+        part = O.partition(net)
+        lam, y, mult = pt["lam"], pt["y"], pt
+    Gx, Gu, A = O.jacobians(net, part, pt)
+    W = O.lagrangian_hessian(net, part, pt, lam, y)
+    K = O.kkt_K(net, part, pt, lam, y, mult["sigma_s"], mult["sigma_x"])
+    Kh = O.reduce_naive(K, Gx, Gu)
+    lmin = np.linalg.eigvalsh(O.condensed(Kh, mult["sigma_u"], 0.0)).min()
+    delta = 0.0 if lmin > 0 else -2 * lmin + 1.0
+    n_u, n_x, m = part["n_u"], part["n_x"], part["m"]
+    r = np.random.default_rng(100 + seed).standard_normal(2 * n_x + n_u + 2 * m)
+    return dict(W=W, Gx=Gx, Gu=Gu, A=A, Kh=Kh, su=mult["sigma_u"], sx=mult["sigma_x"], ss=mult["sigma_s"],
+                delta=delta, r=r, n_u=n_u, n_x=n_x, m=m)
+
+
+@pytest.mark.parametrize("name,seed", [("case9", 0), ("rich8", 0), ("rich8", 1), ("case118", 0)])
+def test_step_recovery_vs_kaug(name, seed):
+    """NEXT-1 pin (SURVEY §8(f), S:L356/361/391): the condensed route —
+    Theorem 1's r̂ and Theorem 2's K_cond p_u = b (R10 signs), then Algorithm 1's
+    dual/slack/state/adjoint steps — equals the direct dense solve of
+    K_aug p = −r (eq. kktmatrix:normal) in all five blocks, with
+    δ_w added to the uu block; and the r̂₂ sign as printed does not."""
+    P = _next1_problem(name, seed)
+    n_u = P["n_u"]
+    b, (rh1, rh2, rh3), Ahat = O.condensed_rhs(P["W"], P["Gx"], P["Gu"], P["A"], P["sx"], P["ss"], P["r"])
+    Kc = O.condensed(P["Kh"], P["su"], P["delta"])
+    p_u = np.linalg.solve(Kc, b)
+    got = O.recover_step(P["W"], P["Gx"], P["Gu"], P["A"], P["sx"], P["ss"], P["r"], p_u)
+    Ka = O.kaug(P["W"], P["Gx"], P["Gu"], P["A"], P["su"] + P["delta"], P["sx"], P["ss"])
+    ref = -np.linalg.solve(Ka, P["r"])
+    assert np.abs(got - ref).max() <= 1e-8 * np.abs(ref).max()
+    for blk_got, blk_ref in zip(O.split_kkt(got, n_u, P["n_x"], P["m"]), O.split_kkt(ref, n_u, P["n_x"], P["m"])):
+        assert np.abs(blk_got - blk_ref).max() <= 1e-8 * max(np.abs(blk_ref).max(), 1e-300)
+    # K_cond = Ŵ_uu + Σ_u + Â_uᵀΣ_sÂ_u (Theorem 2 with R9): the oracle's K̂ carries Â_uᵀΣ_sÂ_u
+    Kc0 = O.condensed(O.reduce_naive(O.kkt_K_from(P["W"], P["A"], None, P["sx"], P["n_u"]), P["Gx"], P["Gu"]),
+                      P["su"], P["delta"])
+    assert np.abs(Kc0 + Ahat.T @ np.diag(P["ss"]) @ Ahat - Kc).max() <= 1e-10 * np.abs(Kc).max()
+    printed = -(rh1 + Ahat.T @ (P["ss"] * rh3) - Ahat.T @ rh2)   # the sign printed in P:L787
+    assert np.abs(np.linalg.solve(Kc, printed) - ref[:n_u]).max() > 1e-6 * np.abs(ref[:n_u]).max()
 
 
 def test_inertia_theorem3():
@@ -322,6 +386,193 @@ def test_naive_vs_adjoint_routes(N):
     V = rng.standard_normal((part["n_u"], N))
     KV = O.reduce_adjoint(K, Gx, Gu.toarray(), V)
     assert np.max(np.abs(KV - Kh @ V)) <= 1e-11 * np.abs(Kh @ V).max()
+
+
+def _khat_inputs(name):
+    if name == "case9":
+        net, part, pt, lam, y, mult = _case9_solved()
+        K = O.kkt_K(net, part, pt, lam, y, mult["sigma_s"], mult["sigma_x"])
+    else:
+        net, pt = table1_grid(name)
+        part = O.partition(net)
+        K = O.kkt_K(net, part, pt, pt["lam"], pt["y"], pt["sigma_s"], pt["sigma_x"])
+    Gx, Gu, _ = O.jacobians(net, part, pt)
+    return K, Gx, Gu, part
+
+
+def test_reduce_columns_vs_dense_adjoint_case9():
+    """reduce_columns (sparse SuperLU solves, the full-size checker) against
+    reduce_adjoint (dense LAPACK solves) and reduce_naive on case9, all n_u
+    unit directions (P8 with a different solve primitive)."""
+    K, Gx, Gu, part = _khat_inputs("case9")
+    n_u = part["n_u"]
+    got = O.reduce_columns(K, Gx, Gu, np.arange(n_u))
+    dense = O.reduce_adjoint(K, Gx, Gu.toarray(), np.eye(n_u))
+    naive = O.reduce_naive(K, Gx, Gu)
+    assert np.abs(got - dense).max() <= 1e-13 * np.abs(dense).max()
+    assert np.abs(got - naive).max() <= 1e-12 * np.abs(naive).max()
+
+
+@pytest.mark.parametrize("name", ["case118", "case1354"])
+@pytest.mark.parametrize("kind", ["colamd", "mmd", "static"])
+def test_reduce_columns_vs_naive(name, kind):
+    """reduce_columns (adjoint route) with each sparse-LU variant
+    vs reduce_naive (sensitivity route): whole K̂ normwise ≤ 1e-10,
+    every column ≤ 1e-8 (independent LU codes disagree per column up to ~3e-10
+    at 1354, R20), and a scattered column subset equals the same columns of
+    the full run (columns are independent)."""
+    K, Gx, Gu, part = _khat_inputs(name)
+    n_u = part["n_u"]
+    perm = None
+    if kind == "static":
+        net, _ = table1_grid(name)
+        perm, _ = O.permutation(part, O.md_ordering(net, part))
+    full = O.reduce_columns(K, Gx, Gu, np.arange(n_u), kind, perm)
+    naive = O.reduce_naive(K, Gx, Gu)
+    assert np.abs(full - naive).max() <= 1e-10 * np.abs(naive).max()
+    col = np.abs(full - naive).max(axis=0) / np.abs(naive).max(axis=0)
+    assert col.max() <= 1e-8, col.max()
+    cols = np.array([n_u - 1, 3, n_u // 2, 0])
+    sub = O.reduce_columns(K, Gx, Gu, cols, kind, perm)
+    assert np.abs(sub - full[:, cols]).max() <= 1e-14 * np.abs(full).max()
+
+
+def test_static_sparse_lu_is_r18():
+    """SparseLU("static") is the R18 factorization: SuperLU keeps the natural
+    order and the diagonal pivots of P G_x Pᵀ, and its U equals the dense
+    no-pivot LU (static_lu) of the same matrix."""
+    net, pt = table1_grid("case118")
+    part = O.partition(net)
+    Gx, _, _ = O.jacobians(net, part, pt)
+    perm, _ = O.permutation(part, O.md_ordering(net, part))
+    lu = O.SparseLU(Gx, "static", perm)
+    info, LU = O.static_lu(Gx, perm)
+    assert info == 0
+    U = np.triu(LU)
+    assert np.abs(lu.lu.U.toarray() - U).max() <= 1e-13 * np.abs(U).max()
+    b = np.random.default_rng(1).standard_normal(len(perm))
+    assert np.abs(Gx @ lu.solve(b) - b).max() <= 1e-12 * np.abs(b).max()
+    assert np.abs(Gx.T @ lu.solve(b, trans="T") - b).max() <= 1e-12 * np.abs(b).max()
+
+
+def _ybus_loop(net):
+    """Y_bus by the plain per-line accumulation (a third formulation)."""
+    Y = {}
+    def add(i, j, v):
+        Y[(i, j)] = Y.get((i, j), 0.0) + v
+    for i in range(int(net["n_b"])):
+        add(i, i, net["Y_sh"][i])
+    for l in range(int(net["n_l"])):
+        f, t = int(net["line_from"][l]), int(net["line_to"][l])
+        add(f, f, net["Y_ff"][l]); add(f, t, net["Y_ft"][l])
+        add(t, f, net["Y_tf"][l]); add(t, t, net["Y_tt"][l])
+    return Y
+
+
+@pytest.mark.parametrize("name", ["case118", "case1354"])
+def test_ybus_sparse_branch(name):
+    """The sparse-storage branch of ybus_entries (taken above 3000 buses, i.e.
+    by every case9241 oracle call) forced on smaller grids: same pattern and
+    values as the dense branch and as a per-line accumulation."""
+    net, _ = table1_grid(name)
+    i0, j0, y0 = O.ybus_entries(net)                 # dense product
+    i1, j1, y1 = O.ybus_entries(net, dense_max=0)    # sparse product
+    assert np.array_equal(i0, i1) and np.array_equal(j0, j1)
+    assert np.abs(y0 - y1).max() <= 1e-13 * np.abs(y0).max()
+    Y = _ybus_loop(net)
+    assert len(Y) == len(i1)
+    ref = np.array([Y[(int(a), int(b))] for a, b in zip(i1, j1)])
+    assert np.abs(ref - y1).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_static_lu_pins():
+    """R18 numeric rule: no pivoting, first failing pivot k → k+1.
+    Hand cases: regular; exact cancellation (u_22 = 0); a zero leading pivot
+    that partial pivoting would swap away; the 1e-12 row-relative threshold on
+    both sides; a NaN; LU reproduces PAPᵀ; and on case118's G_x with the R18
+    ordering the factors solve like LAPACK."""
+    I2 = np.arange(2)
+    assert O.static_lu(np.array([[1.0, 2.0], [3.0, 4.0]]), I2)[0] == 0
+    assert O.static_lu(np.array([[1.0, 2.0], [2.0, 4.0]]), I2)[0] == 2
+    assert O.static_lu(np.array([[0.0, 1.0], [1.0, 0.0]]), I2)[0] == 1
+    assert O.static_lu(np.array([[0.5e-12, 1.0], [1.0, 1.0]]), I2)[0] == 1
+    assert O.static_lu(np.array([[2e-12, 1.0], [1.0, 1.0]]), I2)[0] == 0
+    assert O.static_lu(np.array([[1.0, 0.0], [0.0, np.nan]]), I2)[0] == 2
+    assert O.static_lu(np.array([[1.0, 2.0], [3.0, 4.0]]), np.array([1, 0]))[0] == 0
+    rng = np.random.default_rng(3)
+    M = rng.standard_normal((6, 6)) + 6 * np.eye(6)
+    p = rng.permutation(6)
+    info, LU = O.static_lu(M, p)
+    assert info == 0
+    L, U = np.tril(LU, -1) + np.eye(6), np.triu(LU)
+    assert np.abs(L @ U - M[np.ix_(p, p)]).max() <= 1e-14 * np.abs(M).max()
+    net, pt = table1_grid("case118")
+    part = O.partition(net)
+    Gx, _, _ = O.jacobians(net, part, pt)
+    perm, _ = O.permutation(part, O.md_ordering(net, part))
+    info, LU = O.static_lu(Gx, perm)
+    assert info == 0
+    n = len(perm)
+    L, U = np.tril(LU, -1) + np.eye(n), np.triu(LU)
+    b = rng.standard_normal(n)
+    z = np.zeros(n)
+    z[perm] = np.linalg.solve(U, np.linalg.solve(L, b[perm]))
+    assert np.abs(Gx @ z - b).max() <= 1e-12 * np.abs(b).max()
+    assert np.allclose(z, np.linalg.solve(Gx.toarray(), b), rtol=0, atol=1e-9 * np.abs(z).max())
+
+
+# --------------------------------------------------------------------- P15 structure pins
+def _line_net(n_b, edges, gen_bus, ref_bus):
+    Yff, Yft, Ytf, Ytt = pi_model(np.zeros(len(edges)), np.full(len(edges), 0.1), np.zeros(len(edges)),
+                                  np.ones(len(edges)), np.zeros(len(edges)))
+    e = np.array(edges, dtype=np.int32)
+    return dict(n_b=n_b, n_l=len(edges), n_g=len(gen_bus), line_from=e[:, 0], line_to=e[:, 1],
+                Y_ff=Yff, Y_ft=Yft, Y_tf=Ytf, Y_tt=Ytt, Y_sh=np.zeros(n_b, complex),
+                gen_bus=np.array(gen_bus, np.int32), ref_bus=ref_bus, p_d=np.zeros(n_b), q_d=np.zeros(n_b),
+                F_max=np.ones(len(edges)), c_quad=np.ones(len(gen_bus)), c_lin=np.ones(len(gen_bus)))
+
+
+def test_md_ordering_hand_cases():
+    """R18's written rule worked by hand: minimum current degree on the bus
+    graph without the reference bus, ties to the lowest bus index, eliminated
+    buses join their neighbours into a clique.
+    Path 0-1-2-3-4 (ref 4): degrees 1,2,2,1 → 0 (tie with 3), then 1, 2, 3.
+    Star centre 2, leaves 0,1,3,4 (ref 0): 1, 3, then 2 (tie with 4), 4.
+    Ring 0..4 + ref 5 on bus 0: all degree 2 → 0; its neighbours 1, 4 join;
+    all degree 2 again → 1, then 2, 3, 4."""
+    cases = [(_line_net(5, [(0, 1), (1, 2), (2, 3), (3, 4)], [4], 4), [0, 1, 2, 3]),
+             (_line_net(5, [(2, 0), (2, 1), (2, 3), (2, 4)], [0], 0), [1, 3, 2, 4]),
+             (_line_net(6, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 0), (5, 0)], [5], 5), [0, 1, 2, 3, 4])]
+    for net, want in cases:
+        part = O.partition(net)
+        assert O.md_ordering(net, part).tolist() == want
+
+
+@pytest.mark.parametrize("name", ["case9", "rich8", "case118"])
+def test_patterns_match_numeric_jacobians(name):
+    """The structural (topological, R19) CSR patterns of G_x, G_u and A contain
+    exactly the nonzeros of the numeric Jacobians at a generic point (no
+    structural zero is dropped, no spurious entry): patterns by graph walks vs
+    values by closed-form derivatives."""
+    if name == "case9":
+        net, pt = case9()
+    elif name == "rich8":
+        net, pt = rich_small()
+    else:
+        net, pt = table1_grid(name)
+    part = O.partition(net)
+    rng = np.random.default_rng(9)   # a generic point (case9's is flat: r = 0 transformers give exact zeros)
+    pt = dict(pt, v=pt["v"] + 0.05 * rng.uniform(size=net["n_b"]),
+              theta=pt["theta"] + 0.1 * rng.uniform(size=net["n_b"]))
+    pt["theta"][net["ref_bus"]] = 0.0
+    Gx, Gu, A = O.jacobians(net, part, pt)
+    (px, ix), (pu, iu) = O.gx_gu_patterns(net, part)
+    pa, ia = O.a_pattern(net, part)
+    for M, ptr, idx in ((Gx, px, ix), (Gu, pu, iu), (A, pa, ia)):
+        D = np.asarray(sp.csr_matrix(M).toarray())
+        P = np.zeros(D.shape, dtype=bool)
+        P[np.repeat(np.arange(D.shape[0]), np.diff(ptr)), idx] = True
+        assert np.array_equal(P, D != 0)
 
 
 # --------------------------------------------------------------------- P13 Cholesky
