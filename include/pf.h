@@ -215,7 +215,8 @@ pf_status pf_reduced_hessian_batch(pf_net *net, int32_t n_scen,
  * role in P:L1339–1341; success certifies the inertia, Theorem 3
  * P:L856–866) and the solve L Lᵀ p = b.
  *   K: [n_scen][n_u][n_u] column-major; in K̂, out L in the lower triangle
- *   (strict upper triangle zeroed);
+ *   (strict upper triangle zeroed) — for the scenarios that factorized; a
+ *   scenario whose factorization failed keeps its K̂ (so it can be retried);
  *   sigma_u: [n_scen][n_u] or NULL;  delta_w: scalar shift;
  *   rhs: [n_scen][nrhs][n_u]; in b, out K_cond^{-1} b (untouched for a
  *   scenario whose factorization failed); nrhs >= 0;
@@ -300,6 +301,32 @@ pf_status pf_reduced_gradient(pf_net *net, int32_t n_scen, const double *v,
                               const double *p_d, const double *y,
                               double *lambda, double *grad, void *stream);
 
+/*
+ * ---- NEXT-3: inertia-correcting regularization ----
+ * pf_condensed_kkt_solve_reg — pf_condensed_kkt_solve inside the paper's
+ * regularization loop ("if the factorization fails, we apply
+ * a primal regularization δ_w and refactorize"; Theorem 3: the
+ * Cholesky succeeds iff K_cond is positive definite iff K_aug has the
+ * inertia (n_x+n_u+m, n_x+m, 0), so success certifies a descent direction).
+ * Trial 1 factorizes every scenario with δ_w = delta_init; a scenario that
+ * fails is retried with δ_w = delta_first (if its δ_w was 0) or growth × its
+ * δ_w, while that stays ≤ delta_max.  Each retry factorizes all failed
+ * scenarios of the call at once (one DAG launch per trial, the others
+ * untouched).  Arguments as pf_condensed_kkt_solve; delta_init ≥ 0,
+ * delta_first > 0, growth > 1, delta_max ≥ delta_init.
+ *   out [host] delta_out [n_scen]: the δ_w of the last trial (the accepted one
+ *   when info = 0); trials [n_scen]: factorizations attempted; info [n_scen]:
+ *   0, or the last trial's first failing column + 1.  Each may be NULL.
+ * Synchronizes the stream once per trial (not graph-capturable).
+ */
+pf_status pf_condensed_kkt_solve_reg(pf_net *net, int32_t n_scen, double *K,
+                                     const double *sigma_u, double delta_init,
+                                     double delta_first, double growth,
+                                     double delta_max, double *rhs,
+                                     int32_t nrhs, double *delta_out,
+                                     int32_t *trials, int32_t *info,
+                                     void *stream);
+
 /* Number of kernels this handle has launched so far (bench evidence). */
 int64_t pf_launch_count(const pf_net *net);
 
@@ -308,8 +335,9 @@ int64_t pf_launch_count(const pf_net *net);
  * compute calls record CUDA events on their stream around the hot kernels;
  * pf_kernel_times writes the last calls' per-kernel milliseconds, in the
  * order k_fwd, k_mu, k_hvp, k_adj (pf_reduced_hessian_batch), k_lu
- * (pf_jacobian) and k_proj (pf_reduced_hessian_batch), synchronizing on the
- * events; returns how many were written (0 when profiling is off; at most 6).
+ * (pf_jacobian), k_proj (pf_reduced_hessian_batch) and k_chol_dag
+ * (pf_condensed_kkt_solve[_reg], its first trial), synchronizing on the
+ * events; returns how many were written (0 when profiling is off; at most 7).
  */
 pf_status pf_profile(pf_net *net, int32_t enable);
 int32_t pf_kernel_times(pf_net *net, float *ms /* [host] cap */, int32_t cap);

@@ -518,6 +518,24 @@ def cholesky(Kc):
     return L, 0
 
 
+def regularized_cholesky(Kc0, delta_init, delta_first, growth, delta_max):
+    """NEXT-3, the paper's inertia correction: factorize
+    K_cond + δ_w I with δ_w = delta_init; while the Cholesky fails, δ_w ←
+    delta_first (from 0) or growth·δ_w, up to delta_max.  Success certifies
+    the inertia of K_aug (Theorem 3).
+    Returns (δ_w of the last trial, trials, info, L)."""
+    n = Kc0.shape[0]
+    delta, trials = delta_init, 1
+    L, info = cholesky(Kc0 + delta * np.eye(n))
+    while info:
+        nd = delta_first if delta == 0.0 else delta * growth
+        if nd > delta_max:
+            break
+        delta, trials = nd, trials + 1
+        L, info = cholesky(Kc0 + delta * np.eye(n))
+    return delta, trials, info, L
+
+
 def chol_solve(L, b):
     """Solve L Lᵀ p = b by forward then backward substitution."""
     n = L.shape[0]
@@ -624,7 +642,7 @@ def adjoint_multipliers(net, part, point, y):
     Gx, _, A = jacobians(net, part, point)
     n_u = part["n_u"]
     grad = objective_gradient(net, part, point) + A.T @ y
-    return np.linalg.solve(Gx.toarray().T, -grad[n_u:])
+    return spla.splu(sp.csc_matrix(Gx)).solve(-grad[n_u:], trans="T")
 
 
 def reduced_gradient(net, part, point, y):
@@ -635,7 +653,7 @@ def reduced_gradient(net, part, point, y):
     Gx, Gu, A = jacobians(net, part, point)
     n_u = part["n_u"]
     grad = objective_gradient(net, part, point) + A.T @ y
-    lam = -np.linalg.solve(Gx.toarray().T, grad[n_u:])
+    lam = -spla.splu(sp.csc_matrix(Gx)).solve(grad[n_u:], trans="T")
     return lam, grad[:n_u] + Gu.T @ lam
 
 

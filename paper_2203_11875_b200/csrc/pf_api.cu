@@ -34,7 +34,7 @@ struct pf_net {
   std::vector<int4> u_top, u_bot, ua_top, ua_bot;
   std::vector<int> u_top_ptr, u_bot_ptr, ua_top_ptr, ua_bot_ptr;
   std::vector<int> hvp_order;  // k_hvp bus order (elimination-forest postorder)
-  cudaEvent_t ev[8] = {};    // [0..4] k_fwd/k_mu/k_hvp/k_adj, [5..6] k_lu, [4..7] k_proj
+  cudaEvent_t ev[10] = {};   // [0..4] k_fwd/k_mu/k_hvp/k_adj, [5..6] k_lu, [4..7] k_proj, [8..9] k_chol_dag
 };
 
 #ifndef PF_P1_IMB
@@ -397,7 +397,8 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
        alloc(h, S * chol_tile_doubles(d.n_u), &w.ctile) && alloc(h, S * chol_flag_ints(d.n_u), &w.cflag) &&
        alloc(h, 1 + 1024, &w.cticket) && alloc(h, S * chol_vec_doubles(d.n_u), &w.cy) &&
        alloc(h, S * d.nnz_a, &w.aval) && alloc(h, S * (d.n_u + d.n_x + d.m), &w.zero) &&
-       alloc(h, S * 2 * d.n_b, &w.gbuf) && alloc(h, S, &w.res) && alloc(h, S, &w.active);
+       alloc(h, S * 2 * d.n_b, &w.gbuf) && alloc(h, S, &w.res) && alloc(h, S, &w.active) &&
+       alloc(h, S, &w.csidx) && alloc(h, S, &w.cdelta);
   ok = ok && cudaMemset(w.zero, 0, S * (d.n_u + d.n_x + d.m) * sizeof(double)) == cudaSuccess;
   if (!ok) {
     g_build_err = std::string("device allocation/upload failed: ") + cudaGetErrorString(cudaGetLastError());
@@ -524,7 +525,7 @@ pf_status pf_condensed_kkt_solve(pf_net* h, int32_t n_scen, double* K, const dou
   if (n_scen > h->max_scen) { h->err = "pf_condensed_kkt_solve: n_scen > max_scen"; return PF_ERR_CAPACITY; }
   if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
   h->launches += launch_chol(h->dn, h->w, n_scen, K, sigma_u, delta_w, rhs, nrhs, info, h->w.info + h->max_scen,
-                             (cudaStream_t)stream, h->chol_grid);
+                             (cudaStream_t)stream, h->chol_grid, nullptr, nullptr, h->prof ? h->ev + 8 : nullptr);
   return cuda_check(h, "pf_condensed_kkt_solve");
 }
 
@@ -638,6 +639,61 @@ pf_status pf_power_flow(pf_net* h, int32_t n_scen, double* v, double* theta, con
   return PF_OK;
 }
 
+// ---------------------------------------------------------------- NEXT-3
+pf_status pf_condensed_kkt_solve_reg(pf_net* h, int32_t n_scen, double* K, const double* sigma_u, double delta_init,
+                                     double delta_first, double growth, double delta_max, double* rhs, int32_t nrhs,
+                                     double* delta_out, int32_t* trials, int32_t* info, void* stream) {
+  if (!h) return PF_ERR_ARG;
+  if (!K || n_scen < 1 || nrhs < 0 || (nrhs > 0 && !rhs) || !(delta_init >= 0.0) || !(delta_first > 0.0) ||
+      !(growth > 1.0) || !(delta_max >= delta_init)) {
+    h->err = "pf_condensed_kkt_solve_reg: bad argument";
+    return PF_ERR_ARG;
+  }
+  if (n_scen > h->max_scen) { h->err = "pf_condensed_kkt_solve_reg: n_scen > max_scen"; return PF_ERR_CAPACITY; }
+  if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  int* info_ws = h->w.info + h->max_scen;
+  std::vector<double> delta(n_scen, delta_init);
+  std::vector<int> tr(n_scen, 1), inf(n_scen, 0), idx, got(n_scen);
+  // trial 1: every scenario at δ_init
+  h->launches += launch_chol(h->dn, h->w, n_scen, K, sigma_u, delta_init, rhs, nrhs, nullptr, info_ws, st,
+                             h->chol_grid, nullptr, nullptr, h->prof ? h->ev + 8 : nullptr);
+  if (cudaMemcpyAsync(inf.data(), info_ws, n_scen * sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return cuda_check(h, "pf_condensed_kkt_solve_reg");
+  for (;;) {
+    // next trial: the failed scenarios whose next δ_w stays within δ_max (K̂ and rhs were left untouched)
+    idx.clear();
+    std::vector<double> dv;
+    for (int s = 0; s < n_scen; ++s) {
+      if (!inf[s]) continue;
+      const double nd = delta[s] == 0.0 ? delta_first : delta[s] * growth;
+      if (nd > delta_max) continue;
+      delta[s] = nd;
+      ++tr[s];
+      idx.push_back(s);
+      dv.push_back(nd);
+    }
+    if (idx.empty()) break;
+    const int nv = (int)idx.size();
+    if (cudaMemcpyAsync(h->w.csidx, idx.data(), nv * sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(h->w.cdelta, dv.data(), nv * sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return cuda_check(h, "pf_condensed_kkt_solve_reg");
+    h->launches += launch_chol(h->dn, h->w, nv, K, sigma_u, 0.0, rhs, nrhs, nullptr, info_ws, st, h->chol_grid,
+                               h->w.csidx, h->w.cdelta);
+    if (cudaMemcpyAsync(got.data(), info_ws, nv * sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return cuda_check(h, "pf_condensed_kkt_solve_reg");
+    for (int v = 0; v < nv; ++v) inf[idx[v]] = got[v];
+  }
+  for (int s = 0; s < n_scen; ++s) {
+    if (delta_out) delta_out[s] = delta[s];
+    if (trials) trials[s] = tr[s];
+    if (info) info[s] = inf[s];
+  }
+  return cuda_check(h, "pf_condensed_kkt_solve_reg");
+}
+
 #ifdef PF_LU_TRACE  // debug builds only (tools/lu_trace.py)
 int pf_debug_set_lu_trace(void* dev_ptr) {
   pf::set_lu_trace(static_cast<unsigned long long*>(dev_ptr));
@@ -657,9 +713,9 @@ pf_status pf_profile(pf_net* h, int32_t enable) {
 
 int32_t pf_kernel_times(pf_net* h, float* ms, int32_t cap) {
   if (!h || !h->prof || !ms) return 0;
-  const int pairs[6][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {5, 6}, {4, 7}};
+  const int pairs[7][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {5, 6}, {4, 7}, {8, 9}};
   int k = 0;
-  for (; k < 6 && k < cap; ++k) {
+  for (; k < 7 && k < cap; ++k) {
     float t = -1.0f;
     if (cudaEventSynchronize(h->ev[pairs[k][1]]) == cudaSuccess &&
         cudaEventElapsedTime(&t, h->ev[pairs[k][0]], h->ev[pairs[k][1]]) != cudaSuccess)

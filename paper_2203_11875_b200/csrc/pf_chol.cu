@@ -56,6 +56,7 @@ struct DagArgs {
   double* cy;      // [S][2][kRhsCap][nt*64]  y (forward) and p (backward), padded
   double* rhs;     // [S][rhs_ld][n], already offset to the first vector of this run
   int* crit;       // [kMaxSm] per-SM count of critical-path tasks in their triangular phase
+  const int* sidx; // [S] caller scenario of each (virtual) scenario s, or null = identity (rhs indexing)
 };
 constexpr int kMaxSm = 1024;
 #ifndef PF_CHOL_LOOK
@@ -118,18 +119,21 @@ __device__ __forceinline__ void record_fail(int* info, int code) {
 
 // sym + shift + pack: tile (I, J), I ≥ J, of scenario s, in two 32-column
 // halves; the tile and its mirror are both read down their columns (coalesced).
+// sidx (optional): caller scenario of virtual scenario s; dvec (optional): per-scenario δ_w.
 __global__ void __launch_bounds__(256) k_chol_pack(int n, int nt, const double* __restrict__ K,
                                                    const double* __restrict__ sig_u, double delta,
                                                    double* __restrict__ tiles, int* __restrict__ flags,
                                                    int* __restrict__ ticket, int* __restrict__ info,
-                                                   int* __restrict__ crit) {
+                                                   int* __restrict__ crit, const int* __restrict__ sidx,
+                                                   const double* __restrict__ dvec) {
   __shared__ double a[32][NB + 1];  // a[c][r] = K(R, C)
   __shared__ double b[NB][33];      // b[r][c] = K(C, R)  (mirror)
-  const int s = blockIdx.y, ntri = nt * (nt + 1) / 2;
+  const int s = blockIdx.y, ntri = nt * (nt + 1) / 2, sr = sidx ? sidx[s] : s;
+  if (dvec) delta = dvec[s];
   int J = 0, t = blockIdx.x;
   while (t >= nt - J) { t -= nt - J; ++J; }
   const int I = J + t;
-  const double* A = K + (size_t)s * n * n;
+  const double* A = K + (size_t)sr * n * n;
   double* T = tiles + ((size_t)s * ntri + tidx(nt, I, J)) * TILE_D;
   for (int ch = 0; ch < NB; ch += 32) {
     {
@@ -153,7 +157,7 @@ __global__ void __launch_bounds__(256) k_chol_pack(int n, int nt, const double* 
       double v;
       if (R >= n || C >= n) v = (R == C) ? 1.0 : 0.0;  // identity padding
       else if (R > C) v = 0.5 * (a[c][tx] + b[tx][c]);
-      else if (R == C) v = a[c][tx] + (sig_u ? sig_u[(size_t)s * n + R] : 0.0) + delta;
+      else if (R == C) v = a[c][tx] + (sig_u ? sig_u[(size_t)sr * n + R] : 0.0) + delta;
       else v = 0.0;
       T[(ch + c) * LDT + tx] = v;
     }
@@ -170,11 +174,14 @@ __global__ void __launch_bounds__(256) k_chol_pack(int n, int nt, const double* 
     for (int k = threadIdx.x; k < kMaxSm; k += blockDim.x) crit[k] = 0;
 }
 
-// L back into K: lower (incl. diagonal) from the tiles, strict upper zeroed.
+// L back into K: lower (incl. diagonal) from the tiles, strict upper zeroed — only for the
+// scenarios that factorized (a failed one keeps its K̂, so a caller can retry with a larger δ_w).
 __global__ void __launch_bounds__(256) k_chol_unpack(int n, int nt, const double* __restrict__ tiles,
-                                                     double* __restrict__ K) {
+                                                     double* __restrict__ K, const int* __restrict__ info,
+                                                     const int* __restrict__ sidx) {
   const int s = blockIdx.z, I = blockIdx.x, J = blockIdx.y, ntri = nt * (nt + 1) / 2;
-  double* A = K + (size_t)s * n * n;
+  if (info[s] != 0) return;
+  double* A = K + (size_t)(sidx ? sidx[s] : s) * n * n;
   const double* T = I >= J ? tiles + ((size_t)s * ntri + tidx(nt, I, J)) * TILE_D : nullptr;
   const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
   for (int c = ty; c < NB; c += 4) {
@@ -551,7 +558,7 @@ __device__ void cons_fwd(const TaskCtx& t, Pipe& p, double* sm, double* red, dou
   if (tid < NB) rdv[tid] = 1.0 / Ls[tid * LDT + tid];
   for (int idx = tid; idx < a.nrhs * NB; idx += kCons) {
     const int rr = idx >> 6, r = idx & 63, R = j * NB + r;
-    const double b = R < a.n ? a.rhs[((size_t)t.s * a.rhs_ld + rr) * a.n + R] : 0.0;
+    const double b = R < a.n ? a.rhs[((size_t)(a.sidx ? a.sidx[t.s] : t.s) * a.rhs_ld + rr) * a.n + R] : 0.0;
     vs[rr * NB + r] = b - red[rr * NB + r];
   }
   cons_sync();
@@ -638,7 +645,7 @@ __device__ void cons_bwd(const TaskCtx& t, Pipe& p, double* sm, double* red, dou
     double* po = a.cy + ((size_t)t.s * 2 * kRhsCap + kRhsCap + warp) * nt * NB + j * NB;
     __stcg(po + lane, v0);
     __stcg(po + lane + 32, v1);
-    double* out = a.rhs + ((size_t)t.s * a.rhs_ld + warp) * a.n;
+    double* out = a.rhs + ((size_t)(a.sidx ? a.sidx[t.s] : t.s) * a.rhs_ld + warp) * a.n;
     if (j * NB + lane < a.n) out[j * NB + lane] = v0;
     if (j * NB + lane + 32 < a.n) out[j * NB + lane + 32] = v1;
   }
@@ -744,8 +751,8 @@ __global__ void __launch_bounds__(kDagThreads, 2) k_chol_dag(DagArgs a) {
   }
 }
 
-__global__ void k_info_out(int n_scen, const int* __restrict__ ws, int* __restrict__ out) {
-  for (int s = threadIdx.x; s < n_scen; s += blockDim.x) out[s] = ws[s];
+__global__ void k_info_out(int n_scen, const int* __restrict__ ws, int* __restrict__ out, const int* __restrict__ sidx) {
+  for (int s = threadIdx.x; s < n_scen; s += blockDim.x) out[sidx ? sidx[s] : s] = ws[s];
 }
 
 }  // namespace
@@ -771,15 +778,17 @@ int chol_grid_max() {
 }
 
 int launch_chol(const DevNet& net, const Work& w, int n_scen, double* K, const double* sigma_u, double delta_w,
-                double* rhs, int nrhs, int* info, int* info_ws, cudaStream_t st, int grid_max) {
+                double* rhs, int nrhs, int* info, int* info_ws, cudaStream_t st, int grid_max, const int* sidx,
+                const double* dvec, cudaEvent_t* ev) {
   const int n = net.n_u, nt = (n + NB - 1) / NB, ntri = nt * (nt + 1) / 2;
   cudaFuncSetAttribute(k_chol_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDagSmem);  // per device, idempotent
   int launches = 0;
   k_chol_pack<<<dim3(ntri, n_scen), 256, 0, st>>>(n, nt, K, sigma_u, delta_w, w.ctile, w.cflag, w.cticket, info_ws,
-                                                   w.cticket + 1);
+                                                   w.cticket + 1, sidx, dvec);
   ++launches;
   // the factorization runs with the first kRhsCap right-hand sides fused in; further
   // ones (rare) in solve-only runs over the finished factor
+  if (ev) cudaEventRecord(ev[0], st);
   for (int r0 = 0, first = 1; first || r0 < nrhs; r0 += kRhsCap, first = 0) {
     const int nr = std::max(0, std::min(kRhsCap, nrhs - r0)), f = nr > 0 ? 1 : 0;
     if (!first) {
@@ -790,15 +799,16 @@ int launch_chol(const DevNet& net, const Work& w, int n_scen, double* K, const d
     a.n = n; a.nt = nt; a.ntri = ntri; a.S = n_scen; a.nrhs = nr; a.factor = first; a.rhs_ld = nrhs;
     a.ntask = n_scen * ((first ? ntri : 0) + f * nt) + f * n_scen * nt;
     a.tiles = w.ctile; a.flags = w.cflag; a.ticket = w.cticket; a.info = info_ws;
-    a.cy = w.cy; a.rhs = rhs ? rhs + (size_t)r0 * n : nullptr; a.crit = w.cticket + 1;
+    a.cy = w.cy; a.rhs = rhs ? rhs + (size_t)r0 * n : nullptr; a.crit = w.cticket + 1; a.sidx = sidx;
     if (a.ntask > 0) {
       k_chol_dag<<<std::min(grid_max, a.ntask), kDagThreads, kDagSmem, st>>>(a);
       ++launches;
     }
   }
-  k_chol_unpack<<<dim3(nt, nt, n_scen), 256, 0, st>>>(n, nt, w.ctile, K);
+  if (ev) cudaEventRecord(ev[1], st);
+  k_chol_unpack<<<dim3(nt, nt, n_scen), 256, 0, st>>>(n, nt, w.ctile, K, info_ws, sidx);
   ++launches;
-  if (info) { k_info_out<<<1, 256, 0, st>>>(n_scen, info_ws, info); ++launches; }
+  if (info) { k_info_out<<<1, 256, 0, st>>>(n_scen, info_ws, info, sidx); ++launches; }
   return launches;
 }
 

@@ -87,6 +87,8 @@ struct Work {
   double* gbuf;    // [max_scen][2 n_b]   G of the Newton iterations
   double* res;     // [max_scen]          ‖g‖∞ per scenario (Newton)
   int* active;     // [max_scen]          Newton: 1 while the scenario iterates
+  int* csidx;      // [max_scen]          regularization retries: caller scenario of each retried one
+  double* cdelta;  // [max_scen]          … and its δ_w
   double* slabZ;   // [max_tiles][n_x][C]
   double* slabW;   // [max_tiles][n_x][C]
   double* hu;      // [max_tiles][n_u][C]

@@ -27,7 +27,10 @@ int launch_reduce(const DevNet& n, const Work& w, int C, int n_scen, const doubl
 
 // A9: symmetrize + shift + pack, tile-DAG FP64 Cholesky (DMMA updates) with the solves fused in.
 int launch_chol(const DevNet& n, const Work& w, int n_scen, double* K, const double* sigma_u, double delta_w,
-                double* rhs, int nrhs, int* info, int* info_ws, cudaStream_t st, int grid_max);
+                double* rhs, int nrhs, int* info, int* info_ws, cudaStream_t st, int grid_max,
+                const int* sidx = nullptr /* [n_scen] caller scenario of each, device */,
+                const double* dvec = nullptr /* [n_scen] per-scenario δ_w, device */,
+                cudaEvent_t* ev = nullptr /* optional: [2] around the DAG launch(es) */);
 // resident k_chol_dag CTAs on the current device (sets its SMEM attribute there)
 int chol_grid_max();
 

@@ -26,7 +26,7 @@ STRUCTURE = dict(x_theta=0, x_v=1, u_v=2, u_p=3, gx_ptr=4, gx_idx=5, gu_ptr=6, g
 SYMBOLS = ["pf_build_network", "pf_build_network_ex", "pf_destroy", "pf_query", "pf_get_structure", "pf_last_error", "pf_build_error",
            "pf_eval_constraints", "pf_jacobian", "pf_reduced_hessian_batch", "pf_condensed_kkt_solve",
            "pf_launch_count", "pf_profile", "pf_kernel_times", "pf_condensed_rhs", "pf_recover_step",
-           "pf_power_flow", "pf_reduced_gradient"]
+           "pf_power_flow", "pf_reduced_gradient", "pf_condensed_kkt_solve_reg"]
 
 
 class PFError(RuntimeError):
@@ -86,6 +86,8 @@ def load_library():
     lib.pf_power_flow.restype = ctypes.c_int
     lib.pf_reduced_gradient.argtypes = [P, I32] + [P] * 7 + [VP]
     lib.pf_reduced_gradient.restype = ctypes.c_int
+    lib.pf_condensed_kkt_solve_reg.argtypes = [P, I32, P, P, D, D, D, D, P, I32, P, P, P, VP]
+    lib.pf_condensed_kkt_solve_reg.restype = ctypes.c_int
     lib.pf_launch_count.argtypes = [P]
     lib.pf_launch_count.restype = ctypes.c_int64
     lib.pf_profile.argtypes = [P, I32]
@@ -194,15 +196,15 @@ class Network:
     def launch_count(self):
         return int(self._lib.pf_launch_count(self._h))
 
-    KERNELS = ("k_fwd", "k_mu", "k_hvp", "k_adj", "k_lu", "k_proj")
+    KERNELS = ("k_fwd", "k_mu", "k_hvp", "k_adj", "k_lu", "k_proj", "k_chol_dag")
 
     def profile(self, enable=True):
         self._check(self._lib.pf_profile(self._h, int(enable)), "pf_profile")
 
     def kernel_times(self):
         """Per-kernel ms of the last reduction / jacobian calls (profiling on)."""
-        ms = (ctypes.c_float * 6)()
-        k = self._lib.pf_kernel_times(self._h, ctypes.cast(ms, ctypes.c_void_p), 6)
+        ms = (ctypes.c_float * 7)()
+        k = self._lib.pf_kernel_times(self._h, ctypes.cast(ms, ctypes.c_void_p), 7)
         return {self.KERNELS[i]: float(ms[i]) for i in range(k)}
 
     # ---------------------------------------------------------------- compute
@@ -332,3 +334,22 @@ class Network:
             _dev(grad, "grad", f64, n_scen * d["n_u"]), _stream(stream))
         self._check(st, "pf_reduced_gradient")
         return lam, grad
+
+    # ---------------------------------------------------------------- NEXT-3
+    def pf_condensed_kkt_solve_reg(self, n_scen, K, sigma_u=None, delta_init=0.0, delta_first=1e-8, growth=10.0,
+                                   delta_max=1e12, rhs=None, nrhs=0, stream=None):
+        """Regularized condensed solve; returns (delta, trials, info) host arrays."""
+        import torch
+        d = self.dims
+        f64 = torch.float64
+        delta = np.zeros(n_scen, dtype=np.float64)
+        trials = np.zeros(n_scen, dtype=np.int32)
+        info = np.zeros(n_scen, dtype=np.int32)
+        st = self._lib.pf_condensed_kkt_solve_reg(
+            self._h, n_scen, _dev(K, "K", f64, n_scen * d["n_u"] ** 2), _dev(sigma_u, "sigma_u", f64, n_scen * d["n_u"]),
+            float(delta_init), float(delta_first), float(growth), float(delta_max),
+            _dev(rhs, "rhs", f64, n_scen * nrhs * d["n_u"]) if nrhs > 0 else None, int(nrhs),
+            delta.ctypes.data_as(ctypes.c_void_p), trials.ctypes.data_as(ctypes.c_void_p),
+            info.ctypes.data_as(ctypes.c_void_p), _stream(stream))
+        self._check(st, "pf_condensed_kkt_solve_reg")
+        return delta, trials, info

@@ -235,3 +235,53 @@ def test_reduced_gradient(pfmod, name):
         record("reduced_gradient", case=name, scenario=s, lam_rel_err=float(rel_err(lam[s].cpu().numpy(), lo)),
                grad_rel_err=float(rel_err(g[s].cpu().numpy(), go)))
     h.close()
+
+
+# ---------------------------------------------------------------------------- NEXT-3
+@pytest.mark.parametrize("name", ["case118", "case1354"])
+def test_regularized_condensed_solve(pfmod, name):
+    """NEXT-3: pf_condensed_kkt_solve_reg runs the paper's δ_w loop for three
+    scenarios at once — one PD at δ_w = 0 (large Σ_u), two needing different
+    δ_w — with exactly the oracle loop's δ_w, trial count and info, its factor
+    and solve (1e-10), and K̂/rhs untouched for a scenario capped by δ_max."""
+    import torch
+    net, pt = table1_grid(name)
+    pts = [pt, make_scenario(net, pt, 1), make_scenario(net, pt, 2)]
+    S = 3
+    n_u = O.partition(net)["n_u"]
+    h = pfmod.Network(net, max_batch=n_u, max_scen=S)
+    v, th = dev(stack(pts, "v")), dev(stack(pts, "theta"))
+    h.pf_jacobian(S, v, th)
+    KV = torch.empty(S, n_u, n_u, dtype=torch.float64, device="cuda")
+    h.pf_reduced_hessian_batch(S, v, th, dev(stack(pts, "lam")), dev(stack(pts, "y")), KV,
+                               sigma_s=dev(stack(pts, "sigma_s")), sigma_x=dev(stack(pts, "sigma_x")),
+                               p_d=dev(stack(pts, "p_d")))
+    torch.cuda.synchronize()
+    Kh = KV.cpu().numpy()
+    sig = stack(pts, "sigma_u").copy()
+    sig[0] += 2 * np.abs(Kh[0]).sum(axis=0).max()       # scenario 0 diagonally dominant: PD at δ_w = 0
+    b = np.random.default_rng(17).standard_normal((S, 2, n_u))
+    args = dict(delta_init=0.0, delta_first=1e-4, growth=10.0, delta_max=1e12)
+    K, rhs = dev(Kh.copy()), dev(b.copy())
+    delta, trials, info = h.pf_condensed_kkt_solve_reg(S, K, dev(sig), rhs=rhs, nrhs=2, **args)
+    torch.cuda.synchronize()
+    Lg, xg = K.cpu().numpy(), rhs.cpu().numpy()
+    assert trials[0] == 1 and delta[0] == 0.0
+    for s in range(S):
+        Kc0 = O.condensed(0.5 * (Kh[s] + Kh[s].T), sig[s], 0.0)
+        do, to, io, Lo = O.regularized_cholesky(Kc0, **args)
+        assert (delta[s], trials[s], info[s]) == (do, to, io), (s, delta, trials, info, do, to, io)
+        assert io == 0
+        assert rel_err(Lg[s].T, Lo) <= TOL
+        for k in range(2):
+            assert rel_err(xg[s, k], O.chol_solve(Lo, b[s, k])) <= TOL
+        record("next3_reg", case=name, scenario=s, delta_w=float(do), trials=int(to))
+    # δ_max below what scenario 1 needs: it stops failed, K̂ and rhs untouched, the others solve
+    cap = delta[1] / 10.0
+    K, rhs = dev(Kh.copy()), dev(b.copy())
+    d2, t2, i2 = h.pf_condensed_kkt_solve_reg(S, K, dev(sig), rhs=rhs, nrhs=2, **dict(args, delta_max=cap))
+    torch.cuda.synchronize()
+    assert i2[1] > 0 and d2[1] <= cap
+    assert np.array_equal(K.cpu().numpy()[1], Kh[1]) and np.array_equal(rhs.cpu().numpy()[1], b[1])
+    assert i2[0] == 0
+    h.close()

@@ -347,6 +347,38 @@ def test_inertia_theorem3():
     assert seen == {True, False}
 
 
+def test_regularized_cholesky_certificate():
+    """NEXT-3 pin: the δ_w loop stops at the first δ_w of its geometric
+    schedule above −λ_min(K_cond) (eigenvalues), and there K_aug has the
+    inertia (n_x+n_u+m, n_x+m, 0) while the previous trial's K_aug does not
+    (Theorem 3; Jacobi eigenvalues)."""
+    net, part, pt, lam, y, mult = _case9_solved()
+    Gx, Gu, A = O.jacobians(net, part, pt)
+    W = O.lagrangian_hessian(net, part, pt, lam, y)
+    K = O.kkt_K(net, part, pt, lam, y, mult["sigma_s"], mult["sigma_x"])
+    Kh = O.reduce_naive(K, Gx, Gu)
+    shift = np.linalg.eigvalsh(O.condensed(Kh, mult["sigma_u"], 0.0)).min() + 3.7   # λ_min(K_cond) = −3.7
+    base = O.condensed(Kh, mult["sigma_u"] - shift, 0.0)
+    lmin = np.linalg.eigvalsh(base).min()
+    assert lmin < 0
+    delta, trials, info, L = O.regularized_cholesky(base, 0.0, 1e-8, 10.0, 1e12)
+    assert info == 0 and trials > 2
+    assert delta > -lmin and delta / 10.0 < -lmin
+    sched = [0.0] + [1e-8 * 10.0 ** k for k in range(trials - 1)]
+    assert np.isclose(delta, sched[trials - 1])
+    n_u, n_x, m = part["n_u"], part["n_x"], part["m"]
+    want = (n_x + n_u + m, n_x + m, 0)
+    for d, ok in ((delta, True), (delta / 10.0, False)):
+        Ka = O.kaug(W, Gx, Gu, A, mult["sigma_u"] - shift + d, mult["sigma_x"], mult["sigma_s"])
+        ev = O.jacobi_eigenvalues(Ka)
+        tol = 1e-13 * np.abs(ev).max()
+        inertia = (int(np.sum(ev > tol)), int(np.sum(ev < -tol)), int(np.sum(np.abs(ev) <= tol)))
+        assert (inertia == want) == ok
+    # δ_max caps the loop: info stays the failing column
+    d2, t2, i2, _ = O.regularized_cholesky(base, 0.0, 1e-8, 10.0, delta / 100.0)
+    assert i2 > 0 and d2 <= delta / 100.0
+
+
 def test_jacobi_matches_lapack():
     rng = np.random.default_rng(0)
     M = rng.standard_normal((12, 12))
