@@ -281,7 +281,7 @@ def main():
         if ncols > 0:  # direction mode has S = 1, so KV[:, :ncols] is contiguous
             h.pf_reduced_hessian_batch(S, t["v"], t["theta"], t["lam"], t["y"], KV[:, :ncols],
                                        sigma_s=t["sigma_s"], sigma_x=t["sigma_x"], col0=col0, N=ncols, p_d=t["p_d"])
-        K = allgather_columns(KV, n_u) if (directions and world > 1) else KV
+        K = allgather_columns(KV, n_u) if (directions and world > 1) else KV[:, :n_u]  # S = 1 when cpad > n_u
         if red_ev:
             red_ev[1].record(stream)
         if chol_ev:

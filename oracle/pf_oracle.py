@@ -737,13 +737,21 @@ def condensed_rhs(W, Gx, Gu, A, sigma_x, sigma_s, r):
     return b, (rh1, rh2, rh3), Ahat
 
 
-def recover_step(W, Gx, Gu, A, sigma_x, sigma_s, r, p_u):
+def recover_step(W, Gx, Gu, A, sigma_x, sigma_s, r, p_u, lu=None):
     """Algorithm 1's dual, slack, state and adjoint steps (Theorem 1 recovery,
     Theorem 2 with R10): p_y = Σ_s(Â_u p_u + r̂₃ + Σ_s⁻¹r̂₂), p_s = Σ_s⁻¹(p_y − r̂₂),
     p_x = −G_x⁻¹(r₄ + G_u p_u), p_λ = −G_x⁻ᵀ(r₂ + A_xᵀp_y + W_xu p_u + (W_xx+Σ_x)p_x).
-    Returns the step ordered (p_u, p_x, p_s, p_λ, p_y)."""
+    Returns the step ordered (p_u, p_x, p_s, p_λ, p_y).  lu: None = dense
+    LAPACK solves with G_x, or a SparseLU (an independent factorization, for
+    the measured noise floor of R20) for the p_x and p_λ solves."""
     _, (rh1, rh2, rh3), Ahat = condensed_rhs(W, Gx, Gu, A, sigma_x, sigma_s, r)
+    if lu is not None:
+        solve = lambda b: lu.solve(b)                  # noqa: E731
+        solve_t = lambda b: lu.solve(b, trans="T")     # noqa: E731
     Gx = np.asarray(sp.csr_matrix(Gx).toarray())
+    if lu is None:
+        solve = lambda b: np.linalg.solve(Gx, b)       # noqa: E731
+        solve_t = lambda b: np.linalg.solve(Gx.T, b)   # noqa: E731
     Gu = np.asarray(sp.csr_matrix(Gu).toarray())
     A = np.asarray(sp.csr_matrix(A).toarray())
     W = np.asarray(sp.csr_matrix(W).toarray())
@@ -754,8 +762,8 @@ def recover_step(W, Gx, Gu, A, sigma_x, sigma_s, r, p_u):
     Ax = A[:, n_u:]
     p_y = sigma_s * (Ahat @ p_u + rh3 + rh2 / sigma_s)
     p_s = (p_y - rh2) / sigma_s
-    p_x = -np.linalg.solve(Gx, r4 + Gu @ p_u)
-    p_l = -np.linalg.solve(Gx.T, r2 + Ax.T @ p_y + Wxu @ p_u + Wxx @ p_x)
+    p_x = -solve(r4 + Gu @ p_u)
+    p_l = -solve_t(r2 + Ax.T @ p_y + Wxu @ p_u + Wxx @ p_x)
     return np.concatenate([p_u, p_x, p_s, p_l, p_y])
 
 

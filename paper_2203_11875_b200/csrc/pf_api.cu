@@ -319,24 +319,8 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
     for (int i = 0; i < n_b; ++i)
       if (P.bus_pth[i] < 0 && P.bus_pv[i] < 0) h->hvp_order.push_back(i);
   }
-  std::vector<int4> inc_rec(2 * (size_t)n_l);
-  for (int i = 0; i < n_b; ++i)
-    for (int e = P.inc_ptr[i]; e < P.inc_ptr[i + 1]; ++e) {
-      const int l = P.inc_line[e];
-      const bool from = line_from[l] == i;
-      const int o = from ? line_to[l] : line_from[l];
-      inc_rec[e] = make_int4(l, P.bus_pth[o], P.bus_pv[o] >= 0 ? P.bus_pv[o] : -1 - P.u_v[o],
-                             (from ? 1 : 0) | ((P.bus_gen[o] + 1) << 1));
-    }
 
   const std::vector<int>& hvp_order = h->hvp_order.size() == (size_t)n_b ? h->hvp_order : P.hvp_bus;
-  std::vector<int4> hvp_meta(n_b);
-  std::vector<int2> hvp_inc(n_b);
-  for (int kb = 0; kb < n_b; ++kb) {
-    const int i = hvp_order[kb];
-    hvp_meta[kb] = make_int4(i, P.bus_pth[i], P.bus_pv[i] >= 0 ? P.bus_pv[i] : -1 - P.u_v[i], P.bus_gen[i]);
-    hvp_inc[kb] = make_int2(P.inc_ptr[i], P.inc_ptr[i + 1] - P.inc_ptr[i]);
-  }
   // step recovery / Newton maps: G row of each permuted row, A by columns
   std::vector<int> row_g(P.n_x);
   for (int r = 0; r < P.n_x; ++r) row_g[r] = -1;
@@ -356,9 +340,91 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
         a_crow[q] = k; a_cpos[q] = e;   // ascending rows within a column (deterministic sums)
       }
   }
+  // Bus-block sets of the staged block-SpMM kernels (pf_reduce.cu k_blk): k_hvp over every bus in
+  // hvp_order (μ rows of generator neighbours staged too), k_mu over the generator buses in the
+  // same order; consecutive output buses form a chunk while its distinct staged rows fit the cap.
+  std::vector<int4> hvp_out(n_b);
+  for (int kb = 0; kb < n_b; ++kb) {
+    const int i = h->hvp_order.size() == (size_t)n_b ? h->hvp_order[kb] : P.hvp_bus[kb];
+    hvp_out[kb] = make_int4(i, P.bus_pth[i], P.bus_pv[i] >= 0 ? P.bus_pv[i] : -1 - P.u_v[i], P.bus_gen[i]);
+  }
+  std::vector<int4> mu_out;
+  for (const int4& o : hvp_out) if (P.bus_gen[o.x] >= 0) mu_out.push_back(make_int4(o.x, P.bus_gen[o.x], 0, 0));
+  auto build_set = [&](const std::vector<int4>& outs, bool with_mu, BlkSet& B) {
+    const int row_cap = hvp_stage_rows(h->C), bus_cap = 64;
+    std::vector<int> ptr(1, 0), self, nbr, ck(1, 0), stp(1, 0), str, slot(P.n_x + 2 * n_g, -1), rows;
+    std::vector<int4> meta;
+    std::vector<int2> jt;
+    auto nbrs = [&](int i) {
+      std::vector<int> nb{i};
+      for (int e = P.inc_ptr[i]; e < P.inc_ptr[i + 1]; ++e) {
+        const int l = P.inc_line[e];
+        nb.push_back(line_from[l] == i ? line_to[l] : line_from[l]);
+      }
+      std::sort(nb.begin() + 1, nb.end());  // the bus itself first (the difference form), then ascending
+      nb.erase(std::unique(nb.begin() + 1, nb.end()), nb.end());
+      return nb;
+    };
+    // rows of bus j: θ_j and v_j slab rows (< n_x); with_mu: μ_A rows n_x + 2g, + 1 of a generator bus j
+    auto rows_of = [&](int j, int* r) {
+      r[0] = P.bus_pth[j]; r[1] = P.bus_pv[j];
+      r[2] = with_mu && P.bus_gen[j] >= 0 ? P.n_x + 2 * P.bus_gen[j] : -1;
+    };
+    auto close_chunk = [&]() {
+      for (int r : rows) slot[r] = -1;
+      str.insert(str.end(), rows.begin(), rows.end());
+      stp.push_back((int)str.size());
+      ck.push_back((int)ptr.size() - 1);
+      rows.clear();
+    };
+    for (const int4& o : outs) {
+      const int i = o.x;
+      const std::vector<int> nb = nbrs(i);
+      int extra = 0;  // rows this bus adds to the open chunk
+      for (int j : nb) { int r[3]; rows_of(j, r); for (int q = 0; q < 3; ++q) extra += (r[q] >= 0 && slot[r[q]] < 0) * (q == 2 ? 2 : 1); }
+      const int nbus = (int)ptr.size() - 1 - ck.back();
+      if (nbus > 0 && ((int)rows.size() + extra > row_cap || nbus >= bus_cap)) close_chunk();
+      for (int j : nb) {
+        int r[3]; rows_of(j, r);
+        for (int q = 0; q < 3; ++q)
+          if (r[q] >= 0 && slot[r[q]] < 0) {
+            slot[r[q]] = (int)rows.size(); rows.push_back(r[q]);
+            if (q == 2) rows.push_back(r[q] + 1);  // μ^Q row right after μ^P
+          }
+        const int vs = r[1] >= 0 ? slot[r[1]] : -1 - P.u_v[j];
+        meta.push_back(make_int4(r[0] >= 0 ? slot[r[0]] : -1, vs, r[2] >= 0 ? slot[r[2]] : -1, 0));
+        self.push_back(i);
+        nbr.push_back(j);
+        // θ_i / v_i within J_bus row P_j (Q_j shares the pattern): own columns or an incidence of j towards i
+        int ot = -1, ov = -1;
+        if (with_mu && P.bus_gen[j] >= 0) {
+          if (j == i) { ot = P.jb_self_th[i]; ov = P.jb_self_v[i]; }
+          else
+            for (int e = P.inc_ptr[j]; e < P.inc_ptr[j + 1]; ++e) {
+              const int l = P.inc_line[e];
+              if ((line_from[l] == j ? line_to[l] : line_from[l]) == i) { ot = P.inc_off_th[e]; ov = P.inc_off_v[e]; break; }
+            }
+        }
+        jt.push_back(make_int2(ot, ov));
+      }
+      ptr.push_back((int)meta.size());
+    }
+    close_chunk();
+    B.nout = (int)outs.size(); B.nblk = (int)meta.size(); B.nchunk = (int)ck.size() - 1;
+    B.st_max = B.blk_max = B.ck_max = 0;
+    for (int c = 0; c < B.nchunk; ++c) {
+      B.st_max = std::max(B.st_max, stp[c + 1] - stp[c]);
+      B.blk_max = std::max(B.blk_max, ptr[ck[c + 1]] - ptr[ck[c]]);
+      B.ck_max = std::max(B.ck_max, ck[c + 1] - ck[c]);
+    }
+    return up(h, ptr, &B.ptr) && up(h, meta, &B.meta) && up(h, self, &B.self) && up(h, nbr, &B.nbr) &&
+           up(h, jt, &B.jt) && up(h, outs, &B.out) && up(h, ck, &B.ck_ptr) && up(h, stp, &B.st_ptr) &&
+           up(h, str, &B.st_row);
+  };
+  bool blk_ok = build_set(hvp_out, true, d.hb) && build_set(mu_out, false, d.mb);
   std::vector<int> u_gen(P.n_u, -1);
   for (int g = 0; g < n_g; ++g) if (P.u_p[g] >= 0) u_gen[P.u_p[g]] = g;
-  bool ok = up(h, lf, &d.lf) && up(h, lt, &d.lt) && up(h, coef, &d.coef) && up(h, gsh, &d.gsh) &&
+  bool ok = blk_ok && up(h, lf, &d.lf) && up(h, lt, &d.lt) && up(h, coef, &d.coef) && up(h, gsh, &d.gsh) &&
             up(h, bsh, &d.bsh) && up(h, gb, &d.gen_bus) && up(h, P.bus_gen, &d.bus_gen) &&
             up(h, cq, &d.c_quad) && up(h, cl, &d.c_lin) && up(h, pd, &d.p_d0) && up(h, qd, &d.q_d0) &&
             up(h, P.x_th, &d.x_th) && up(h, P.x_v, &d.x_v) && up(h, P.u_v, &d.u_v) && up(h, P.u_p, &d.u_p) &&
@@ -375,8 +441,8 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
             up(h, P.levU_blk, &d.levU_blk) && up(h, P.guc_ptr, &d.guc_ptr) && up(h, P.guc_row, &d.guc_row) &&
             up(h, P.guc_src, &d.guc_src) && up(h, P.gur_ptr, &d.gur_ptr) && up(h, P.gur_col, &d.gur_col) &&
             up(h, P.gur_src, &d.gur_src) && up(h, P.bus_pth, &d.bus_pth) && up(h, P.bus_pv, &d.bus_pv) &&
-            up(h, gbus, &d.gbus) && up(h, rowmeta, &d.rowmeta) && up(h, hvp_order, &d.hvp_bus) && up(h, hvp_meta, &d.hvp_meta) && up(h, hvp_inc, &d.hvp_inc) &&
-            up(h, inc_rec, &d.inc_rec) && up(h, taskL, &d.taskL) && up(h, taskU, &d.taskU) &&
+            up(h, gbus, &d.gbus) && up(h, rowmeta, &d.rowmeta) && up(h, hvp_order, &d.hvp_bus) &&
+            up(h, taskL, &d.taskL) && up(h, taskU, &d.taskU) &&
             up(h, taskLr, &d.taskLr) && up(h, levLr_ptr, &d.levLr_ptr) && up(h, rowbm, &d.rowbm) &&
             up(h, taskUa, &d.taskUa) && up(h, levUa_ptr, &d.levUa_ptr) && up(h, h->p1_task, &d.p1_task) &&
             up(h, h->p1_ptr, &d.p1_ptr) && up(h, h->u_top, &d.u_top) && up(h, h->u_top_ptr, &d.u_top_ptr) &&
@@ -398,7 +464,8 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
        alloc(h, 1 + 1024, &w.cticket) && alloc(h, S * chol_vec_doubles(d.n_u), &w.cy) &&
        alloc(h, S * d.nnz_a, &w.aval) && alloc(h, S * (d.n_u + d.n_x + d.m), &w.zero) &&
        alloc(h, S * 2 * d.n_b, &w.gbuf) && alloc(h, S, &w.res) && alloc(h, S, &w.active) &&
-       alloc(h, S, &w.csidx) && alloc(h, S, &w.cdelta);
+       alloc(h, S, &w.csidx) && alloc(h, S, &w.cdelta) && alloc(h, S * (size_t)d.hb.nblk * 8, &w.hbval) &&
+       alloc(h, S * (size_t)d.mb.nblk * 8, &w.mbval);
   ok = ok && cudaMemset(w.zero, 0, S * (d.n_u + d.n_x + d.m) * sizeof(double)) == cudaSuccess;
   if (!ok) {
     g_build_err = std::string("device allocation/upload failed: ") + cudaGetErrorString(cudaGetLastError());

@@ -5,6 +5,21 @@
 
 namespace pf {
 
+// A set of 2×2 bus blocks for the SMEM-staged block-SpMM kernel (pf_reduce.cu k_blk): per
+// output bus (position p of `out`) the blocks of its neighbours j, the bus itself first; the
+// chunks of consecutive output buses whose distinct rows fit the SMEM budget; and per chunk the
+// rows it stages (slab row r < n_x of the direction tile, or μ_A row n_x + 2g / + 1).
+struct BlkSet {
+  const int *ptr;        // [nout + 1] blocks of output position p
+  const int4 *meta;      // [nblk] {slot of θ_j (−1: ref), slot of v_j or −1−u(v_j), slot of μ^P_j (μ^Q next) or −1, 0}
+  const int *self, *nbr; // [nblk] bus i, neighbour j (the per-scenario prep)
+  const int2 *jt;        // [nblk] hb only: offsets of θ_i, v_i in J_bus rows P_j / Q_j of a generator bus j
+  const int4 *out;       // [nout] hb: {bus, θ row, v row or −1−u, gen}; mb: {bus, gen, 0, 0}
+  const int *ck_ptr;     // [nchunk + 1] output positions per chunk
+  const int *st_ptr, *st_row;  // [nchunk + 1], [nstage]
+  int nout, nblk, nchunk, st_max, blk_max, ck_max;
+};
+
 // Network-level device data (read-only, shared by all scenarios).
 struct DevNet {
   int n_b, n_l, n_g, n_x, n_u, m, n_r, n_h, r0, g_r, n_gb, nblk;
@@ -27,8 +42,6 @@ struct DevNet {
   const int *gbus;              // [n_gb] generator buses ascending (the r buses)
   const int4 *rowmeta;          // [n_x] {lu_ptr[r], lu_diag[r], lu_ptr[r+1], block of r}
   const int *hvp_bus;           // [n_b] buses in elimination order, the reference bus last
-  const int4 *hvp_meta;         // [n_b] per hvp_bus position: {bus, θ row, v row or −1−(u index), gen or −1}
-  const int2 *hvp_inc;          // [n_b] per hvp_bus position: {first incidence record, degree}
   const int4 *taskL, *taskU;    // [n_blocks] sweep tasks in level order (pf_reduce.cu sweep())
   // Sparse right-hand sides (Gilbert–Peierls reach): for unit directions the L sweep of
   // canonical column tile t (columns [tC, tC+C)) only visits the blocks on the
@@ -48,13 +61,14 @@ struct DevNet {
   // to the ancestors of G_u's rows (the Lᵀ sweep)
   const int4 *u_top, *u_bot, *ua_top, *ua_bot;
   const int *u_top_ptr, *u_bot_ptr, *ua_top_ptr, *ua_bot_ptr;
-  const int4 *inc_rec;          // [2 n_l] per incidence: {line, far θ row, far v row | −1−u, from | 2(gen+1)}
   // step recovery / Newton (pf_step): permuted slab row <-> x index, the G row
   // (P_i = i, Q_i = n_b + i) of each permuted row, and A by columns (CSC over
   // z = [u; x]: rows and positions in the CSR value array)
   const int *perm, *iperm, *row_g;
   const int *a_cptr, *a_crow, *a_cpos, *a_idx;
   const int *u_gen;             // [n_u] generator of a p_g control, −1 for v controls
+  BlkSet hb;                    // k_hvp: K's bus blocks (every bus) + A_rᵀ at generator neighbours
+  BlkSet mb;                    // k_mu: ∂(P_g, Q_g)/∂(θ_j, v_j) blocks of the generator buses g
   int C;                        // directions per tile (slab row width)
   int lu_maxlen;                // longest row of the filled LU pattern
 };
@@ -87,6 +101,8 @@ struct Work {
   double* gbuf;    // [max_scen][2 n_b]   G of the Newton iterations
   double* res;     // [max_scen]          ‖g‖∞ per scenario (Newton)
   int* active;     // [max_scen]          Newton: 1 while the scenario iterates
+  double* hbval;   // [max_scen][hb.nblk][8] per bus block: B (θθ θv vθ vv) of K, then JT (θ←μP θ←μQ v←μP v←μQ)
+  double* mbval;   // [max_scen][mb.nblk][8] per generator block: (∂P/∂θ ∂P/∂v ∂Q/∂θ ∂Q/∂v), 4 unused
   int* csidx;      // [max_scen]          regularization retries: caller scenario of each retried one
   double* cdelta;  // [max_scen]          … and its δ_w
   double* slabZ;   // [max_tiles][n_x][C]

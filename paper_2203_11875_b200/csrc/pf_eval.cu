@@ -626,6 +626,95 @@ __global__ void k_prep_bus2(DevNet n, Work w, int n_scen) {
   }
 }
 
+// K's 2×2 bus blocks for k_hvp (A6): B_ij on (θ, v) of buses i, j from the line
+// blocks H (3×3 on (v_f, v_t, Δ), Δ = θ_f − θ_t) of the lines between them —
+//   B_ff = [[H22, H02], [H02, H00]],   B_ft = [[−H22, H12], [−H02, H01]],
+//   B_tt = [[H22, −H12], [−H12, H11]], B_tf = B_ftᵀ —
+// plus, on the diagonal, Σ_x and the ψ^d curvature 2w̄^d; and JT_ij =
+// ∂(P_j, Q_j)/∂(θ_i, v_i)ᵀ from J_bus when j is a generator bus (the A_rᵀ μ_A part).
+// The θ columns of B sum to zero over j (every line term depends on Δ only), so
+// k_hvp applies them to angle DIFFERENCES, (h_θ, h_v)_i += B_ij[:, θ] (dθ_j − dθ_i),
+// as the line form does (no cancellation for smooth directions such as state
+// steps); the diagonal block then keeps only Σ_x on its θ column.
+__global__ void k_prep_hblk(DevNet n, Work w, int n_scen) {
+  const long long total = (long long)n_scen * n.hb.nblk;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / n.hb.nblk), e = (int)(t % n.hb.nblk);
+    const int i = __ldg(n.hb.self + e), j = __ldg(n.hb.nbr + e);
+    const double* lb = w.lblk + (size_t)s * n.n_l * LB_N;
+    double b00 = 0.0, b01 = 0.0, b10 = 0.0, b11 = 0.0;
+    for (int q = __ldg(n.inc_ptr + i); q < __ldg(n.inc_ptr + i + 1); ++q) {
+      const int l = __ldg(n.inc_line + q);
+      const bool from = __ldg(n.lf + l) == i;
+      const int o = from ? __ldg(n.lt + l) : __ldg(n.lf + l);
+      if (j != i && o != j) continue;
+      const double* H = lb + (size_t)l * LB_N;
+      const double h00 = H[LB_H00], h01 = H[LB_H01], h02 = H[LB_H02], h11 = H[LB_H11], h12 = H[LB_H12],
+                   h22 = H[LB_H22];
+      if (j == i) {  // θ column: carried by the off-diagonal blocks' differences
+        if (from) { b01 += h02; b11 += h00; }
+        else { b01 -= h12; b11 += h11; }
+      } else {
+        if (from) { b00 -= h22; b01 += h12; b10 -= h02; b11 += h01; }
+        else { b00 -= h22; b01 -= h02; b10 += h12; b11 += h01; }
+      }
+    }
+    if (j == i) {
+      const double* bs = w.bs + (size_t)s * BS_N * n.n_b;
+      b00 += bs[BS_SXT * n.n_b + i];
+      b11 += bs[BS_WD2 * n.n_b + i] + bs[BS_SXV * n.n_b + i];
+    }
+    double jt[4] = {0.0, 0.0, 0.0, 0.0};
+    const int2 off = __ldg(n.hb.jt + e);
+    if (__ldg(n.bus_gen + j) >= 0) {
+      const double* jb = w.jb + (size_t)s * n.nnz_jb;
+      const int rp = __ldg(n.jb_ptr + j), rq = __ldg(n.jb_ptr + n.n_b + j);
+      if (off.x >= 0) { jt[0] = jb[rp + off.x]; jt[1] = jb[rq + off.x]; }
+      if (off.y >= 0) { jt[2] = jb[rp + off.y]; jt[3] = jb[rq + off.y]; }
+    }
+    double2* o = reinterpret_cast<double2*>(w.hbval + ((size_t)s * n.hb.nblk + e) * 8);
+    o[0] = make_double2(b00, b01); o[1] = make_double2(b10, b11);
+    o[2] = make_double2(jt[0], jt[1]); o[3] = make_double2(jt[2], jt[3]);
+  }
+}
+
+// The generator-bus blocks of k_mu (A7.3 first half): dG_g = A_r,g · d as 2×2 blocks
+// M_gj = ∂(P_g, Q_g)/∂(θ_j, v_j) from the line Jacobians J (4×3 on (v_f, v_t, Δ)) —
+// θ columns applied to angle differences (dθ_j − dθ_g) like k_hvp's, so the diagonal
+// block carries only the v column (own line ends + the shunt 2 g_sh v_g, −2 b_sh v_g).
+__global__ void k_prep_mblk(DevNet n, Work w, int n_scen) {
+  const long long total = (long long)n_scen * n.mb.nblk;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / n.mb.nblk), e = (int)(t % n.mb.nblk);
+    const int g = __ldg(n.mb.self + e), j = __ldg(n.mb.nbr + e);
+    const double* lb = w.lblk + (size_t)s * n.n_l * LB_N;
+    double pt = 0.0, pv = 0.0, qt = 0.0, qv = 0.0;
+    for (int q = __ldg(n.inc_ptr + g); q < __ldg(n.inc_ptr + g + 1); ++q) {
+      const int l = __ldg(n.inc_line + q);
+      const bool from = __ldg(n.lf + l) == g;
+      const int o = from ? __ldg(n.lt + l) : __ldg(n.lf + l);
+      if (j != g && o != j) continue;
+      const double* J = lb + (size_t)l * LB_N + LB_J;   // rows (s_p^f, s_q^f, s_p^t, s_q^t), cols (v_f, v_t, Δ)
+      const double* Jp = J + (from ? 0 : 6);
+      const double* Jq = J + (from ? 3 : 9);
+      if (j == g) { pv += Jp[from ? 0 : 1]; qv += Jq[from ? 0 : 1]; }
+      else {        // Δ = θ_f − θ_t: ∂/∂θ_j = −∂/∂Δ at the from end, +∂/∂Δ at the to end
+        pt += from ? -Jp[2] : Jp[2]; qt += from ? -Jq[2] : Jq[2];
+        pv += Jp[from ? 1 : 0]; qv += Jq[from ? 1 : 0];
+      }
+    }
+    if (j == g) {
+      const double vg = w.bs[(size_t)s * BS_N * n.n_b + BS_V * n.n_b + g];
+      pv += 2.0 * __ldg(n.gsh + g) * vg;
+      qv -= 2.0 * __ldg(n.bsh + g) * vg;
+    }
+    double2* out = reinterpret_cast<double2*>(w.mbval + ((size_t)s * n.mb.nblk + e) * 8);
+    out[0] = make_double2(pt, pv); out[1] = make_double2(qt, qv);
+  }
+}
+
 }  // namespace
 
 #ifdef PF_LU_TRACE
@@ -691,7 +780,9 @@ int launch_prep(const DevNet& n, const Work& w, int n_scen, const double* p_d, c
   k_prep_bus1<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen, p_d, lam, y, sigma_s, sigma_x);
   k_prep_line<<<blocks_for((long long)n_scen * n.n_l), kThreads, 0, st>>>(n, w, n_scen, y, sigma_s);
   k_prep_bus2<<<blocks_for((long long)n_scen * n.n_b), kThreads, 0, st>>>(n, w, n_scen);
-  return 3;
+  k_prep_hblk<<<blocks_for((long long)n_scen * n.hb.nblk), kThreads, 0, st>>>(n, w, n_scen);
+  k_prep_mblk<<<blocks_for((long long)n_scen * n.mb.nblk), kThreads, 0, st>>>(n, w, n_scen);
+  return 5;
 }
 
 }  // namespace pf

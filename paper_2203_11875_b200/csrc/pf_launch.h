@@ -43,6 +43,7 @@ int launch_pf_resid(const DevNet& n, const Work& w, int n_scen, cudaStream_t st)
 int launch_newton_step(const DevNet& n, const Work& w, int C, int n_scen, double* v, double* th, cudaStream_t st);
 
 int pick_tile_cols(int n_x, int n_scen_x_N);
+int hvp_stage_rows(int C);  // slab rows one k_hvp chunk may stage in SMEM (pf_reduce.cu)
 #ifdef PF_LU_TRACE
 void set_lu_trace(unsigned long long* p);  // debug builds: per-level k_lu timestamps
 #endif

@@ -27,27 +27,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kCH = 64;        // u-columns per transposed output chunk
-#ifndef PF_BUS_PER_CTA
-#define PF_BUS_PER_CTA 128
-#endif
-#ifndef PF_MU_BUS_PER_CTA
-#define PF_MU_BUS_PER_CTA 64
-#endif
-constexpr int kBusPerCta = PF_MU_BUS_PER_CTA;  // generator buses per k_mu CTA
-#ifndef PF_HVP_MIN_BLOCKS
-#define PF_HVP_MIN_BLOCKS 2
-#endif
-constexpr int kHvpMinBlocks = PF_HVP_MIN_BLOCKS;  // CTAs per SM k_hvp is register-capped for
-#ifndef PF_HVP_TILES
-#define PF_HVP_TILES 2
-#endif
-constexpr int kHvpTiles = PF_HVP_TILES;  // direction tiles per k_hvp CTA
-#ifndef PF_MU_TILES
-#define PF_MU_TILES 1
-#endif
-constexpr int kMuTiles = PF_MU_TILES;    // … per k_mu CTA
-constexpr int kHvpBusPerCta = PF_BUS_PER_CTA; // buses per k_hvp CTA (a compact run of the postorder)
-static_assert(kHvpBusPerCta <= kThreads, "k_hvp: a team's buses must fit its lanes");
 #ifndef PF_DOT_W
 #define PF_DOT_W 4
 #endif
@@ -449,34 +428,6 @@ __device__ __forceinline__ void row_st(double* S, int r, int lane, const double*
   }
 }
 
-// dθ, dv at a bus (own rows) and at the far end of an incidence record
-// {line, θ row, v row or −1−(u index), 1·from | 2·(gen + 1)} (pf_api.cu).
-template <int C>
-__device__ __forceinline__ void dirs_at(const Dir<C>& d, int pth, int pv, double* dth, double* dv) {
-  constexpr int CPL = Geo<C>::CPL;
-  if (pth >= 0) row_ld<C>(d.X, pth, d.lane, dth);
-  else
-#pragma unroll
-    for (int j = 0; j < CPL; ++j) dth[j] = 0.0;
-  if (pv >= 0) row_ld<C>(d.X, pv, d.lane, dv);
-  else
-#pragma unroll
-    for (int j = 0; j < CPL; ++j) dv[j] = d.vdir(-1 - pv, j);
-}
-
-// Line block of K (pf_eval.cu k_prep_line): H (3×3 sym) and J (4×3) on the
-// local coordinates (v_f, v_t, Δ), 16-byte loads.
-__device__ __forceinline__ void load_h(const double* p, double* h) {
-  const double2* q = reinterpret_cast<const double2*>(p);
-  const double2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
-  h[0] = a.x; h[1] = a.y; h[2] = b.x; h[3] = b.y; h[4] = c.x; h[5] = c.y;
-}
-__device__ __forceinline__ void load_j(const double* p, double* j) {
-  const double2* q = reinterpret_cast<const double2*>(p + LB_J);
-#pragma unroll
-  for (int k = 0; k < 6; ++k) { const double2 v = __ldg(q + k); j[2 * k] = v.x; j[2 * k + 1] = v.y; }
-}
-
 // ---------------------------------------------------------------- a, b
 template <int C>
 __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Work w, const double* __restrict__ V, int col0,
@@ -535,219 +486,142 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
 }
 
 // ---------------------------------------------------------------- c1
-// μ_A at the generator buses: dG = R_r M dψ = Σ_{ends at i} J_end · d_loc plus
-// the shunt part of G_ii ψ^d; μ_A = Σ_r dG (+ 2c1 dG on P_r0, folded into Σ_rP).
-template <int C, int NT>
-__global__ void __launch_bounds__(kThreads) k_mu(DevNet n, Work w, const double* __restrict__ V, int col0, int N) {
-  constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL, D = NT * CPL;  // NT tiles per CTA, as in k_hvp
-  const int ntile = (N + C - 1) / C;
-  const int s = blockIdx.z;
-  const int lane = threadIdx.x % W, team = threadIdx.x / W, nteam = blockDim.x / W;
-  Dir<C> d[NT];
-  double* MU[NT];
-  bool on[NT];
-#pragma unroll
-  for (int u = 0; u < NT; ++u) {
-    const int t = blockIdx.y * NT + u, tile = min(t, ntile - 1);
-    const size_t cta = (size_t)s * ntile + tile;
-    on[u] = t < ntile;
-    d[u] = make_dir<C>(n, w, V, col0, N, s, tile, cta, lane);
-    MU[u] = w.mu + cta * n.n_g * 2 * C;
-  }
-  const int n_b = n.n_b;
-  const double* lb = w.lblk + (size_t)s * n.n_l * LB_N;
-  const double* bs = w.bs + (size_t)s * BS_N * n_b;
-  const int g1 = min(n.n_gb, (int)(blockIdx.x + 1) * kBusPerCta);
-  for (int gi = blockIdx.x * kBusPerCta + team; gi < g1; gi += nteam) {
-    const int i = __ldg(n.gbus + gi);
-    const int pth = __ldg(n.bus_pth + i), pvi = __ldg(n.bus_pv + i) >= 0 ? __ldg(n.bus_pv + i) : -1 - __ldg(n.u_v + i);
-    double dvi[D], dthi[D], dP[D], dQ[D];
-#pragma unroll
-    for (int u = 0; u < NT; ++u) dirs_at<C>(d[u], pth, pvi, dthi + u * CPL, dvi + u * CPL);
-#pragma unroll
-    for (int k = 0; k < D; ++k) { dP[k] = 0.0; dQ[k] = 0.0; }
-    for (int e = __ldg(n.inc_ptr + i); e < __ldg(n.inc_ptr + i + 1); ++e) {
-      const int4 rec = __ldg(n.inc_rec + e);
-      const bool from = rec.w & 1;
-      double dvo[D], dtho[D], J[12];
-#pragma unroll
-      for (int u = 0; u < NT; ++u) dirs_at<C>(d[u], rec.y, rec.z, dtho + u * CPL, dvo + u * CPL);
-      load_j(lb + (size_t)rec.x * LB_N, J);
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
-        const double dvf = from ? dvi[k] : dvo[k], dvt = from ? dvo[k] : dvi[k];
-        const double dD = from ? dthi[k] - dtho[k] : dtho[k] - dthi[k];
-        // rows (s_p, s_q) of this end
-        dP[k] += from ? J[0] * dvf + J[1] * dvt + J[2] * dD : J[6] * dvf + J[7] * dvt + J[8] * dD;
-        dQ[k] += from ? J[3] * dvf + J[4] * dvt + J[5] * dD : J[9] * dvf + J[10] * dvt + J[11] * dD;
-      }
-    }
-    const double vi = bs[BS_V * n_b + i], gsh = __ldg(n.gsh + i), bsh = __ldg(n.bsh + i);
-    const double srp = bs[BS_SRP * n_b + i], srq = bs[BS_SRQ * n_b + i];
-    const int g = __ldg(n.bus_gen + i);
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      dP[k] = srp * (dP[k] + 2.0 * gsh * vi * dvi[k]);
-      dQ[k] = srq * (dQ[k] - 2.0 * bsh * vi * dvi[k]);
-    }
-#pragma unroll
-    for (int u = 0; u < NT; ++u)
-      if (on[u]) {
-        row_st<C>(MU[u], 2 * g, lane, dP + u * CPL);
-        row_st<C>(MU[u], 2 * g + 1, lane, dQ + u * CPL);
-      }
-  }
-  (void)W;
-}
+// μ_A at the generator buses: dG = R_r M dψ = A_r d (the rows P_g, Q_g of J_bus on the bus's
+// neighbourhood), μ_A = Σ_r dG (+ 2c₁ dG on P_r0, folded into Σ_rP) — k_blk<C, true> below.
 
 // ---------------------------------------------------------------- c2
-// [H_u; H_x] = K [V; Z]: per bus, Σ over incident lines of the line block
-// (H d_loc + Jᵀ μ_A(ends)) restricted to the bus's own (v, θ), plus the bus
-// terms 2w̄^d dv (ψ^d curvature), the shunt part of Mᵀμ_A, and Σ_x.
-template <int C, int NT>
-__global__ void __launch_bounds__(kThreads, kHvpMinBlocks) k_hvp(DevNet n, Work w, const double* __restrict__ V, int col0, int N) {
-  // NT direction tiles per CTA: the per-bus and per-line work (records, line
-  // blocks, index arithmetic) is shared by NT·C directions
-  constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL, D = NT * CPL;
+// [H_u; H_x] = K [V; Z] as a 2×2 bus-block SpMM: for bus i,
+//   (h_θ, h_v)_i = Σ_{j ∈ N(i) ∪ {i}} B_ij (dθ_j, dv_j) + JT_ij (μ^P_j, μ^Q_j)   (JT only at generator buses j)
+// with the blocks precomputed per scenario (k_prep_hblk: the line blocks of K, Σ_x, the ψ^d
+// curvature and A_rᵀ).  A CTA takes one chunk of consecutive buses of the elimination-forest
+// postorder and one direction tile: the chunk's distinct slab rows (own and neighbour buses) are
+// pulled into SMEM by cp.async.bulk row copies issued up front (many bytes in flight, no
+// registers held), then each team walks its buses reading d from SMEM.
+constexpr int kHvpRowCap64 = 80;  // staged rows per chunk at C = 64 (40 KB + the chunk's blocks: 4 CTAs per SM)
+
+__device__ __forceinline__ unsigned sm_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+// MU = false: k_hvp (block set n.hb, values w.hbval) writes H_x / H_u rows;
+// MU = true:  k_mu  (block set n.mb, values w.mbval) writes μ_A = Σ_r ⊙ dG_r rows at the
+//             generator buses (Σ_rP includes the p_ref curvature 2c₁, R8).
+template <int C, bool MU>
+__global__ void __launch_bounds__(kThreads, 4) k_blk(DevNet n, Work w, const double* __restrict__ V, int col0, int N) {
+  constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
+  const BlkSet& B = MU ? n.mb : n.hb;
+  // SMEM: [st_max rows][C] staged d / μ rows | [blk_max][8] block values | [blk_max] block meta | [ck_max] output meta
+  extern __shared__ __align__(128) double stg[];
+  __shared__ __align__(8) uint64_t bar;
   const int ntile = (N + C - 1) / C;
-  const int s = blockIdx.z;
+  const int ck = blockIdx.x, tile = blockIdx.y, s = blockIdx.z;
+  const size_t cta = (size_t)s * ntile + tile;
   const int lane = threadIdx.x % W, team = threadIdx.x / W, nteam = blockDim.x / W;
-  const int n_b = n.n_b;
-  Dir<C> d[NT];
-  const double* MU[NT];
-  double *Y[NT], *Hs[NT];
-  bool on[NT];
-#pragma unroll
-  for (int u = 0; u < NT; ++u) {
-    const int t = blockIdx.y * NT + u, tile = min(t, ntile - 1);  // a missing last tile repeats the previous one
-    const size_t cta = (size_t)s * ntile + tile;
-    on[u] = t < ntile;
-    d[u] = make_dir<C>(n, w, V, col0, N, s, tile, cta, lane);
-    MU[u] = w.mu + cta * n.n_g * 2 * C;
-    Y[u] = w.slabW + cta * n.n_x * C;
-    Hs[u] = w.hu + cta * n.n_u * C;
+  const double* X = w.slabZ + cta * n.n_x * C;
+  double* MU_ = w.mu + cta * n.n_g * 2 * C;
+  const int r0 = __ldg(B.st_ptr + ck), nr = __ldg(B.st_ptr + ck + 1) - r0;
+  const int p0 = __ldg(B.ck_ptr + ck), p1 = __ldg(B.ck_ptr + ck + 1);
+  const int e0 = __ldg(B.ptr + p0), ne = __ldg(B.ptr + p1) - e0;
+  double* vals = stg + (size_t)B.st_max * C;                           // [blk_max][8]
+  int4* meta = reinterpret_cast<int4*>(vals + (size_t)B.blk_max * 8);  // [blk_max]
+  int4* bmeta = meta + B.blk_max;                                      // [ck_max]
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_addr(&bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const double* lb = w.lblk + (size_t)s * n.n_l * LB_N;
-  const double* bs = w.bs + (size_t)s * BS_N * n_b;
-  const int k1 = min(n_b, (int)(blockIdx.x + 1) * kHvpBusPerCta);
-  // buses in elimination order: a chunk's own θ/v rows are contiguous slab rows.
-  // Lane j holds the metadata of the team's j-th bus (one load for all of them),
-  // and the next bus's incidence records are fetched lane-parallel while this
-  // bus runs, so a line costs one round trip (its slab rows and line block).
-  const unsigned mask = team_mask<W>();
-  const int kb0 = blockIdx.x * kHvpBusPerCta + team;
-  const int nb = k1 > kb0 ? (k1 - kb0 + nteam - 1) / nteam : 0;  // ≤ W (kHvpBusPerCta ≤ W·nteam)
-  int4 mym = make_int4(0, 0, 0, 0);
-  int2 mye = make_int2(0, 0);
-  if (lane < nb) { mym = __ldg(n.hvp_meta + kb0 + lane * nteam); mye = __ldg(n.hvp_inc + kb0 + lane * nteam); }
-  auto shfl4 = [&](int4 v, int src) {
-    return make_int4(__shfl_sync(mask, v.x, src, W), __shfl_sync(mask, v.y, src, W), __shfl_sync(mask, v.z, src, W),
-                     __shfl_sync(mask, v.w, src, W));
-  };
-  int4 recn = make_int4(0, 0, 0, 0);
-  if (nb > 0) {
-    const int e0 = __shfl_sync(mask, mye.x, 0, W), dg = __shfl_sync(mask, mye.y, 0, W);
-    if (lane < dg) recn = __ldg(n.inc_rec + e0 + lane);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    auto bulk = [&](void* dst, const void* src, unsigned bytes) {
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(sm_addr(dst)), "l"(src), "r"(bytes), "r"(sm_addr(&bar)) : "memory");
+    };
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_addr(&bar)),
+                   "r"((unsigned)(nr * C * 8 + ne * (64 + 16) + (p1 - p0) * 16)) : "memory");
+      bulk(vals, (MU ? w.mbval : w.hbval) + ((size_t)s * B.nblk + e0) * 8, ne * 64);
+      bulk(meta, B.meta + e0, ne * 16);
+      bulk(bmeta, B.out + p0, (p1 - p0) * 16);
+    }
+    for (int k = threadIdx.x; k < nr; k += 32) {
+      const int row = __ldg(B.st_row + r0 + k);
+      bulk(stg + (size_t)k * C, row < n.n_x ? X + (size_t)row * C : MU_ + (size_t)(row - n.n_x) * C, C * 8);
+    }
   }
-  for (int jb = 0; jb < nb; ++jb) {
-    const int4 m = shfl4(mym, jb);
-    const int i = m.x, pt = m.y, pvc = m.z, gi_own = m.w;
-    const int e0 = __shfl_sync(mask, mye.x, jb, W), dg = __shfl_sync(mask, mye.y, jb, W);
-    const int pv = pvc >= 0 ? pvc : -1, uv = pvc >= 0 ? -1 : -1 - pvc;
-    const int4 recc = recn;
-    if (jb + 1 < nb) {  // next bus's records
-      const int e0n = __shfl_sync(mask, mye.x, jb + 1, W), dgn = __shfl_sync(mask, mye.y, jb + 1, W);
-      recn = lane < dgn ? __ldg(n.inc_rec + e0n + lane) : make_int4(0, 0, 0, 0);
-    }
-    double dvi[D], dthi[D], mPi[D], mQi[D], hv[D], hth[D];
+  const Dir<C> d = make_dir<C>(n, w, V, col0, N, s, tile, cta, lane);
+  double* Y = w.slabW + cta * n.n_x * C;
+  double* Hs = w.hu + cta * n.n_u * C;
+  const double* bsv = w.bs + (size_t)s * BS_N * n.n_b;
+  {
+    unsigned done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(sm_addr(&bar)) : "memory");
+  }
+  const double2* vv = reinterpret_cast<const double2*>(vals);
+  for (int p = team; p < p1 - p0; p += nteam) {
+    const int4 me = bmeta[p];
+    double ath[CPL], av[CPL];
 #pragma unroll
-    for (int u = 0; u < NT; ++u) {
-      dirs_at<C>(d[u], pt, pvc, dthi + u * CPL, dvi + u * CPL);
-      if (gi_own >= 0) {
-        row_ld<C>(MU[u], 2 * gi_own, lane, mPi + u * CPL);
-        row_ld<C>(MU[u], 2 * gi_own + 1, lane, mQi + u * CPL);
+    for (int j = 0; j < CPL; ++j) { ath[j] = 0.0; av[j] = 0.0; }
+    const int eb = __ldg(B.ptr + p0 + p) - e0, ee = __ldg(B.ptr + p0 + p + 1) - e0;
+    double th_i[CPL];  // dθ of the bus itself (its block comes first)
+    for (int e = eb; e < ee; ++e) {
+      const int4 m = meta[e];
+      const double2 b0 = vv[4 * e], b1 = vv[4 * e + 1];
+      double dth[CPL], dv[CPL];
+      if (m.x >= 0) row_ld<C>(stg, m.x, lane, dth);
+      else
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) dth[j] = 0.0;
+      if (m.y >= 0) row_ld<C>(stg, m.y, lane, dv);
+      else
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) dv[j] = d.vdir(-1 - m.y, j);
+      if (e == eb) {
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) th_i[j] = dth[j];  // the diagonal θ column is Σ_x (k_hvp) or 0 (k_mu)
+      } else {
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) dth[j] -= th_i[j];  // θ columns act on angle differences
       }
-    }
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      if (gi_own < 0) { mPi[k] = 0.0; mQi[k] = 0.0; }
-      hv[k] = 0.0; hth[k] = 0.0;
-    }
-    for (int e = 0; e < dg; ++e) {
-      const int4 rec = e < W ? shfl4(recc, e) : __ldg(n.inc_rec + e0 + e);
-      const bool from = rec.w & 1;
-      const int go = (rec.w >> 1) - 1;
-      double dvo[D], dtho[D], h[6];
-#pragma unroll
-      for (int u = 0; u < NT; ++u) dirs_at<C>(d[u], rec.y, rec.z, dtho + u * CPL, dvo + u * CPL);
-      const double* p = lb + (size_t)rec.x * LB_N;
-      load_h(p, h);
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
-        const double dvf = from ? dvi[k] : dvo[k], dvt = from ? dvo[k] : dvi[k];
-        const double dD = from ? dthi[k] - dtho[k] : dtho[k] - dthi[k];
-        hv[k] += from ? h[0] * dvf + h[1] * dvt + h[2] * dD : h[1] * dvf + h[3] * dvt + h[4] * dD;
-        const double hD = h[2] * dvf + h[4] * dvt + h[5] * dD;
-        hth[k] += from ? hD : -hD;
+      for (int j = 0; j < CPL; ++j) {  // explicit FMAs: the same rounding for every tile width (T3)
+        ath[j] = fma(b0.y, dv[j], fma(b0.x, dth[j], ath[j]));
+        av[j] = fma(b1.y, dv[j], fma(b1.x, dth[j], av[j]));
       }
-    }
-    // Jᵀ μ_A, only on lines touching an r bus — a second pass, so its line block and
-    // far-end μ do not hold registers alongside the first pass's slab rows
-    for (int e = 0; e < dg; ++e) {
-      const int4 rec = e < W ? shfl4(recc, e) : __ldg(n.inc_rec + e0 + e);
-      const bool from = rec.w & 1;
-      const int go = (rec.w >> 1) - 1;
-      if (gi_own < 0 && go < 0) continue;
-      double J[12], mPo[D], mQo[D];
-      load_j(lb + (size_t)rec.x * LB_N, J);
+      if (!MU && m.z >= 0) {  // A_rᵀ μ_A: generator bus j (μ^P, μ^Q rows staged at m.z, m.z + 1)
+        const double2 j0 = vv[4 * e + 2], j1 = vv[4 * e + 3];
+        double mp[CPL], mq[CPL];
+        row_ld<C>(stg, m.z, lane, mp);
+        row_ld<C>(stg, m.z + 1, lane, mq);
 #pragma unroll
-      for (int u = 0; u < NT; ++u) {
-        if (go >= 0) {
-          row_ld<C>(MU[u], 2 * go, lane, mPo + u * CPL);
-          row_ld<C>(MU[u], 2 * go + 1, lane, mQo + u * CPL);
-        } else {
-#pragma unroll
-          for (int j = 0; j < CPL; ++j) { mPo[u * CPL + j] = 0.0; mQo[u * CPL + j] = 0.0; }
+        for (int j = 0; j < CPL; ++j) {
+          ath[j] = fma(j0.y, mq[j], fma(j0.x, mp[j], ath[j]));
+          av[j] = fma(j1.y, mq[j], fma(j1.x, mp[j], av[j]));
         }
       }
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
-        const double mpf = from ? mPi[k] : mPo[k], mqf = from ? mQi[k] : mQo[k];
-        const double mpt = from ? mPo[k] : mPi[k], mqt = from ? mQo[k] : mQi[k];
-        hv[k] += from ? J[0] * mpf + J[3] * mqf + J[6] * mpt + J[9] * mqt
-                      : J[1] * mpf + J[4] * mqf + J[7] * mpt + J[10] * mqt;
-        const double jD = J[2] * mpf + J[5] * mqf + J[8] * mpt + J[11] * mqt;
-        hth[k] += from ? jD : -jD;
-      }
     }
-    const double vi = bs[BS_V * n_b + i], gsh = __ldg(n.gsh + i), bsh = __ldg(n.bsh + i);
-    const double wd2 = bs[BS_WD2 * n_b + i], sxv = bs[BS_SXV * n_b + i], sxt = bs[BS_SXT * n_b + i];
+    if (MU) {  // me = {bus, gen}: μ^P = Σ_rP dP, μ^Q = Σ_rQ dQ
+      const double srp = bsv[BS_SRP * n.n_b + me.x], srq = bsv[BS_SRQ * n.n_b + me.x];
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-      hv[k] += wd2 * dvi[k] + 2.0 * vi * (gsh * mPi[k] - bsh * mQi[k]) + sxv * dvi[k];
-      hth[k] += sxt * dthi[k];
+      for (int j = 0; j < CPL; ++j) { ath[j] *= srp; av[j] *= srq; }
+      row_st<C>(MU_, 2 * me.y, lane, ath);
+      row_st<C>(MU_, 2 * me.y + 1, lane, av);
+    } else {   // me = {bus, θ row, v row or −1−u, gen}
+      if (me.y >= 0) row_st<C>(Y, me.y, lane, ath);
+      if (me.z >= 0) row_st<C>(Y, me.z, lane, av);
+      else row_st<C>(Hs, -1 - me.z, lane, av);
     }
-#pragma unroll
-    for (int u = 0; u < NT; ++u)
-      if (on[u]) {
-        if (pt >= 0) row_st<C>(Y[u], pt, lane, hth + u * CPL);
-        if (pv >= 0) row_st<C>(Y[u], pv, lane, hv + u * CPL);
-        else row_st<C>(Hs[u], uv, lane, hv + u * CPL);
-      }
   }
-  if (blockIdx.x == 0)  // objective curvature on explicit p_g
+  if (!MU && blockIdx.x == 0)  // objective curvature on explicit p_g
     for (int g = team; g < n.n_g; g += nteam) {
       const int up = __ldg(n.u_p + g);
-      if (up >= 0)
+      if (up >= 0) {
+        double o[CPL];
 #pragma unroll
-        for (int u = 0; u < NT; ++u)
-          if (on[u]) {
-            double o[CPL];
-#pragma unroll
-            for (int j = 0; j < CPL; ++j) o[j] = 2.0 * __ldg(n.c_quad + g) * d[u].vdir(up, j);
-            row_st<C>(Hs[u], up, lane, o);
-          }
+        for (int j = 0; j < CPL; ++j) o[j] = 2.0 * __ldg(n.c_quad + g) * d.vdir(up, j);
+        row_st<C>(Hs, up, lane, o);
+      }
     }
+  (void)W;
 }
 
 // ---------------------------------------------------------------- d, e
@@ -964,13 +838,22 @@ __global__ void k_pf_update(DevNet n, Work w, int n_scen, double* __restrict__ v
 
 inline int grid_for(long long n) { return (int)std::max<long long>(1, std::min<long long>(148LL * 16, (n + kThreads - 1) / kThreads)); }
 
+template <int C, bool MU>
+size_t blk_smem(const DevNet& n) {
+  const BlkSet& B = MU ? n.mb : n.hb;
+  const size_t b = (size_t)B.st_max * C * sizeof(double) + (size_t)B.blk_max * 80 + (size_t)B.ck_max * 16;
+  // per device and function, so set on every launch (a host-side call, graph-capture safe)
+  cudaFuncSetAttribute(k_blk<C, MU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+  return b;
+}
+
 template <int C>
 void one_dir_fwd_hvp(const DevNet& n, const Work& w, int n_scen, const double* V, const double* X4, const int* map,
                      int x4ld, bool hvp, cudaStream_t st) {
   k_fwd<C><<<dim3(1, n_scen), kThreads, 0, st>>>(n, w, V, 0, 1, -1, X4, map, x4ld);
   if (!hvp) return;
-  k_mu<C, kMuTiles><<<dim3((n.n_gb + kBusPerCta - 1) / kBusPerCta, 1, n_scen), kThreads, 0, st>>>(n, w, V, 0, 1);
-  k_hvp<C, kHvpTiles><<<dim3((n.n_b + kHvpBusPerCta - 1) / kHvpBusPerCta, 1, n_scen), kThreads, 0, st>>>(n, w, V, 0, 1);
+  k_blk<C, true><<<dim3(n.mb.nchunk, 1, n_scen), kThreads, blk_smem<C, true>(n), st>>>(n, w, V, 0, 1);
+  k_blk<C, false><<<dim3(n.hb.nchunk, 1, n_scen), kThreads, blk_smem<C, false>(n), st>>>(n, w, V, 0, 1);
 }
 
 template <int C>
@@ -1026,11 +909,9 @@ void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int
   const int rt = (V == nullptr && col0 % C == 0) ? col0 / C : -1;  // canonical tile of the call's first tile
   k_fwd<C><<<dim3(ntile, n_scen), kThreads, rt >= 0 ? 2 * n.bmw * sizeof(unsigned) : 0, st>>>(n, w, V, col0, N, rt);
   if (ev) cudaEventRecord(ev[1], st);
-  k_mu<C, kMuTiles><<<dim3((n.n_gb + kBusPerCta - 1) / kBusPerCta, (ntile + kMuTiles - 1) / kMuTiles, n_scen), kThreads,
-                       0, st>>>(n, w, V, col0, N);
+  k_blk<C, true><<<dim3(n.mb.nchunk, ntile, n_scen), kThreads, blk_smem<C, true>(n), st>>>(n, w, V, col0, N);
   if (ev) cudaEventRecord(ev[2], st);
-  k_hvp<C, kHvpTiles><<<dim3((n.n_b + kHvpBusPerCta - 1) / kHvpBusPerCta, (ntile + kHvpTiles - 1) / kHvpTiles, n_scen),
-                        kThreads, 0, st>>>(n, w, V, col0, N);
+  k_blk<C, false><<<dim3(n.hb.nchunk, ntile, n_scen), kThreads, blk_smem<C, false>(n), st>>>(n, w, V, col0, N);
   if (ev) cudaEventRecord(ev[3], st);
   k_adj<C><<<dim3(ntile, n_scen), kThreads, 0, st>>>(n, w, N);
   if (ev) cudaEventRecord(ev[4], st);
@@ -1039,6 +920,12 @@ void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int
 }
 
 }  // namespace
+
+int hvp_stage_rows(int C) {
+  // 48 KB of staged rows per CTA at C = 64 (4 CTAs per SM); narrower tiles stage more rows of
+  // fewer bytes (capped at the same byte budget, at most 4 × the buses of a chunk)
+  return std::min(256, kHvpRowCap64 * 64 / C);
+}
 
 int pick_tile_cols(int n_x, int total_cols) {
   (void)n_x;

