@@ -401,6 +401,20 @@ def main():
             next_rows[name] = {"ms": statistics.mean(ms), "scenarios": S}
         next_rows["pf_condensed_kkt_solve_reg (NEXT-3)"] = {"ms": chol_avg, "trials_max": max(trials),
                                                             "delta_w_max": max(deltas)}
+        # NEXT-4: the LinRed IPM driver (Algorithm 1, host loop over the C-ABI) on case9 to 1e-8
+        from paper_2203_11875_b200.ipm import LinRedIPM
+        from synth import case9
+        from synth.case9 import case9_bounds
+        net9, pt9 = case9()
+        b9, c0 = case9_bounds()
+        solver = LinRedIPM(net9, b9, device=local, tol=1e-8)
+        t0 = time.perf_counter()
+        res = solver.solve(v0=pt9["v"], p_g0=pt9["p_g"])
+        dt_ipm = time.perf_counter() - t0
+        solver.close()
+        next_rows["LinRed IPM (NEXT-4), case9 to 1e-8"] = {
+            "status": res["status"], "iterations": res["iterations"], "objective_usd_per_h": res["objective"] + c0,
+            "published_optimum_usd_per_h": 5296.69, "ms_per_iteration_wall": 1e3 * dt_ipm / max(1, res["iterations"])}
 
     # ------------------------------------------------------------ end-to-end through the public API, host buffers
     e2e = None

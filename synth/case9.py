@@ -28,6 +28,10 @@ _GEN = [
     (2, 163.0, 1.025, 0.085, 1.2),
     (3, 85.0, 1.025, 0.1225, 1.0),
 ]
+# OPF data of case9.m: Pmin, Pmax, Qmin, Qmax (MW, MVAr), constant cost c0 ($/h); Vmin, Vmax
+_GEN_LIM = [(10.0, 250.0, -300.0, 300.0, 150.0), (10.0, 300.0, -300.0, 300.0, 600.0),
+            (10.0, 270.0, -300.0, 300.0, 335.0)]
+_VLIM = (0.9, 1.1)
 _LOAD = {5: (90.0, 30.0), 7: (100.0, 35.0), 9: (125.0, 50.0)}
 
 
@@ -65,3 +69,14 @@ def case9_multipliers(seed=9):
     net, _ = case9()
     cnt = counts(9, net["gen_bus"], net["F_max"])
     return _multipliers(np.random.default_rng(seed), 9, 3, cnt, 9)
+
+
+def case9_bounds():
+    """OPF bounds of MATPOWER case9 in p.u. (NEXT-4), and the constant cost
+    Σ c0 = 1085 $/h the objective f omits (MATPOWER's optimum 5296.69 $/h
+    includes it)."""
+    lim = np.array(_GEN_LIM)
+    b = dict(v_lo=np.full(9, _VLIM[0]), v_hi=np.full(9, _VLIM[1]),
+             p_lo=lim[:, 0] / BASE_MVA, p_hi=lim[:, 1] / BASE_MVA,
+             q_lo=lim[:, 2] / BASE_MVA, q_hi=lim[:, 3] / BASE_MVA)
+    return b, float(lim[:, 4].sum())

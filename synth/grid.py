@@ -210,3 +210,17 @@ def make_scenario(net, base_point, s, seed_base=None):
 def table1_grid(name, seed=None):
     n_b, n_l, n_g = TABLE1[name]
     return make_grid(n_b, n_l, n_g, seed if seed is not None else n_b)
+
+
+def opf_bounds(net, seed=None):
+    """Seeded OPF bounds for a synthetic grid (NEXT-4 tests): v ∈ [0.9, 1.1];
+    generator p_g ∈ [0, p_hi] with capacities drawn so the fleet covers the
+    total load 1.5–2.5×; q_g ∈ [−q_hi, q_hi], q_hi = 0.5 p_hi + 0.3 (p.u.)."""
+    rng = np.random.default_rng((net["seed"] if seed is None else seed) + 77)
+    n_b, n_g = int(net["n_b"]), int(net["n_g"])
+    share = rng.uniform(0.5, 1.5, size=n_g)
+    total = float(np.sum(net["p_d"]))
+    p_hi = share / share.sum() * total * rng.uniform(1.5, 2.5)
+    q_hi = 0.5 * p_hi + 0.3
+    return dict(v_lo=np.full(n_b, 0.9), v_hi=np.full(n_b, 1.1), p_lo=np.zeros(n_g), p_hi=p_hi,
+                q_lo=-q_hi, q_hi=q_hi)
