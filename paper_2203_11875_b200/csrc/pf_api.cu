@@ -158,21 +158,46 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
   for (int r = 0; r < P.n_x; ++r) rowmeta[r] = make_int4(P.lu_ptr[r], P.lu_diag[r], P.lu_ptr[r + 1], P.row_blk[r]);
   d.C = h->C;
   d.lu_maxlen = P.lu_maxlen;
-  // sweep tasks (pf_reduce.cu): each row's packed range includes its diagonal and intra-block entry
+  // Sweep entry streams (pf_reduce.cu run_seq): per block and orientation one contiguous
+  // segment  [row A gathers, m][row B gathers, m (two-row blocks)][{d_A, intra}, {d_B, 0}]
+  // with row A the row solved first (LOWER: θ, UPPER: v) and m = the longer row's gather
+  // count rounded up to even; a short row is padded with {0, a column the block gathers}
+  // (a zero product with a final row).  The task is {r0 | two << 31, segment start, m, 0}.
+  // sw_src says where each slot comes from (k_lu packs the L/U and Lᵀ/Uᵀ value streams):
+  //   {e, -1} gather {v(e), column(e)·C};  {e, -2} pad {0, column(e)·C};
+  //   {a, b ≥ 0} scalars {v(a), v(b)};     {a, -3} scalars {v(a) or 0 if a < 0, 0}
   const int nblk = (int)P.blk_bus.size();
   std::vector<int4> taskL(nblk), taskU(nblk);
-  for (int bi = 0; bi < nblk; ++bi) {
-    int p = P.levL_blk[bi], r0 = P.blk_ptr[p];
-    bool two = P.blk_ptr[p + 1] - r0 == 2;
-    int s0 = P.lu_ptr[r0], c0 = P.lu_diag[r0] - s0 + 1;
-    int s1 = two ? P.lu_ptr[r0 + 1] : 0, c1 = two ? P.lu_diag[r0 + 1] - s1 + 1 : 0;
-    taskL[bi] = make_int4(r0 | (two ? (int)0x80000000u : 0), s0, s1, (c0 << 16) | c1);
-    p = P.levU_blk[bi]; r0 = P.blk_ptr[p];
-    two = P.blk_ptr[p + 1] - r0 == 2;
-    s0 = P.lu_diag[r0]; c0 = P.lu_ptr[r0 + 1] - s0;
-    s1 = two ? P.lu_diag[r0 + 1] : 0; c1 = two ? P.lu_ptr[r0 + 2] - s1 : 0;
-    taskU[bi] = make_int4(r0 | (two ? (int)0x80000000u : 0), s0, s1, (c0 << 16) | c1);
+  std::vector<int2> sw_src;
+  auto segment = [&](int p, bool lower) {
+    const int r0 = P.blk_ptr[p];
+    const bool two = P.blk_ptr[p + 1] - r0 == 2;
+    const int rA = r0 + (!lower && two), rB = r0 + lower;
+    int a0, a1, b0 = 0, b1 = 0, intra = -1;
+    if (lower) {
+      a0 = P.lu_ptr[rA]; a1 = P.lu_diag[rA];
+      if (two) { b0 = P.lu_ptr[rB]; b1 = P.lu_diag[rB] - 1; intra = b1; }
+    } else {
+      a0 = P.lu_diag[rA] + 1; a1 = P.lu_ptr[rA + 1];
+      if (two) { intra = P.lu_diag[rB] + 1; b0 = intra + 1; b1 = P.lu_ptr[rB + 1]; }
+    }
+    if (two && P.lu_idx[intra] != rA) { fprintf(stderr, "pf: intra-block entry missing\n"); abort(); }
+    const int m = (std::max(a1 - a0, b1 - b0) + 1) & ~1;
+    const int any = a1 > a0 ? a0 : b0;  // a gathered column for the pads
+    const int start = (int)sw_src.size();
+    for (int k = 0; k < m; ++k) sw_src.push_back(a0 + k < a1 ? make_int2(a0 + k, -1) : make_int2(any, -2));
+    if (two)
+      for (int k = 0; k < m; ++k) sw_src.push_back(b0 + k < b1 ? make_int2(b0 + k, -1) : make_int2(any, -2));
+    sw_src.push_back(two ? make_int2(P.lu_diag[rA], intra) : make_int2(P.lu_diag[rA], -3));
+    sw_src.push_back(make_int2(two ? P.lu_diag[rB] : -1, -3));
+    return make_int4(r0 | (two ? (int)0x80000000u : 0), start, m, 0);
+  };
+  {
+    std::vector<int4> segL(nblk), segU(nblk);
+    for (int p = 0; p < nblk; ++p) { segL[p] = segment(p, true); segU[p] = segment(p, false); }
+    for (int bi = 0; bi < nblk; ++bi) { taskL[bi] = segL[P.levL_blk[bi]]; taskU[bi] = segU[P.levU_blk[bi]]; }
   }
+  d.nsw = (int)sw_src.size();
   // sparse-RHS reach (pf_dev.cuh): elimination tree of the filled L, then per
   // canonical tile the union of the tree paths from its columns' G_u rows
   std::vector<int> parent(P.n_x, -1);
@@ -442,7 +467,7 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
             up(h, P.guc_src, &d.guc_src) && up(h, P.gur_ptr, &d.gur_ptr) && up(h, P.gur_col, &d.gur_col) &&
             up(h, P.gur_src, &d.gur_src) && up(h, P.bus_pth, &d.bus_pth) && up(h, P.bus_pv, &d.bus_pv) &&
             up(h, gbus, &d.gbus) && up(h, rowmeta, &d.rowmeta) && up(h, hvp_order, &d.hvp_bus) &&
-            up(h, taskL, &d.taskL) && up(h, taskU, &d.taskU) &&
+            up(h, taskL, &d.taskL) && up(h, taskU, &d.taskU) && up(h, sw_src, &d.sw_src) &&
             up(h, taskLr, &d.taskLr) && up(h, levLr_ptr, &d.levLr_ptr) && up(h, rowbm, &d.rowbm) &&
             up(h, taskUa, &d.taskUa) && up(h, levUa_ptr, &d.levUa_ptr) && up(h, h->p1_task, &d.p1_task) &&
             up(h, h->p1_ptr, &d.p1_ptr) && up(h, h->u_top, &d.u_top) && up(h, h->u_top_ptr, &d.u_top_ptr) &&
@@ -456,7 +481,7 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
   w.max_tiles = max_scen * ((max_batch + h->C - 1) / h->C);
   const size_t T = w.max_tiles, C = h->C;
   ok = ok && alloc(h, S * d.nnz_jb, &w.jb) && alloc(h, S * d.nnz_gu, &w.gu) && alloc(h, S * d.nnz_lu, &w.lu) &&
-       alloc(h, S * d.nnz_lu, &w.luT) && alloc(h, S * d.nnz_lu, &w.pkA) && alloc(h, S * d.nnz_lu, &w.pkT) && alloc(h, S * d.nnz_gu, &w.pkG) && alloc(h, S * d.n_x, &w.rowmax) && alloc(h, S * d.n_x, &w.invd) && alloc(h, S * LS_N * d.n_l, &w.ls) &&
+       alloc(h, S * d.nsw, &w.swA) && alloc(h, S * d.nsw, &w.swT) && alloc(h, S * d.nnz_gu, &w.pkG) && alloc(h, S * d.n_x, &w.rowmax) && alloc(h, S * d.n_x, &w.invd) && alloc(h, S * LS_N * d.n_l, &w.ls) &&
        alloc(h, S * BS_N * d.n_b, &w.bs) && alloc(h, S * LB_N * d.n_l, &w.lblk) && alloc(h, S * 4 * d.n_l, &w.sflow) && alloc(h, 2 * S, &w.info) &&
        alloc(h, T * d.n_x * C, &w.slabZ) && alloc(h, T * d.n_x * C, &w.slabW) &&
        alloc(h, T * d.n_u * C, &w.hu) && alloc(h, T * d.n_g * 2 * C, &w.mu) &&
@@ -760,6 +785,13 @@ pf_status pf_condensed_kkt_solve_reg(pf_net* h, int32_t n_scen, double* K, const
   }
   return cuda_check(h, "pf_condensed_kkt_solve_reg");
 }
+
+#ifdef PF_SWEEP_TRACE  // debug builds only (tools/sweep_trace.py)
+int pf_debug_set_sweep_trace(void* dev_ptr) {
+  pf::set_sweep_trace(static_cast<unsigned long long*>(dev_ptr));
+  return 0;
+}
+#endif
 
 #ifdef PF_LU_TRACE  // debug builds only (tools/lu_trace.py)
 int pf_debug_set_lu_trace(void* dev_ptr) {

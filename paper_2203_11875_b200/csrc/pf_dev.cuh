@@ -42,7 +42,9 @@ struct DevNet {
   const int *gbus;              // [n_gb] generator buses ascending (the r buses)
   const int4 *rowmeta;          // [n_x] {lu_ptr[r], lu_diag[r], lu_ptr[r+1], block of r}
   const int *hvp_bus;           // [n_b] buses in elimination order, the reference bus last
-  const int4 *taskL, *taskU;    // [n_blocks] sweep tasks in level order (pf_reduce.cu sweep())
+  const int4 *taskL, *taskU;    // [n_blocks] sweep tasks in level order (pf_reduce.cu sweep()): {r0|two<<31, segment, m, 0}
+  const int2 *sw_src;           // [nsw] source of each sweep-stream slot (pf_api.cu, packed by k_lu)
+  int nsw;
   // Sparse right-hand sides (Gilbert–Peierls reach): for unit directions the L sweep of
   // canonical column tile t (columns [tC, tC+C)) only visits the blocks on the
   // elimination-tree paths from G_u's nonzeros to the root; the Lᵀ sweep of the
@@ -85,9 +87,9 @@ struct Work {
   double* jb;      // [max_scen][nnz_jb]  J_bus values
   double* gu;      // [max_scen][nnz_gu]  G_u values (internal copy)
   double* lu;      // [max_scen][nnz_lu]  LU values (row-wise)
-  double* luT;     // [max_scen][nnz_lu]  transposed values: luT[e] = lu[tpos[e]]
-  double2* pkA;    // [max_scen][nnz_lu]  packed {lu[e] (1/u_rr on the diagonal), bits(idx[e]*C)} for the L / U sweeps
-  double2* pkT;    // [max_scen][nnz_lu]  packed {luT[e] (1/u_rr on the diagonal), bits(idx[e]*C)} for the Uᵀ / Lᵀ sweeps
+  double2* swA;    // [max_scen][nsw]     sweep streams of L (LOWER) / U (UPPER) segments: {value, bits(column·C)} with
+                   //                     1/u_rr for the diagonal, the block scalars {d_A, intra} {d_B, 0} at the end
+  double2* swT;    // [max_scen][nsw]     … the same over the transposed values (Uᵀ LOWER / Lᵀ UPPER)
   double2* pkG;    // [max_scen][nnz_gu]  G_u by column (CSC): {value, bits(row*C)} for the projection
   double* rowmax;  // [max_scen][n_x]     pivot threshold scale (R18)
   double* invd;    // [max_scen][n_x]     1 / u_rr of the factorized rows

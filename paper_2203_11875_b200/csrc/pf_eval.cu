@@ -466,19 +466,28 @@ __global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int CS) {
     }
 #endif
   }
-  double* luT = w.luT + (size_t)s * n.nnz_lu;
-  double2* pkA = w.pkA + (size_t)s * n.nnz_lu;
-  double2* pkT = w.pkT + (size_t)s * n.nnz_lu;
-  // packed sweep entries {value, column·C}; a diagonal entry (its own transpose
-  // position) is packed as 1/u_rr, so the sweeps that divide multiply instead
-  for (int e = gthread; e < n.nnz_lu; e += nthread) {
+  // sweep streams (pf_api.cu segment layout): a diagonal entry (its own transpose position)
+  // is packed as 1/u_rr, so the sweeps that divide multiply instead
+  double2* swA = w.swA + (size_t)s * n.nsw;
+  double2* swT = w.swT + (size_t)s * n.nsw;
+  auto vA = [&](int e) { const double x = __ldcg(lu + e); return __ldg(n.lu_tpos + e) == e ? 1.0 / x : x; };
+  auto vT = [&](int e) {
     const int tp = __ldg(n.lu_tpos + e);
-    const double t = __ldcg(lu + tp);
-    const double c = __longlong_as_double((long long)__ldg(n.lu_idx + e) * n.C);
-    luT[e] = t;
-    const double a = tp == e ? 1.0 / t : __ldcg(lu + e);
-    pkA[e] = make_double2(a, c);
-    pkT[e] = make_double2(tp == e ? a : t, c);
+    return tp == e ? 1.0 / __ldcg(lu + e) : __ldcg(lu + tp);
+  };
+  for (int q = gthread; q < n.nsw; q += nthread) {
+    const int2 src = __ldg(n.sw_src + q);
+    double2 a, t;
+    if (src.y == -1 || src.y == -2) {  // gather / pad: {value or 0, column·C}
+      const double c = __longlong_as_double((long long)__ldg(n.lu_idx + src.x) * n.C);
+      a = make_double2(src.y == -1 ? vA(src.x) : 0.0, c);
+      t = make_double2(src.y == -1 ? vT(src.x) : 0.0, c);
+    } else {                           // block scalars
+      a = make_double2(src.x >= 0 ? vA(src.x) : 0.0, src.y >= 0 ? vA(src.y) : 0.0);
+      t = make_double2(src.x >= 0 ? vT(src.x) : 0.0, src.y >= 0 ? vT(src.y) : 0.0);
+    }
+    swA[q] = a;
+    swT[q] = t;
   }
 }
 

@@ -47,6 +47,9 @@ int hvp_stage_rows(int C);  // slab rows one k_hvp chunk may stage in SMEM (pf_r
 #ifdef PF_LU_TRACE
 void set_lu_trace(unsigned long long* p);  // debug builds: per-level k_lu timestamps
 #endif
+#ifdef PF_SWEEP_TRACE
+void set_sweep_trace(unsigned long long* p);  // debug builds: per-phase sweep timestamps of CTA (0, 0)
+#endif
 size_t chol_tile_doubles(int n_u);  // Cholesky workspaces per scenario (pf_chol.cu)
 size_t chol_flag_ints(int n_u);
 size_t chol_vec_doubles(int n_u);

@@ -27,22 +27,15 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kCH = 64;        // u-columns per transposed output chunk
-#ifndef PF_DOT_W
-#define PF_DOT_W 4
-#endif
 #ifndef PF_SWEEP_MIN_BLOCKS
 #define PF_SWEEP_MIN_BLOCKS 3
 #endif
 constexpr int kSweepMinBlocks = PF_SWEEP_MIN_BLOCKS;  // CTAs per SM the sweep kernels are register-capped for
-constexpr int kDotW = PF_DOT_W;                       // entries per row whose slab loads are issued together
 
 template <int C> struct Geo {
   static constexpr int W = C < 32 ? C : 32;  // team width (lanes)
   static constexpr int CPL = C / W;          // directions per lane
-  static constexpr int DW = CPL > 1 ? (kDotW + 1) / 2 : kDotW;  // entries per load batch (register budget)
 };
-
-__device__ __forceinline__ double2 ldpk(const double2* p) { return __ldg(p); }
 
 // The lanes of this thread's team (W consecutive lanes of the warp): teams of
 // one warp follow different rows, so every shuffle names only its own team.
@@ -57,125 +50,31 @@ __device__ __forceinline__ unsigned team_mask() {
 }
 
 // ---------------------------------------------------------------- sweeps
-// A level-scheduled triangular sweep over bus blocks (1–2 rows each), driven
-// by a per-level task list built on the host (pf_api.cu, one int4 per block):
-//   {r0 | two << 31, start of row 0's entries, start of row 1's, cnt0 << 16 | cnt1}
-// where each row's packed {value, column·C} entries are ONE contiguous range
-// that includes its diagonal and the intra-block entry:
-//   LOWER (L, Uᵀ; strict-lower parts, rows forward):
-//     row 0 (θ): [lower part..., diag]    row 1 (v): [lower part..., (v,θ), diag]
-//   UPPER (U, Lᵀ; strict-upper parts, rows backward):
-//     row 1 (v): [diag, upper part...]    row 0 (θ): [diag, (θ,v), upper part...]
-// The v row of a LOWER block (θ row of an UPPER block) depends on its partner
-// only through the intra entry, applied once the partner is final.  A row's
-// range is fetched lane-parallel (one coalesced load) and broadcast by
-// shuffles; the next block's task and ranges are prefetched while the current
-// block's slab loads (kDotW entries × 2 rows × CPL directions, all issued
-// before the first FMA) are in flight, so a block costs about one round trip.
-struct Task { int r0, s0, s1, c0, c1; bool two; };
+// A level-scheduled triangular sweep over bus blocks (1–2 rows each), driven by
+// per-level task lists built on the host (pf_api.cu): task {r0 | two << 31, s, m, 0}
+// names the block's segment of a sweep stream (w.swA for L / U, w.swT for Uᵀ / Lᵀ):
+//   [row A gathers, m][row B gathers, m (two-row blocks)][{d_A, intra}, {d_B, 0}]
+// of packed {value, column·C} gathers.  Row A is solved first (LOWER — the L and Uᵀ
+// sweeps — the θ row r0; UPPER — U and Lᵀ — the v row r0 + 1); row B depends on it
+// only through the intra entry.  m is even and short rows are padded with zero-valued
+// entries that read a row the block gathers anyway, so the inner loop carries no
+// bounds predicates: per step it issues the slab loads of two entries of each row,
+// then their FMAs, about six instructions per entry.  A segment is copied
+// lane-parallel into the team's SMEM buffer one block ahead (cp.async); the rare
+// segments longer than the buffer are read from global memory.
+struct Task { int r0, s, m; bool two; };
 __device__ __forceinline__ Task unpack(int4 t) {
   Task k;
-  k.r0 = t.x & 0x7fffffff; k.two = (t.x >> 31) & 1;
-  k.s0 = t.y; k.s1 = t.z; k.c0 = t.w >> 16; k.c1 = t.w & 0xffff;
+  k.r0 = t.x & 0x7fffffff; k.two = (t.x >> 31) & 1; k.s = t.y; k.m = t.z;
   return k;
 }
+template <int W> struct Seg { static constexpr int CAP = 2 * W + 2; };  // entries of a buffered segment
 
-__device__ __forceinline__ double2 fetch(const double2* __restrict__ pk, int s, int cnt, int i) {
-  return i < cnt ? ldpk(pk + s + i) : make_double2(0.0, 0.0);
-}
-
-template <int W>
-__device__ __forceinline__ double shv(unsigned mask, double2 q, int e) { return __shfl_sync(mask, q.x, e, W); }
-
-// acc0[j] -= Σ_{k<n0} v0[o0+k] X[c0[o0+k] + lane + W j], acc1 likewise; the
-// entries are held one per lane in q0 / q1 (all within one fetch of ≤ W).
 // With a reach bitmap bm (SMEM, one bit per slab row), rows outside the reach
 // read as 0 (their slab rows were never written).
-__device__ __forceinline__ bool in_reach(const unsigned* bm, int colC, int log2C) {
-  const int r = colC >> log2C;
+__device__ __forceinline__ bool in_reach(const unsigned* bm, unsigned colC, int log2C) {
+  const unsigned r = colC >> log2C;
   return (bm[r >> 5] >> (r & 31)) & 1u;
-}
-
-// Lane l of a team owns the CPL adjacent directions l·CPL … l·CPL + CPL − 1, so a
-// gathered row piece is one 16-byte load for CPL = 2.
-template <int CPL>
-__device__ __forceinline__ void ld_dirs(const double* p, bool ok, double* x) {
-  if constexpr (CPL == 2) {
-    const double2 v = ok ? *reinterpret_cast<const double2*>(p) : make_double2(0.0, 0.0);
-    x[0] = v.x; x[1] = v.y;
-  } else {
-#pragma unroll
-    for (int j = 0; j < CPL; ++j) x[j] = ok ? p[j] : 0.0;
-  }
-}
-
-template <int C>
-__device__ __forceinline__ void dot2(const double* X, unsigned mask, int lane, double2 q0, int o0, int n0,
-                                     double2 q1, int o1, int n1, double* acc0, double* acc1,
-                                     const unsigned* bm = nullptr) {
-  constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL, DW = Geo<C>::DW;
-  constexpr int L2C = C == 8 ? 3 : C == 16 ? 4 : C == 32 ? 5 : 6;
-  const int m = max(n0, n1);
-  for (int e0 = 0; e0 < m; e0 += DW) {
-    double x0[DW][CPL], x1[DW][CPL];
-#pragma unroll
-    for (int k = 0; k < DW; ++k) {
-      const int i0 = (o0 + e0 + k) & (W - 1), i1 = (o1 + e0 + k) & (W - 1);
-      const int c0 = __shfl_sync(mask, __double2loint(q0.y), i0, W);  // column · C (< 2^31)
-      const int c1 = __shfl_sync(mask, __double2loint(q1.y), i1, W);
-      const bool ok0 = e0 + k < n0 && (!bm || in_reach(bm, c0, L2C));
-      const bool ok1 = e0 + k < n1 && (!bm || in_reach(bm, c1, L2C));
-      ld_dirs<CPL>(X + c0 + lane * CPL, ok0, x0[k]);
-      ld_dirs<CPL>(X + c1 + lane * CPL, ok1, x1[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < DW; ++k) {
-      const int i0 = (o0 + e0 + k) & (W - 1), i1 = (o1 + e0 + k) & (W - 1);
-      const double v0 = e0 + k < n0 ? __shfl_sync(mask, q0.x, i0, W) : 0.0;
-      const double v1 = e0 + k < n1 ? __shfl_sync(mask, q1.x, i1, W) : 0.0;
-#pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        acc0[j] -= v0 * x0[k][j];
-        acc1[j] -= v1 * x1[k][j];
-      }
-    }
-  }
-}
-
-// As dot2, with the block's entries in SMEM (e0[i] = entry i of row 0, read as a
-// broadcast): no shuffles, and the prefetched entries hold no registers, so a
-// whole row's gathers (up to DS per batch) are in flight at once.
-#ifndef PF_DOT_S
-#define PF_DOT_S 2
-#endif
-template <int C>
-__device__ __forceinline__ void dot2s(const double* X, int lane, const double2* e0, int n0, const double2* e1, int n1,
-                                      double* acc0, double* acc1, const unsigned* bm = nullptr) {
-  constexpr int CPL = Geo<C>::CPL, DS = PF_DOT_S;
-  constexpr int L2C = C == 8 ? 3 : C == 16 ? 4 : C == 32 ? 5 : 6;
-  const int m = max(n0, n1);
-  for (int b = 0; b < m; b += DS) {
-    double x0[DS][CPL], x1[DS][CPL];
-#pragma unroll
-    for (int k = 0; k < DS; ++k) {
-      const int c0 = b + k < n0 ? __double2loint(e0[b + k].y) : 0;  // column · C (< 2^31)
-      const int c1 = b + k < n1 ? __double2loint(e1[b + k].y) : 0;
-      const bool ok0 = b + k < n0 && (!bm || in_reach(bm, c0, L2C));
-      const bool ok1 = b + k < n1 && (!bm || in_reach(bm, c1, L2C));
-      ld_dirs<CPL>(X + c0 + lane * CPL, ok0, x0[k]);
-      ld_dirs<CPL>(X + c1 + lane * CPL, ok1, x1[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < DS; ++k) {
-      const double v0 = b + k < n0 ? e0[b + k].x : 0.0;
-      const double v1 = b + k < n1 ? e1[b + k].x : 0.0;
-#pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        acc0[j] -= v0 * x0[k][j];
-        acc1[j] -= v1 * x1[k][j];
-      }
-    }
-  }
 }
 
 __device__ __forceinline__ void cp_ent(double2* dst, const double2* src) {
@@ -186,17 +85,78 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N_>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N_) : "memory"); }
 
-// Rows longer than one fetch (separator rows of the L part): acc[j] -= Σ in
-// chunks of W entries, no prefetch.
-template <int C>
-__device__ __forceinline__ void dot_long(const double2* __restrict__ pk, const double* X, unsigned mask, int lane,
-                                         int s, int n, double* acc, const unsigned* bm = nullptr) {
-  constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
-  double dummy[CPL];
-  for (int base = 0; base < n; base += W) {
-    const double2 q = fetch(pk, s + base, n - base, lane);
-    dot2<C>(X, mask, lane, q, 0, min(W, n - base), q, 0, 0, acc, dummy, bm);
+// base + c doubles as one IMAD.WIDE.U32 (the compiler otherwise rebuilds a 64-bit
+// index from lane·CPL + c and scales it: four instructions per gathered entry)
+__device__ __forceinline__ const double* off8(const double* base, unsigned c) {
+  const double* r;
+  asm("mad.wide.u32 %0, %1, 8, %2;" : "=l"(r) : "r"(c), "l"(base));
+  return r;
+}
+
+// Lane l of a team owns the CPL adjacent directions l·CPL … l·CPL + CPL − 1, so a
+// gathered row piece is one 16-byte load for CPL = 2.
+template <int C, bool REACH>
+__device__ __forceinline__ void gather(const double* Xl, double2 q, const unsigned* bm, double* x) {
+  constexpr int CPL = Geo<C>::CPL;
+  constexpr int L2C = C == 8 ? 3 : C == 16 ? 4 : C == 32 ? 5 : 6;
+  const unsigned c = (unsigned)__double2loint(q.y);  // column · C (< 2^31)
+  if (REACH && !in_reach(bm, c, L2C)) {
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) x[j] = 0.0;
+    return;
   }
+  const double* p = off8(Xl, c);
+  if constexpr (CPL == 2) {
+    const double2 v = *reinterpret_cast<const double2*>(p);
+    x[0] = v.x; x[1] = v.y;
+  } else {
+    x[0] = *p;
+  }
+}
+
+// accA[j] −= Σ_{i<m} E(i).x · X[column(E(i)) + lane·CPL + j], in entry order, and for
+// two-row blocks accB likewise over E(m + i).
+template <int C, bool REACH, class EntF>
+__device__ __forceinline__ void dot_seg(const EntF& E, int m, bool two, const double* Xl, const unsigned* bm,
+                                        double* accA, double* accB) {
+  constexpr int CPL = Geo<C>::CPL;
+  if (two) {
+#pragma unroll 1
+    for (int i = 0; i < m; i += 2) {
+      const double2 a0 = E(i), a1 = E(i + 1), b0 = E(m + i), b1 = E(m + i + 1);
+      double xa0[CPL], xa1[CPL], xb0[CPL], xb1[CPL];
+      gather<C, REACH>(Xl, a0, bm, xa0);
+      gather<C, REACH>(Xl, b0, bm, xb0);
+      gather<C, REACH>(Xl, a1, bm, xa1);
+      gather<C, REACH>(Xl, b1, bm, xb1);
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        accA[j] -= a0.x * xa0[j];
+        accB[j] -= b0.x * xb0[j];
+        accA[j] -= a1.x * xa1[j];
+        accB[j] -= b1.x * xb1[j];
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int i = 0; i < m; i += 2) {
+      const double2 a0 = E(i), a1 = E(i + 1);
+      double xa0[CPL], xa1[CPL];
+      gather<C, REACH>(Xl, a0, bm, xa0);
+      gather<C, REACH>(Xl, a1, bm, xa1);
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        accA[j] -= a0.x * xa0[j];
+        accA[j] -= a1.x * xa1[j];
+      }
+    }
+  }
+}
+
+template <int CPL>
+__device__ __forceinline__ void st_dirs(double* p, const double* x) {
+  if constexpr (CPL == 2) *reinterpret_cast<double2*>(p) = make_double2(x[0], x[1]);
+  else *p = x[0];
 }
 
 // Initial row values of a sweep: the slab itself, or (first forward sweep) the
@@ -234,110 +194,74 @@ struct FromRhs {
 
 // One team runs the blocks tasks[first], tasks[first + stride], … < end in
 // order (the blocks of one level, or the team's bottom subtrees in postorder).
-template <int C, bool LOWER, class Init>
+template <int C, bool LOWER, bool REACH, class Init>
 __device__ __forceinline__ void run_seq(const int4* __restrict__ tasks, int first, int end, int stride,
-                                        const double2* __restrict__ pk, double* X, bool divide, int lane,
+                                        const double2* __restrict__ sv, double* X, bool divide, int lane,
                                         double2* ent, const Init& init, const unsigned* bm) {
-  constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL;
+  constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL, CAP = Seg<W>::CAP;
   const unsigned mask = team_mask<W>();
-  auto fits = [](const Task& k) { return k.c0 <= W && k.c1 <= W; };
-  auto fill = [&](const Task& k, double2* e) {  // lane-parallel copy of the block's entry ranges
-    if (lane < k.c0) cp_ent(e + lane, pk + k.s0 + lane);
-    if (k.two && lane < k.c1) cp_ent(e + W + lane, pk + k.s1 + lane);
+  auto len = [](const Task& k) { return k.m * (1 + k.two) + 2; };
+  auto fill = [&](const Task& k, double2* e) {  // lane-parallel copy of the block's segment
+    const int n = len(k);
+    if (n <= CAP)
+      for (int i = lane; i < n; i += W) cp_ent(e + i, sv + k.s + i);
   };
+  const double* Xl = X + lane * CPL;
   int bi = first, buf = 0;
   Task k, nk;
   if (bi < end) {
     k = unpack(__ldg(tasks + bi));
-    if (fits(k)) fill(k, ent);
+    fill(k, ent);
     cp_commit();
     if (bi + stride < end) nk = unpack(__ldg(tasks + bi + stride));
   }
   for (; bi < end; bi += stride) {
-    const bool hn = bi + stride < end;
-    if (hn && fits(nk)) fill(nk, ent + (buf ^ 1) * 2 * W);  // next block's entries in flight
+    if (bi + stride < end) fill(nk, ent + (buf ^ 1) * CAP);  // next block's segment in flight
     cp_commit();
     Task nnk = nk;
     if (bi + 2 * stride < end) nnk = unpack(__ldg(tasks + bi + 2 * stride));
-    double* x0p = X + (size_t)k.r0 * C + lane * CPL;
-    double* x1p = x0p + C;
-    double a0[CPL], a1[CPL];
+    const int rA = k.r0 + (!LOWER && k.two), rB = k.r0 + (LOWER ? 1 : 0);
+    double* xa = X + (size_t)rA * C + lane * CPL;
+    double* xb = X + (size_t)rB * C + lane * CPL;
+    double aA[CPL], aB[CPL];
     if constexpr (std::is_same<Init, FromSlab>::value) {
 #pragma unroll
-      for (int j = 0; j < CPL; ++j) { a0[j] = x0p[j]; a1[j] = k.two ? x1p[j] : 0.0; }
+      for (int j = 0; j < CPL; ++j) { aA[j] = xa[j]; aB[j] = k.two ? xb[j] : 0.0; }
     } else if constexpr (std::is_same<Init, FromSlabReach>::value || std::is_same<Init, FromSlabMarked>::value) {
-      const bool in0 = (init.bm[k.r0 >> 5] >> (k.r0 & 31)) & 1u;
-      const bool in1 = k.two && ((init.bm[(k.r0 + 1) >> 5] >> ((k.r0 + 1) & 31)) & 1u);
+      const bool inA = (init.bm[rA >> 5] >> (rA & 31)) & 1u;
+      const bool inB = k.two && ((init.bm[rB >> 5] >> (rB & 31)) & 1u);
 #pragma unroll
-      for (int j = 0; j < CPL; ++j) { a0[j] = in0 ? x0p[j] : 0.0; a1[j] = in1 ? x1p[j] : 0.0; }
+      for (int j = 0; j < CPL; ++j) { aA[j] = inA ? xa[j] : 0.0; aB[j] = inB ? xb[j] : 0.0; }
     } else {
-      init(k.r0, a0);
+      init(rA, aA);
       if (k.two) {
-        init(k.r0 + 1, a1);
+        init(rB, aB);
       } else {
 #pragma unroll
-        for (int j = 0; j < CPL; ++j) a1[j] = 0.0;
+        for (int j = 0; j < CPL; ++j) aB[j] = 0.0;
       }
     }
-    cp_wait<1>();  // this block's entries have landed (this lane's copies) …
+    cp_wait<1>();      // this block's segment has landed (this lane's copies) …
     __syncwarp(mask);  // … and every lane's
-    const double2* e0 = ent + buf * 2 * W;
-    const double2* e1 = e0 + W;
-    const bool f = fits(k);
-    if (LOWER) {
-      const int n0 = k.c0 - 1, n1 = k.two ? k.c1 - 2 : 0;      // entries before diag / intra
-      if (f) {
-        dot2s<C>(X, lane, e0, n0, e1, n1, a0, a1, bm);
-      } else {
-        dot_long<C>(pk, X, mask, lane, k.s0, n0, a0, bm);
-        if (k.two) dot_long<C>(pk, X, mask, lane, k.s1, n1, a1, bm);
-      }
-      const double d0 = f ? e0[k.c0 - 1].x : ldpk(pk + k.s0 + k.c0 - 1).x;
-      double intra = 0.0, d1 = 1.0;
-      if (k.two) {
-        intra = f ? e1[k.c1 - 2].x : ldpk(pk + k.s1 + k.c1 - 2).x;
-        d1 = f ? e1[k.c1 - 1].x : ldpk(pk + k.s1 + k.c1 - 1).x;
-      }
-#pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        double x0 = a0[j];
-        if (divide) x0 *= d0;
-        x0p[j] = x0;
-        if (k.two) {
-          double x1 = a1[j] - intra * x0;
-          if (divide) x1 *= d1;
-          x1p[j] = x1;
-        }
-      }
+    const int n = len(k);
+    double2 sc0, sc1;  // {d_A, intra}, {d_B, 0}
+    if (n <= CAP) {
+      const double2* es = ent + buf * CAP;
+      dot_seg<C, REACH>([&](int i) { return es[i]; }, k.m, k.two, Xl, bm, aA, aB);
+      sc0 = es[n - 2]; sc1 = es[n - 1];
     } else {
-      // row 1 = [diag, U...], row 0 = [diag, intra?, U...]
-      const int o0 = k.two ? 2 : 1;
-      const int n0 = k.c0 - o0, n1 = k.two ? k.c1 - 1 : 0;
-      if (f) {
-        dot2s<C>(X, lane, e0 + o0, n0, e1 + 1, n1, a0, a1);
-      } else {
-        dot_long<C>(pk, X, mask, lane, k.s0 + o0, n0, a0);
-        if (k.two) dot_long<C>(pk, X, mask, lane, k.s1 + 1, n1, a1);
-      }
-      const double d0 = f ? e0[0].x : ldpk(pk + k.s0).x;
-      double intra = 0.0, d1 = 1.0;
-      if (k.two) {
-        intra = f ? e0[1].x : ldpk(pk + k.s0 + 1).x;
-        d1 = f ? e1[0].x : ldpk(pk + k.s1).x;
-      }
-#pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        double x1 = 0.0;
-        if (k.two) {
-          x1 = a1[j];
-          if (divide) x1 *= d1;
-          x1p[j] = x1;
-        }
-        double x0 = a0[j] - intra * x1;
-        if (divide) x0 *= d0;
-        x0p[j] = x0;
-      }
+      const double2* eg = sv + k.s;
+      dot_seg<C, REACH>([&](int i) { return __ldg(eg + i); }, k.m, k.two, Xl, bm, aA, aB);
+      sc0 = __ldg(eg + n - 2); sc1 = __ldg(eg + n - 1);
     }
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      if (divide) aA[j] *= sc0.x;
+      aB[j] -= sc0.y * aA[j];
+      if (divide) aB[j] *= sc1.x;
+    }
+    st_dirs<CPL>(xa, aA);
+    if (k.two) st_dirs<CPL>(xb, aB);
     __syncwarp(mask);  // every lane is done with this buffer before it is refilled
     buf ^= 1;
     k = nk;
@@ -346,31 +270,46 @@ __device__ __forceinline__ void run_seq(const int4* __restrict__ tasks, int firs
   cp_wait<0>();
 }
 
-// A level-scheduled triangular sweep.  With a phase-1 list (p1, p1ptr) the
-// bottom levels < lev0 are run first without barriers, each team walking its
-// own bottom subtrees in postorder (every row a LOWER row gathers is a
-// descendant, so a subtree is self-contained and its rows are re-read while
-// still in L2); the levels ≥ lev0 then run level by level.
-template <int C, bool LOWER, class Init = FromSlab>
+#ifdef PF_SWEEP_TRACE
+__device__ unsigned long long* g_sw_trace;  // tools/sweep_trace.py: [sweep slot][512] globaltimer stamps of CTA (0, 0)
+__device__ __forceinline__ void sw_stamp(int tr, int ev) {
+  if (tr >= 0 && g_sw_trace && blockIdx.x == 0 && blockIdx.y == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_sw_trace[tr * 512 + ev] = t;
+  }
+}
+#define SW_STAMP(ev) sw_stamp(tr, ev)
+#else
+#define SW_STAMP(ev) (void)0
+#endif
+
+template <int C, bool LOWER, bool REACH = false, class Init = FromSlab>
 __device__ __forceinline__ void sweep(const int4* __restrict__ tasks, const int* __restrict__ lptr, int nlev,
                                       const double2* __restrict__ pk, double* X, bool divide, int lane, int team,
                                       int nteam, double2* ent, Init init = Init(), const unsigned* bm = nullptr,
                                       const int4* __restrict__ p1 = nullptr, const int* __restrict__ p1ptr = nullptr,
-                                      int lev0 = 0) {
+                                      int lev0 = 0, int tr = -1) {
+  (void)tr;
+  if (threadIdx.x == 0) SW_STAMP(0);
   // LOWER: bottom subtrees (children first), then the levels ≥ lev0.  UPPER: the
   // given (top) levels, then the bottom subtrees (parents first).
   if (LOWER && p1) {
-    run_seq<C, LOWER>(p1, __ldg(p1ptr + team), __ldg(p1ptr + team + 1), 1, pk, X, divide, lane, ent, init, bm);
+    run_seq<C, LOWER, REACH>(p1, __ldg(p1ptr + team), __ldg(p1ptr + team + 1), 1, pk, X, divide, lane, ent, init, bm);
+    if (lane == 0) SW_STAMP(1 + team);
     __syncthreads();
   }
   for (int lev = (LOWER && p1) ? lev0 : 0; lev < nlev; ++lev) {
-    run_seq<C, LOWER>(tasks, __ldg(lptr + lev) + team, __ldg(lptr + lev + 1), nteam, pk, X, divide, lane, ent, init, bm);
+    run_seq<C, LOWER, REACH>(tasks, __ldg(lptr + lev) + team, __ldg(lptr + lev + 1), nteam, pk, X, divide, lane, ent, init, bm);
     __syncthreads();
+    if (threadIdx.x == 0) SW_STAMP(64 + lev);
   }
   if (!LOWER && p1) {
-    run_seq<C, LOWER>(p1, __ldg(p1ptr + team), __ldg(p1ptr + team + 1), 1, pk, X, divide, lane, ent, init, bm);
+    run_seq<C, LOWER, REACH>(p1, __ldg(p1ptr + team), __ldg(p1ptr + team + 1), 1, pk, X, divide, lane, ent, init, bm);
+    if (lane == 0) SW_STAMP(1 + team);
     __syncthreads();
   }
+  if (threadIdx.x == 0) SW_STAMP(511);
 }
 
 // ---------------------------------------------------------------- directions in bus space
@@ -429,13 +368,15 @@ __device__ __forceinline__ void row_st(double* S, int r, int lane, const double*
 }
 
 // ---------------------------------------------------------------- a, b
-template <int C>
+// RT: unit directions from canonical tile rt (sparse right-hand sides, reach-restricted L sweep);
+// otherwise dense V (or V = 0 with the extra right-hand side X4) and full sweeps.
+template <int C, bool RT>
 __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Work w, const double* __restrict__ V, int col0,
                                                                    int N, int rt, const double* __restrict__ X4 = nullptr,
                                                                    const int* __restrict__ x4map = nullptr, int x4ld = 0) {
   constexpr int W = Geo<C>::W;
   extern __shared__ unsigned bm_sm[];  // reach bitmap of this tile (rt ≥ 0)
-  __shared__ __align__(16) double2 ent_sm[kThreads / Geo<C>::W][2][2][Geo<C>::W];  // per-team entry buffers
+  __shared__ __align__(16) double2 ent_sm[kThreads / Geo<C>::W][2][Seg<Geo<C>::W>::CAP];  // per-team segment buffers
   const int ntile = (N + C - 1) / C;
   const int tile = blockIdx.x, s = blockIdx.y;
   const size_t cta = (size_t)s * ntile + tile;
@@ -444,15 +385,9 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
   const int n_x = n.n_x, n_u = n.n_u;
   double* X = w.slabZ + cta * n_x * C;
   const double* gu = w.gu + (size_t)s * n.nnz_gu;
-  const double2* pk = w.pkA + (size_t)s * n.nnz_lu;
-  double2* ent = &ent_sm[team][0][0][0];
-  // A7.1 fused into the first sweep: B = −P G_u V row by row (unit V: G_u's column col0 + j)
-  FromRhs<C> rhs;
-  rhs.gur_ptr = n.gur_ptr; rhs.gur_col = n.gur_col; rhs.gur_src = n.gur_src; rhs.gu = gu;
-  rhs.Vs = V ? V + ((size_t)s * N + tile * C + lane * Geo<C>::CPL) * n_u : nullptr;
-  rhs.base = col0 + tile * C; rhs.nvalid = nvalid; rhs.n_u = n_u; rhs.lane = lane;
-  rhs.X4 = X4 ? X4 + (size_t)s * x4ld : nullptr; rhs.x4map = x4map;
-  if (rt >= 0) {
+  const double2* pk = w.swA + (size_t)s * n.nsw;
+  double2* ent = &ent_sm[team][0][0];
+  if constexpr (RT) {
     // sparse RHS: only the tile's reach (tree paths of its columns' G_u rows) is nonzero
     const unsigned* bmg = n.rowbm + (size_t)(rt + tile) * n.bmw;
     unsigned* rhs_sm = bm_sm + n.bmw;  // rows of B with a nonzero in this tile
@@ -473,11 +408,17 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
       for (int e = __ldg(n.guc_ptr + base + c) + lane; e < __ldg(n.guc_ptr + base + c + 1); e += W)
         X[(size_t)__ldg(n.guc_row + e) * C + c] = -gu[__ldg(n.guc_src + e)];
     __syncthreads();
-    sweep<C, true>(n.taskLr, n.levLr_ptr + (size_t)(rt + tile) * (n.nlevL + 1), n.nlevL, pk, X, false, lane, team,
-                   nteam, ent, FromSlabMarked{rhs_sm}, bm_sm);                                   // L^{-1} B
+    sweep<C, true, true>(n.taskLr, n.levLr_ptr + (size_t)(rt + tile) * (n.nlevL + 1), n.nlevL, pk, X, false, lane, team,
+                   nteam, ent, FromSlabMarked{rhs_sm}, bm_sm, nullptr, nullptr, 0, 0);                                   // L^{-1} B
     sweep<C, false>(n.u_top, n.u_top_ptr, n.nlevU, pk, X, true, lane, team, nteam, ent, FromSlabReach{bm_sm}, nullptr,
-                    n.u_bot, n.u_bot_ptr);                                                 // U^{-1}
+                    n.u_bot, n.u_bot_ptr, 0, 1);                                                 // U^{-1}
   } else {
+    // A7.1 fused into the first sweep: B = −P G_u V row by row (unit V: G_u's column col0 + j)
+    FromRhs<C> rhs;
+    rhs.gur_ptr = n.gur_ptr; rhs.gur_col = n.gur_col; rhs.gur_src = n.gur_src; rhs.gu = gu;
+    rhs.Vs = V ? V + ((size_t)s * N + tile * C + lane * Geo<C>::CPL) * n_u : nullptr;
+    rhs.base = col0 + tile * C; rhs.nvalid = nvalid; rhs.n_u = n_u; rhs.lane = lane;
+    rhs.X4 = X4 ? X4 + (size_t)s * x4ld : nullptr; rhs.x4map = x4map;
     sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, X, false, lane, team, nteam, ent, rhs, nullptr, n.p1_task,
                    n.p1_ptr, n.p1_lev0);                                                  // L^{-1} B
     sweep<C, false>(n.u_top, n.u_top_ptr, n.nlevU, pk, X, true, lane, team, nteam, ent, FromSlab(), nullptr, n.u_bot,
@@ -628,16 +569,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_blk(DevNet n, Work w, const dou
 template <int C>
 __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_adj(DevNet n, Work w, int N, bool full = false) {
   constexpr int W = Geo<C>::W;
-  __shared__ __align__(16) double2 sm_adj[(kThreads / W) * 4 * W];  // the sweeps' per-team entry buffers
+  __shared__ __align__(16) double2 sm_adj[(kThreads / W) * 2 * Seg<W>::CAP];  // the sweeps' per-team segment buffers
   const int ntile = (N + C - 1) / C;
   const int tile = blockIdx.x, s = blockIdx.y;
   const size_t cta = (size_t)s * ntile + tile;
   const int lane = threadIdx.x % W, team = threadIdx.x / W, nteam = blockDim.x / W;
   double* Y = w.slabW + cta * n.n_x * C;
-  const double2* pk = w.pkT + (size_t)s * n.nnz_lu;
-  double2* ent = sm_adj + (size_t)team * 4 * W;
+  const double2* pk = w.swT + (size_t)s * n.nsw;
+  double2* ent = sm_adj + (size_t)team * 2 * Seg<W>::CAP;
   sweep<C, true>(n.taskL, n.levL_ptr, n.nlevL, pk, Y, true, lane, team, nteam, ent, FromSlab(), nullptr, n.p1_task,
-                 n.p1_ptr, n.p1_lev0);                                                  // U^{-T}
+                 n.p1_ptr, n.p1_lev0, 2);                                                 // U^{-T}
   // L^{-T}: only the ancestors of G_u's rows (the projection reads Ψ there), or every row
   // when the whole Ψ is an output (adjoint step / multipliers)
   if (full)
@@ -645,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_adj(DevNet n, Wor
                     n.u_bot_ptr);
   else
     sweep<C, false>(n.ua_top, n.ua_top_ptr, n.nlevU, pk, Y, false, lane, team, nteam, ent, FromSlab(), nullptr, n.ua_bot,
-                    n.ua_bot_ptr);
+                    n.ua_bot_ptr, 0, 3);
 }
 
 // G_u of each scenario in column (CSC) order, packed {value, row·C} for the projection
@@ -850,7 +791,7 @@ size_t blk_smem(const DevNet& n) {
 template <int C>
 void one_dir_fwd_hvp(const DevNet& n, const Work& w, int n_scen, const double* V, const double* X4, const int* map,
                      int x4ld, bool hvp, cudaStream_t st) {
-  k_fwd<C><<<dim3(1, n_scen), kThreads, 0, st>>>(n, w, V, 0, 1, -1, X4, map, x4ld);
+  k_fwd<C, false><<<dim3(1, n_scen), kThreads, 0, st>>>(n, w, V, 0, 1, -1, X4, map, x4ld);
   if (!hvp) return;
   k_blk<C, true><<<dim3(n.mb.nchunk, 1, n_scen), kThreads, blk_smem<C, true>(n), st>>>(n, w, V, 0, 1);
   k_blk<C, false><<<dim3(n.hb.nchunk, 1, n_scen), kThreads, blk_smem<C, false>(n), st>>>(n, w, V, 0, 1);
@@ -907,7 +848,13 @@ void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int
               st>>>(n, w, n_scen);
   if (ev) cudaEventRecord(ev[0], st);
   const int rt = (V == nullptr && col0 % C == 0) ? col0 / C : -1;  // canonical tile of the call's first tile
-  k_fwd<C><<<dim3(ntile, n_scen), kThreads, rt >= 0 ? 2 * n.bmw * sizeof(unsigned) : 0, st>>>(n, w, V, col0, N, rt);
+#ifdef PF_SWEEP_CARVEOUT  // experiment: SMEM carve-out of the sweep kernels (L1 size)
+  cudaFuncSetAttribute(k_fwd<C, true>, cudaFuncAttributePreferredSharedMemoryCarveout, PF_SWEEP_CARVEOUT);
+  cudaFuncSetAttribute(k_fwd<C, false>, cudaFuncAttributePreferredSharedMemoryCarveout, PF_SWEEP_CARVEOUT);
+  cudaFuncSetAttribute(k_adj<C>, cudaFuncAttributePreferredSharedMemoryCarveout, PF_SWEEP_CARVEOUT);
+#endif
+  if (rt >= 0) k_fwd<C, true><<<dim3(ntile, n_scen), kThreads, 2 * n.bmw * sizeof(unsigned), st>>>(n, w, V, col0, N, rt);
+  else k_fwd<C, false><<<dim3(ntile, n_scen), kThreads, 0, st>>>(n, w, V, col0, N, rt);
   if (ev) cudaEventRecord(ev[1], st);
   k_blk<C, true><<<dim3(n.mb.nchunk, ntile, n_scen), kThreads, blk_smem<C, true>(n), st>>>(n, w, V, col0, N);
   if (ev) cudaEventRecord(ev[2], st);
@@ -979,6 +926,10 @@ int launch_newton_step(const DevNet& n, const Work& w, int C, int n_scen, double
     default: return newton_step<8>(n, w, n_scen, v, th, st);
   }
 }
+
+#ifdef PF_SWEEP_TRACE
+void set_sweep_trace(unsigned long long* p) { cudaMemcpyToSymbol(g_sw_trace, &p, sizeof(p)); }
+#endif
 
 int launch_reduce(const DevNet& n, const Work& w, int C, int n_scen, const double* V, int col0,
                   int N, double* KV, cudaStream_t st, cudaEvent_t* ev) {
