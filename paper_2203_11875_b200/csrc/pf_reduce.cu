@@ -114,40 +114,79 @@ __device__ __forceinline__ void gather(const double* Xl, double2 q, const unsign
   }
 }
 
-// accA[j] −= Σ_{i<m} E(i).x · X[column(E(i)) + lane·CPL + j], in entry order, and for
-// two-row blocks accB likewise over E(m + i).
-template <int C, bool REACH, class EntF>
-__device__ __forceinline__ void dot_seg(const EntF& E, int m, bool two, const double* Xl, const unsigned* bm,
+// Segment entry i: its column·C (the low word of .y) and its value, read separately so
+// a gather in flight holds only its data registers.  G: the segment is in global memory.
+template <bool G>
+__device__ __forceinline__ unsigned ent_col(const double2* e, int i) {
+  const int* p = reinterpret_cast<const int*>(e) + 4 * i + 2;
+  return (unsigned)(G ? __ldg(p) : *p);
+}
+template <bool G>
+__device__ __forceinline__ double ent_val(const double2* e, int i) {
+  const double* p = reinterpret_cast<const double*>(e) + 2 * i;
+  return G ? __ldg(p) : *p;
+}
+
+template <int C, bool REACH>
+__device__ __forceinline__ void gather_c(const double* Xl, unsigned c, const unsigned* bm, double* x) {
+  gather<C, REACH>(Xl, make_double2(0.0, __hiloint2double(0, (int)c)), bm, x);
+}
+
+// accA[j] −= Σ_{i<m} v_i · X[column_i + lane·CPL + j] over the entries e[0, m) in order, and
+// for two-row blocks accB likewise over e[m, 2m) (m even).  Four entries of each row per
+// step: all their slab loads are issued before the first FMA (one memory round trip per step).
+template <int C, bool REACH, bool G>
+__device__ __forceinline__ void dot_seg(const double2* e, int m, bool two, const double* Xl, const unsigned* bm,
                                         double* accA, double* accB) {
   constexpr int CPL = Geo<C>::CPL;
+  int i = 0;
   if (two) {
 #pragma unroll 1
-    for (int i = 0; i < m; i += 2) {
-      const double2 a0 = E(i), a1 = E(i + 1), b0 = E(m + i), b1 = E(m + i + 1);
-      double xa0[CPL], xa1[CPL], xb0[CPL], xb1[CPL];
-      gather<C, REACH>(Xl, a0, bm, xa0);
-      gather<C, REACH>(Xl, b0, bm, xb0);
-      gather<C, REACH>(Xl, a1, bm, xa1);
-      gather<C, REACH>(Xl, b1, bm, xb1);
+    for (; i + 4 <= m; i += 4) {
+      double xa[4][CPL], xb[4][CPL];
 #pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        accA[j] -= a0.x * xa0[j];
-        accB[j] -= b0.x * xb0[j];
-        accA[j] -= a1.x * xa1[j];
-        accB[j] -= b1.x * xb1[j];
+      for (int k = 0; k < 4; ++k) {
+        gather_c<C, REACH>(Xl, ent_col<G>(e, i + k), bm, xa[k]);
+        gather_c<C, REACH>(Xl, ent_col<G>(e, m + i + k), bm, xb[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double va = ent_val<G>(e, i + k), vb = ent_val<G>(e, m + i + k);
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+          accA[j] -= va * xa[k][j];
+          accB[j] -= vb * xb[k][j];
+        }
+      }
+    }
+    if (i < m) {  // m is even: one pair left
+      double xa[2][CPL], xb[2][CPL];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        gather_c<C, REACH>(Xl, ent_col<G>(e, i + k), bm, xa[k]);
+        gather_c<C, REACH>(Xl, ent_col<G>(e, m + i + k), bm, xb[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double va = ent_val<G>(e, i + k), vb = ent_val<G>(e, m + i + k);
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+          accA[j] -= va * xa[k][j];
+          accB[j] -= vb * xb[k][j];
+        }
       }
     }
   } else {
 #pragma unroll 1
-    for (int i = 0; i < m; i += 2) {
-      const double2 a0 = E(i), a1 = E(i + 1);
-      double xa0[CPL], xa1[CPL];
-      gather<C, REACH>(Xl, a0, bm, xa0);
-      gather<C, REACH>(Xl, a1, bm, xa1);
+    for (; i < m; i += 2) {
+      double xa[2][CPL];
 #pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        accA[j] -= a0.x * xa0[j];
-        accA[j] -= a1.x * xa1[j];
+      for (int k = 0; k < 2; ++k) gather_c<C, REACH>(Xl, ent_col<G>(e, i + k), bm, xa[k]);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double va = ent_val<G>(e, i + k);
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) accA[j] -= va * xa[k][j];
       }
     }
   }
@@ -247,11 +286,11 @@ __device__ __forceinline__ void run_seq(const int4* __restrict__ tasks, int firs
     double2 sc0, sc1;  // {d_A, intra}, {d_B, 0}
     if (n <= CAP) {
       const double2* es = ent + buf * CAP;
-      dot_seg<C, REACH>([&](int i) { return es[i]; }, k.m, k.two, Xl, bm, aA, aB);
+      dot_seg<C, REACH, false>(es, k.m, k.two, Xl, bm, aA, aB);
       sc0 = es[n - 2]; sc1 = es[n - 1];
     } else {
       const double2* eg = sv + k.s;
-      dot_seg<C, REACH>([&](int i) { return __ldg(eg + i); }, k.m, k.two, Xl, bm, aA, aB);
+      dot_seg<C, REACH, true>(eg, k.m, k.two, Xl, bm, aA, aB);
       sc0 = __ldg(eg + n - 2); sc1 = __ldg(eg + n - 1);
     }
 #pragma unroll
