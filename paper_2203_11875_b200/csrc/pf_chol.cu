@@ -16,10 +16,12 @@
 //     tile (i, j)  C = A_ij − Σ_{k<j} L_ik L_jkᵀ  (left-looking; DMMA m8n8k4 f64 —
 //                  tcgen05 has no kind::f64 — operands streamed by cp.async.bulk
 //                  through a 3-stage mbarrier ring), then
-//                  i = j: L_jj = chol(C)  (unscaled LDLᵀ, one row per thread, info);
-//                  i > j: L_ij = C L_jj^{-T} (4 threads per row, no barriers).
-//     fwd j        y_j = L_jj^{-1}(b_j − Σ_{k<j} L_jk y_k)   (runs during the factorization)
-//     bwd j        p_j = L_jj^{-T}(y_j − Σ_{i>j} L_ijᵀ p_i)
+//                  i = j: L_jj = chol(C) (blocked, info) and L_jj⁻¹ (block triangular
+//                         inversion), stored beside the tiles;
+//                  i > j: L_ij = C L_jj⁻ᵀ as one more DMMA tile product (L_jj⁻¹ streamed
+//                         in as the task's last ring chunk).
+//     fwd j        y_j = L_jj⁻¹(b_j − Σ_{k<j} L_jk y_k)   (runs during the factorization)
+//     bwd j        p_j = L_jj⁻ᵀ(y_j − Σ_{i>j} L_ijᵀ p_i)   (GEMVs with the stored inverse)
 //   k_chol_unpack  L back into K (column-major, strict upper zeroed).
 // The critical path is ~3 short tile steps per block column, instead of one
 // launch-separated panel per column; every tile's arithmetic order is fixed,
@@ -65,6 +67,8 @@ constexpr int kMaxSm = 1024;
 constexpr int kLook = PF_CHOL_LOOK;  // look-ahead band of the task order (k_chol_dag)
 
 __host__ __device__ __forceinline__ int tidx(int nt, int i, int j) { return j * nt - j * (j - 1) / 2 + (i - j); }
+// tiles per scenario: the ntri packed lower tiles of K_cond / L, then the nt inverses L_jj⁻¹
+__host__ __device__ __forceinline__ size_t tstride(int nt) { return (size_t)nt * (nt + 1) / 2 + nt; }
 
 __device__ __forceinline__ unsigned saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -134,7 +138,7 @@ __global__ void __launch_bounds__(256) k_chol_pack(int n, int nt, const double* 
   while (t >= nt - J) { t -= nt - J; ++J; }
   const int I = J + t;
   const double* A = K + (size_t)sr * n * n;
-  double* T = tiles + ((size_t)s * ntri + tidx(nt, I, J)) * TILE_D;
+  double* T = tiles + ((size_t)s * tstride(nt) + tidx(nt, I, J)) * TILE_D;
   for (int ch = 0; ch < NB; ch += 32) {
     {
       const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 × 4
@@ -179,10 +183,10 @@ __global__ void __launch_bounds__(256) k_chol_pack(int n, int nt, const double* 
 __global__ void __launch_bounds__(256) k_chol_unpack(int n, int nt, const double* __restrict__ tiles,
                                                      double* __restrict__ K, const int* __restrict__ info,
                                                      const int* __restrict__ sidx) {
-  const int s = blockIdx.z, I = blockIdx.x, J = blockIdx.y, ntri = nt * (nt + 1) / 2;
+  const int s = blockIdx.z, I = blockIdx.x, J = blockIdx.y;
   if (info[s] != 0) return;
   double* A = K + (size_t)(sidx ? sidx[s] : s) * n * n;
-  const double* T = I >= J ? tiles + ((size_t)s * ntri + tidx(nt, I, J)) * TILE_D : nullptr;
+  const double* T = I >= J ? tiles + ((size_t)s * tstride(nt) + tidx(nt, I, J)) * TILE_D : nullptr;
   const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
   for (int c = ty; c < NB; c += 4) {
     const int R = I * NB + tx, C = J * NB + c;
@@ -263,19 +267,20 @@ struct TaskCtx {
   double* T;  // tiles of scenario s
   int* F;     // flags of scenario s
   __device__ const double* tile(int r, int c) const { return T + (size_t)tidx(a->nt, r, c) * TILE_D; }
+  __device__ const double* linv(int c) const { return T + (size_t)(a->ntri + c) * TILE_D; }  // L_cc⁻¹
   __device__ int* tflag(int r, int c) const { return F + tidx(a->nt, r, c); }
   __device__ int* fwdflag(int k) const { return F + a->ntri + k; }
   __device__ int* bwdflag(int k) const { return F + a->ntri + a->nt + k; }
 };
 
 // ---- producer: the operand stream of each task kind
-// L_jj into `dst` (epilogue area) once every ring chunk of the task is consumed
-__device__ void prod_ljj(const TaskCtx& t, Pipe& p, double* dst) {
+// L_jj (or, inv, L_jj⁻¹) into `dst` (epilogue area) once every ring chunk of the task is consumed
+__device__ void prod_ljj(const TaskCtx& t, Pipe& p, double* dst, bool inv = false) {
   for (unsigned c = p.cc >= NST ? p.cc - NST : 0; c < p.cc; ++c) mbar_wait(p.empty + c % NST, (c / NST) & 1);
   wait_flag(t.tflag(t.j, t.j));
   fence_proxy_global();
   mbar_expect(p.lbar, TILE_D * sizeof(double));
-  bulk_g2s(dst, t.tile(t.j, t.j), TILE_D * sizeof(double), p.lbar);
+  bulk_g2s(dst, inv ? t.linv(t.j) : t.tile(t.j, t.j), TILE_D * sizeof(double), p.lbar);
 }
 
 __device__ void produce(const TaskCtx& t, int kind, Pipe& p, double* sm) {
@@ -306,19 +311,22 @@ __device__ void produce(const TaskCtx& t, int kind, Pipe& p, double* sm) {
         prod_issue(p, sm, t.tile(t.i, k) + h * HALF_D, diag ? nullptr : t.tile(t.j, k) + h * HALF_D, half);
     }
     hold(false);
-    if (!diag) prod_ljj(t, p, sm + NB * LDC);
+    if (!diag) {  // L_jj⁻¹ as the task's last ring chunk (one full slot), in flight during the last GEMM chunks
+      wait_flag(t.tflag(t.j, t.j));
+      prod_issue(p, sm, t.linv(t.j), t.linv(t.j) + HALF_D, half);
+    }
   } else if (kind == T_FWD) {
     for (int k = 0; k < t.j; ++k) {
       wait_flag(t.tflag(t.j, k));
       prod_issue(p, sm, t.tile(t.j, k), nullptr, full);
     }
-    prod_ljj(t, p, sm);
+    prod_ljj(t, p, sm, true);
   } else if (kind == T_BWD) {
     for (int i = t.a->nt - 1; i > t.j; --i) {
       wait_flag(t.tflag(i, t.j));
       prod_issue(p, sm, t.tile(i, t.j), nullptr, full);
     }
-    prod_ljj(t, p, sm);
+    prod_ljj(t, p, sm, true);
   }
 }
 
@@ -394,40 +402,45 @@ __device__ int potrf64(double* Cs, double* rdv, int* sh) {
   return 0;
 }
 
-// X L_jjᵀ = C in place (Cs row-major stride LDC); L_jj in the packed tile layout
-// (L(c, k) = Ls[k·LDT + c]); rdv[c] = 1 / L(c, c) must be ready.
-__device__ void trsm64(double* Cs, const double* Ls, const double* rdv) {
+// Li (packed layout: Li[c·LDT + r] = L⁻¹(r, c)) ← the inverse of the lower-triangular L in Cs
+// (row-major, stride LDC), rdv[c] = 1 / L(c, c); tmp: 3 × 256 doubles.  On 16×16 blocks: the
+// diagonal blocks by forward substitution (one column per thread), then the block diagonals
+// d = 1, 2, 3: L⁻¹_ij = −L⁻¹_ii Σ_{k=j}^{i−1} L_ik L⁻¹_kj.  The off-diagonal tiles of the
+// column then solve X L_jjᵀ = C as the DMMA product X = C L_jj⁻ᵀ, and the solves use L_jj⁻¹.
+__device__ void trinv64(const double* Cs, const double* rdv, double* Li, double* tmp) {
   const int tid = threadIdx.x;
-  for (int b0 = 0; b0 < NB; b0 += SB) {
-    if (tid < NB) {  // X_b = C_b L_bb^{-T}, one row per thread in registers
-      double* row = Cs + tid * LDC + b0;
-      double x[SB];
+  for (int e = tid; e < NB * NB; e += kCons) {  // blocks above the block diagonal are zero
+    const int c = e >> 6, r = e & 63;
+    if ((r >> 4) < (c >> 4)) Li[c * LDT + r] = 0.0;
+  }
+  if (tid < NB) {
+    const int b0 = tid & ~(SB - 1), c = tid & (SB - 1);
+    double y[SB];
 #pragma unroll
-      for (int k = 0; k < SB; ++k) x[k] = row[k];
+    for (int r = 0; r < SB; ++r) {
+      double v = (r == c) ? 1.0 : 0.0;
 #pragma unroll
-      for (int c = 0; c < SB; ++c) {
-        double q4[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int k = 0; k < r; ++k) v -= Cs[(b0 + r) * LDC + b0 + k] * y[k];
+      y[r] = r < c ? 0.0 : v * rdv[b0 + r];
+    }
 #pragma unroll
-        for (int k = 0; k < c; ++k) q4[k & 3] += x[k] * Ls[(b0 + k) * LDT + b0 + c];
-        x[c] = (x[c] - ((q4[0] + q4[1]) + (q4[2] + q4[3]))) * rdv[b0 + c];
-      }
-#pragma unroll
-      for (int k = 0; k < SB; ++k) row[k] = x[k];
+    for (int r = 0; r < SB; ++r) Li[(b0 + c) * LDT + b0 + r] = y[r];
+  }
+  cons_sync();
+  for (int d = 1; d < NB / SB; ++d) {
+    const int nblk = NB / SB - d;  // blocks (i, i − d), i = d … 3
+    for (int e = tid; e < nblk * SB * SB; e += kCons) {
+      const int bi = e >> 8, r = (e >> 4) & (SB - 1), c = e & (SB - 1), i = d + bi, j = bi;
+      double v = 0.0;
+      for (int k = j * SB; k < i * SB; ++k) v += Cs[(i * SB + r) * LDC + k] * Li[(j * SB + c) * LDT + k];
+      tmp[e] = v;  // T_ij(r, c) = Σ_k L_ik L⁻¹_kj
     }
     cons_sync();
-    const int nc = NB - b0 - SB;
-    if (nc == 0) break;
-    // C[r][c] −= Σ_{k in block} X[r][k] L(c, k) for the columns right of the block
-    for (int e = tid; e < NB * nc; e += kCons) {
-      const int r = e / nc, c = b0 + SB + e % nc;
-      const double* Xr = Cs + r * LDC + b0;
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int k = 0; k < SB; k += 2) {
-        s0 += Xr[k] * Ls[(b0 + k) * LDT + c];
-        s1 += Xr[k + 1] * Ls[(b0 + k + 1) * LDT + c];
-      }
-      Cs[r * LDC + c] -= s0 + s1;
+    for (int e = tid; e < nblk * SB * SB; e += kCons) {
+      const int bi = e >> 8, r = (e >> 4) & (SB - 1), c = e & (SB - 1), i = d + bi, j = bi;
+      double v = 0.0;
+      for (int k = 0; k <= r; ++k) v += Li[(i * SB + k) * LDT + i * SB + r] * tmp[(bi << 8) + (k << 4) + c];
+      Li[(j * SB + c) * LDT + i * SB + r] = -v;
     }
     cons_sync();
   }
@@ -467,44 +480,80 @@ __device__ void cons_tile(const TaskCtx& t, Pipe& p, double* sm, int* sh) {
   }
   cons_sync();  // every warp is past the ring before the epilogue reuses it
   PF_MARK(0);
-  double* Cs = sm;               // [64][LDC]
-  double* Ls = sm + NB * LDC;    // L_jj (packed layout), filled by the producer
-  double* sv = Ls + TILE_D;      // [64]
-#pragma unroll
-  for (int m = 0; m < 4; ++m)
-#pragma unroll
-    for (int x = 0; x < 2; ++x)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = wr * 32 + m * 8 + g, c = wc * 16 + x * 8 + 2 * q + h;
-        Cs[r * LDC + c] = -acc[m][x][h];
-      }
+  double* Out = const_cast<double*>(Aij);
   const bool critical = t.i <= t.j + 1;
   int* crit = t.a->crit + smid();
-  if (diag && tid == 0) atomicAdd(crit, 1);
-  cons_sync();
-  PF_MARK(1);
-  double* Out = const_cast<double*>(Aij);
   if (diag) {
+    double* Cs = sm;               // [64][LDC] row-major
+    double* Li = sm + TILE_D;      // L_jj⁻¹ (packed layout)
+    double* sv = Li + TILE_D;      // [64]
+    double* tmp = sv + NB;         // [3][256]
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = wr * 32 + m * 8 + g, c = wc * 16 + x * 8 + 2 * q + h;
+          Cs[r * LDC + c] = -acc[m][x][h];
+        }
+    if (tid == 0) atomicAdd(crit, 1);
+    cons_sync();
+    PF_MARK(1);
     const int fail = potrf64(Cs, sv, sh);
+    if (!fail) trinv64(Cs, sv, Li, tmp);
     PF_MARK(2);
     if (fail && tid == 0) record_fail(t.a->info + t.s, t.j * NB + fail);
+    double* Inv = const_cast<double*>(t.linv(t.j));
     for (int idx = tid; idx < NB * NB; idx += kCons) {
       const int c = idx >> 6, r = idx & 63;
       Out[c * LDT + r] = r >= c ? Cs[r * LDC + c] : 0.0;
+      Inv[c * LDT + r] = fail ? 0.0 : (r >= c ? Li[c * LDT + r] : Li[r * LDT + c]);  // strict upper: L⁻ᵀ
     }
   } else {
-    mbar_wait(p.lbar, p.lpar);
-    p.lpar ^= 1;
-    if (critical && tid == 0) atomicAdd(crit, 1);  // L_jj is here: the chain runs on this SM now
-    if (tid < NB) sv[tid] = 1.0 / Ls[tid * LDT + tid];
+    // C = −acc (packed layout, the DMMA A operand), then X = C L_jj⁻ᵀ on DMMA; L_jj⁻¹ is the
+    // task's last ring chunk and C goes to the slot after it (consumed)
+    const double* Li = cons_acquire(p, sm);
+    double* Ct = stage_ptr(sm, (p.cc + 1) % NST);  // C(r, c) = Ct[c·LDT + r]
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = wr * 32 + m * 8 + g, c = wc * 16 + x * 8 + 2 * q + h;
+          Ct[c * LDT + r] = -acc[m][x][h];
+          acc[m][x][h] = 0.0;
+        }
+    if (critical && tid == 0) atomicAdd(crit, 1);  // L_jj⁻¹ is here: the chain runs on this SM now
     cons_sync();
-    trsm64(Cs, Ls, sv);
-    PF_MARK(2);
-    for (int idx = tid; idx < NB * NB; idx += kCons) {
-      const int c = idx >> 6, rr = idx & 63;
-      Out[c * LDT + rr] = Cs[rr * LDC + c];
+    PF_MARK(1);
+#pragma unroll 4
+    for (int kk = 0; kk < NB; kk += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) af[m] = Ct[(kk + q) * LDT + wr * 32 + m * 8 + g];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {  // L⁻¹(col, k), zero above the diagonal (the slot holds L⁻ᵀ there)
+        const int col = wc * 16 + x * 8 + g;
+        bf[x] = kk + q <= col ? Li[(kk + q) * LDT + col] : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int x = 0; x < 2; ++x) dmma_8x8x4(acc[m][x][0], acc[m][x][1], af[m], bf[x]);
     }
+    cons_release(p);
+    PF_MARK(2);
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = wr * 32 + m * 8 + g, c = wc * 16 + x * 8 + 2 * q + h;
+          Out[c * LDT + r] = acc[m][x][h];
+        }
   }
   cons_sync();
   PF_MARK(3);
@@ -552,28 +601,28 @@ __device__ void cons_fwd(const TaskCtx& t, Pipe& p, double* sm, double* red, dou
       if (lane == 0 && rr < a.nrhs) red[rr * NB + 8 * warp + r8] = v;
     }
   cons_sync();
-  mbar_wait(p.lbar, p.lpar);  // L_jj (packed layout: L(r, c) = Ls[c·LDT + r])
+  mbar_wait(p.lbar, p.lpar);  // L_jj⁻¹ (lower: Li[c·LDT + r] = L⁻¹(r, c), r ≥ c)
   p.lpar ^= 1;
-  const double* Ls = sm;
-  if (tid < NB) rdv[tid] = 1.0 / Ls[tid * LDT + tid];
+  const double* Li = sm;
   for (int idx = tid; idx < a.nrhs * NB; idx += kCons) {
     const int rr = idx >> 6, r = idx & 63, R = j * NB + r;
     const double b = R < a.n ? a.rhs[((size_t)(a.sidx ? a.sidx[t.s] : t.s) * a.rhs_ld + rr) * a.n + R] : 0.0;
     vs[rr * NB + r] = b - red[rr * NB + r];
   }
   cons_sync();
-  if (warp < a.nrhs) {  // one warp per right-hand side: lane owns rows lane, lane + 32
-    double* y = vs + warp * NB;
-    double y0 = y[lane], y1 = y[lane + 32];
+  if (warp < a.nrhs) {  // y = L⁻¹ v, one warp per right-hand side: lane owns rows lane, lane + 32
+    const double* v = vs + warp * NB;
+    double y0[4] = {0.0, 0.0, 0.0, 0.0}, y1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
     for (int c = 0; c < NB; ++c) {
-      const double yc = __shfl_sync(0xffffffffu, c < 32 ? y0 : y1, c & 31) * rdv[c];
-      if (lane == (c & 31)) { if (c < 32) y0 = yc; else y1 = yc; }
-      if (lane > c) y0 -= Ls[c * LDT + lane] * yc;
-      if (lane + 32 > c) y1 -= Ls[c * LDT + lane + 32] * yc;
+      const double vc = v[c];
+      if (c <= lane) y0[c & 3] += Li[c * LDT + lane] * vc;
+      y1[c & 3] += Li[c * LDT + lane + 32] * (c <= lane + 32 ? vc : 0.0);
     }
+    const double ya = (y0[0] + y0[1]) + (y0[2] + y0[3]), yb = (y1[0] + y1[1]) + (y1[2] + y1[3]);
     double* yo = a.cy + ((size_t)t.s * 2 * kRhsCap + warp) * nt * NB + j * NB;
-    __stcg(yo + lane, y0);
-    __stcg(yo + lane + 32, y1);
+    __stcg(yo + lane, ya);
+    __stcg(yo + lane + 32, yb);
   }
   cons_sync();
   if (tid == 0) {
@@ -622,26 +671,25 @@ __device__ void cons_bwd(const TaskCtx& t, Pipe& p, double* sm, double* red, dou
     sh[0] = *(volatile int*)(a.info + t.s) == 0;
   }
   cons_sync();  // red and y_j visible to every consumer
-  mbar_wait(p.lbar, p.lpar);  // L_jj (packed layout: L(r, c) = Ls[c·LDT + r])
+  mbar_wait(p.lbar, p.lpar);  // L_jj⁻¹ with L⁻ᵀ in the strict upper part: Li[c·LDT + r] = L⁻¹(c, r) for r < c
   p.lpar ^= 1;
-  const double* Ls = sm;
-  if (tid < NB) rdv[tid] = 1.0 / Ls[tid * LDT + tid];
+  const double* Li = sm;
   for (int idx = tid; idx < a.nrhs * NB; idx += kCons) {
     const int rr = idx >> 6, c = idx & 63;
     vs[rr * NB + c] = __ldcg(a.cy + ((size_t)t.s * 2 * kRhsCap + rr) * nt * NB + j * NB + c) - red[rr * NB + c];
   }
   cons_sync();
   const bool ok = sh[0];
-  if (ok && warp < a.nrhs) {  // Lᵀ p = v backwards; lane owns entries lane, lane + 32
-    double* v = vs + warp * NB;
-    double v0 = v[lane], v1 = v[lane + 32];
-    for (int c = NB - 1; c >= 0; --c) {
-      const double pc = __shfl_sync(0xffffffffu, c < 32 ? v0 : v1, c & 31) * rdv[c];
-      if (lane == (c & 31)) { if (c < 32) v0 = pc; else v1 = pc; }
-      // (Lᵀ p)[r] for r < c gets L(c, r) p_c; L(c, r) = Ls[r·LDT + c]
-      if (lane < c) v0 -= Ls[lane * LDT + c] * pc;
-      if (lane + 32 < c) v1 -= Ls[(lane + 32) * LDT + c] * pc;
+  if (ok && warp < a.nrhs) {  // p = L⁻ᵀ v: p_r = Σ_{c ≥ r} L⁻¹(c, r) v_c; lane owns entries lane, lane + 32
+    const double* v = vs + warp * NB;
+    double q0[4] = {0.0, 0.0, 0.0, 0.0}, q1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+    for (int c = 0; c < NB; ++c) {
+      const double vc = v[c];
+      q0[c & 3] += Li[c * LDT + lane] * (c >= lane ? vc : 0.0);
+      if (c >= lane + 32) q1[c & 3] += Li[c * LDT + lane + 32] * vc;
     }
+    const double v0 = (q0[0] + q0[1]) + (q0[2] + q0[3]), v1 = (q1[0] + q1[1]) + (q1[2] + q1[3]);
     double* po = a.cy + ((size_t)t.s * 2 * kRhsCap + kRhsCap + warp) * nt * NB + j * NB;
     __stcg(po + lane, v0);
     __stcg(po + lane + 32, v1);
@@ -721,7 +769,7 @@ __global__ void __launch_bounds__(kDagThreads, 2) k_chol_dag(DagArgs a) {
 #ifdef PF_CHOL_TRACE
     const unsigned long long t0 = gtimer();
 #endif
-    TaskCtx t{&a, s, i, j, a.tiles + (size_t)s * a.ntri * TILE_D, a.flags + (size_t)s * (a.ntri + 2 * a.nt)};
+    TaskCtx t{&a, s, i, j, a.tiles + (size_t)s * tstride(a.nt) * TILE_D, a.flags + (size_t)s * (a.ntri + 2 * a.nt)};
     if (kind == -T_TILE) {
       if (tid == 0) st_release(t.tflag(i, j), 1);  // skipped: publish so dependants proceed
     } else if (tid >= kCons) {
@@ -757,10 +805,7 @@ __global__ void k_info_out(int n_scen, const int* __restrict__ ws, int* __restri
 
 }  // namespace
 
-size_t chol_tile_doubles(int n_u) {
-  const size_t nt = (n_u + NB - 1) / NB;
-  return nt * (nt + 1) / 2 * TILE_D;
-}
+size_t chol_tile_doubles(int n_u) { return tstride((n_u + NB - 1) / NB) * TILE_D; }
 size_t chol_flag_ints(int n_u) {
   const size_t nt = (n_u + NB - 1) / NB;
   return nt * (nt + 1) / 2 + 2 * nt;

@@ -38,6 +38,7 @@ int main(int argc, char** argv) {
   cudaMemset(dtr, 0, (size_t)ntask_max * 8 * 8);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int gmax = pf::chol_grid_max();
   float best = 1e30f;
   for (int r = 0; r < reps; ++r) {
     cudaMemcpy(dK, dK0, K.size() * 8, cudaMemcpyDeviceToDevice);
@@ -46,7 +47,7 @@ int main(int argc, char** argv) {
     if (r == reps - 1 && trace) cudaMemcpyToSymbol(pf::g_chol_trace, &dtr, sizeof(dtr));
 #endif
     cudaEventRecord(e0);
-    pf::launch_chol(net, w, S, dK, nullptr, 0.0, drhs, 1, dinfo, dws, 0);
+    pf::launch_chol(net, w, S, dK, nullptr, 0.0, drhs, 1, dinfo, dws, 0, gmax);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0;
