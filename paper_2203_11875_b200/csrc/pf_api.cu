@@ -30,6 +30,8 @@ struct pf_net {
   bool prof = false;         // instrumentation: events around the hot kernels
   int reach_rows_l = 0, reach_rows_ua = 0, gu_rows = 0;  // sparse-RHS statistics (pf_dims)
   std::vector<int4> p1_task;  // bottom-subtree schedules (host copies for the upload)
+  std::vector<int> lu_p1_blk, lu_p1_ptr;  // … and k_lu's (blocks per warp pair)
+  std::vector<int> lu_lev_blk;            // k_lu's level-synchronous block order
   std::vector<int> p1_ptr;
   std::vector<int4> u_top, u_bot, ua_top, ua_bot;
   std::vector<int> u_top_ptr, u_bot_ptr, ua_top_ptr, ua_bot_ptr;
@@ -39,6 +41,9 @@ struct pf_net {
 
 #ifndef PF_P1_IMB
 #define PF_P1_IMB 10
+#endif
+#ifndef PF_LU_IMB
+#define PF_LU_IMB 30
 #endif
 
 static std::string g_build_err;
@@ -233,6 +238,24 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
     levUa_ptr[l + 1] = (int)taskUa.size();
   }
   d.ntc = ntc; d.bmw = bmw;
+  // dense LU front: the lowest level cut whose rows (levels ≥ cut) number at most kFrontMax
+  std::vector<int> fr_row, fr_pos(P.n_x, -1);
+  {
+    std::vector<int> row_lev(P.n_x, 0), cnt_ge(nlevL + 1, 0);
+    for (int l = 0; l < nlevL; ++l)
+      for (int bi = P.levL_ptr[l]; bi < P.levL_ptr[l + 1]; ++bi) {
+        const int p = P.levL_blk[bi];
+        for (int r = P.blk_ptr[p]; r < P.blk_ptr[p + 1]; ++r) row_lev[r] = l;
+      }
+    for (int r = 0; r < P.n_x; ++r) ++cnt_ge[row_lev[r]];
+    for (int l = nlevL - 1; l >= 0; --l) cnt_ge[l] += cnt_ge[l + 1];
+    int cut = nlevL;
+    while (cut > 0 && cnt_ge[cut - 1] <= kFrontMax) --cut;
+    d.fr_lev = cut;
+    for (int r = 0; r < P.n_x; ++r)
+      if (row_lev[r] >= cut) { fr_pos[r] = (int)fr_row.size(); fr_row.push_back(r); }
+    d.fr_n = (int)fr_row.size();
+  }
   for (size_t k = 0; k < rowbm.size(); ++k) h->reach_rows_l += __builtin_popcount(rowbm[k]);
   for (int r = 0; r < P.n_x; ++r) h->reach_rows_ua += row_mark[r] == ntc;
   for (int r = 0; r < P.n_x; ++r) h->gu_rows += P.gur_ptr[r + 1] > P.gur_ptr[r];
@@ -249,9 +272,12 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
       const int last = P.blk_ptr[p + 1] - 1;
       if (parent[last] >= 0) bpar[p] = P.row_blk[parent[last]];
     }
-    std::vector<int> best_order, best_ptr(nteam + 1, 0);
-    int best_lev0 = 0;
-    for (int lev0 = 1; lev0 <= nlevL; ++lev0) {
+    // the deepest cut ≤ max_lev0 whose team loads stay within PF_P1_IMB% of the mean
+    auto schedule = [&](int nteam, int max_lev0, int imb, std::vector<int>& best_order, std::vector<int>& best_ptr,
+                        int& best_lev0) {
+    best_order.clear(); best_ptr.assign(nteam + 1, 0);
+    best_lev0 = 0;
+    for (int lev0 = 1; lev0 <= max_lev0; ++lev0) {
       // subtree roots: blocks below lev0 whose parent is at or above lev0
       for (int l = lev0 - 1; l >= 0; --l)
         for (int bi = P.levL_ptr[l]; bi < P.levL_ptr[l + 1]; ++bi) {
@@ -281,7 +307,7 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
       }
       const long long tot = std::accumulate(load.begin(), load.end(), 0LL);
       const long long mx = *std::max_element(load.begin(), load.end());
-      if (lev0 > 1 && mx * 100 > tot * (100 + PF_P1_IMB) / nteam) break;  // imbalance beyond PF_P1_IMB%: keep the previous cut
+      if (lev0 > 1 && mx * 100 > tot * (100 + imb) / nteam) break;  // imbalance beyond imb %: keep the previous cut
       std::vector<int> order, ptr(nteam + 1, 0);
       for (int t = 0; t < nteam; ++t) {
         for (int r : mine[t]) {  // iterative postorder of the subtree of r
@@ -295,6 +321,28 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
         ptr[t + 1] = (int)order.size();
       }
       best_order.swap(order); best_ptr.swap(ptr); best_lev0 = lev0;
+    }
+    };
+    std::vector<int> best_order, best_ptr;
+    int best_lev0 = 0;
+    schedule(nteam, nlevL, PF_P1_IMB, best_order, best_ptr, best_lev0);
+    {  // k_lu: warp pairs of a 16-CTA cluster (a smaller cluster walks several pairs' lists)
+      std::vector<int> lo, lp;
+      int l0 = 0;
+      schedule(kLuPairs, d.fr_lev, PF_LU_IMB, lo, lp, l0);
+      h->lu_p1_blk = lo; h->lu_p1_ptr = lp;
+      d.lu_lev0 = l0; d.lu_nteam = kLuPairs;
+      // the level-synchronous levels hand blocks to the pairs in order and only the low pairs
+      // have SMEM staging areas: longest rows first within a level
+      h->lu_lev_blk = P.levL_blk;
+      auto piv = [&](int b) {
+        int m = 0;
+        for (int r = P.blk_ptr[b]; r < P.blk_ptr[b + 1]; ++r) m = std::max(m, P.lu_diag[r] - P.lu_ptr[r]);
+        return m;
+      };
+      for (int l = 0; l < nlevL; ++l)
+        std::stable_sort(h->lu_lev_blk.begin() + P.levL_ptr[l], h->lu_lev_blk.begin() + P.levL_ptr[l + 1],
+                         [&](int x, int y) { return piv(x) > piv(y); });
     }
     std::vector<int4> p1_task(best_order.size());
     for (size_t k = 0; k < best_order.size(); ++k) p1_task[k] = taskL[task_of[best_order[k]]];
@@ -461,13 +509,15 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
             up(h, P.a_src, &d.a_src) && up(h, P.ah_off, &d.ah_off) && up(h, P.h_line, &d.h_line) &&
             up(h, P.h_end, &d.h_end) && up(h, P.blk_ptr, &d.blk_ptr) && up(h, P.lu_ptr, &d.lu_ptr) &&
             up(h, P.lu_idx, &d.lu_idx) && up(h, P.lu_diag, &d.lu_diag) && up(h, P.lu_src, &d.lu_src) &&
-            up(h, P.lu_tpos, &d.lu_tpos) && up(h, P.upd_ptr, &d.upd_ptr) && up(h, P.upd_dst, &d.upd_dst) &&
+            up(h, P.lu_tpos, &d.lu_tpos) && up(h, P.upd_ptr, &d.upd_ptr) && up(h, P.upd_dst, &d.upd_dst) && up(h, P.upd_src, &d.upd_src) &&
             up(h, P.levL_ptr, &d.levL_ptr) && up(h, P.levL_blk, &d.levL_blk) && up(h, P.levU_ptr, &d.levU_ptr) &&
             up(h, P.levU_blk, &d.levU_blk) && up(h, P.guc_ptr, &d.guc_ptr) && up(h, P.guc_row, &d.guc_row) &&
             up(h, P.guc_src, &d.guc_src) && up(h, P.gur_ptr, &d.gur_ptr) && up(h, P.gur_col, &d.gur_col) &&
             up(h, P.gur_src, &d.gur_src) && up(h, P.bus_pth, &d.bus_pth) && up(h, P.bus_pv, &d.bus_pv) &&
             up(h, gbus, &d.gbus) && up(h, rowmeta, &d.rowmeta) && up(h, hvp_order, &d.hvp_bus) &&
             up(h, taskL, &d.taskL) && up(h, taskU, &d.taskU) && up(h, sw_src, &d.sw_src) &&
+            up(h, fr_row, &d.fr_row) && up(h, fr_pos, &d.fr_pos) && up(h, h->lu_p1_blk, &d.lu_p1_blk) &&
+            up(h, h->lu_p1_ptr, &d.lu_p1_ptr) && up(h, h->lu_lev_blk, &d.lu_lev_blk) &&
             up(h, taskLr, &d.taskLr) && up(h, levLr_ptr, &d.levLr_ptr) && up(h, rowbm, &d.rowbm) &&
             up(h, taskUa, &d.taskUa) && up(h, levUa_ptr, &d.levUa_ptr) && up(h, h->p1_task, &d.p1_task) &&
             up(h, h->p1_ptr, &d.p1_ptr) && up(h, h->u_top, &d.u_top) && up(h, h->u_top_ptr, &d.u_top_ptr) &&

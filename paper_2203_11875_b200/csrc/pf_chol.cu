@@ -461,7 +461,18 @@ __device__ void cons_tile(const TaskCtx& t, Pipe& p, double* sm, int* sh) {
 #pragma unroll
       for (int h = 0; h < 2; ++h)
         acc[m][x][h] = -Aij[(wc * 16 + x * 8 + 2 * q + h) * LDT + wr * 32 + m * 8 + g];
+#ifdef PF_CHOL_CONS_THROTTLE
+  const bool crit_task = t.i <= t.j + 1;
+  const int* critc = t.a->crit + smid();
+#endif
   for (int c = 0; c < 2 * t.j; ++c) {
+#ifdef PF_CHOL_CONS_THROTTLE
+    if (!crit_task) {  // experiment: the consumers of a non-critical tile also pause for the chain
+      if (lane == 0)
+        while (ld_relaxed(critc) > 0) __nanosleep(100);
+      __syncwarp();
+    }
+#endif
     const double* A = cons_acquire(p, sm);
     const double* B = diag ? A : A + HALF_D;
 #pragma unroll

@@ -35,7 +35,7 @@ struct DevNet {
   const int *inc_ptr, *inc_line, *inc_off_th, *inc_off_v;
   const int *jb_ptr, *jb_self_th, *jb_self_v;
   const int *gx_src, *gu_src, *a_ptr, *a_src, *ah_off, *h_line, *h_end;
-  const int *blk_ptr, *lu_ptr, *lu_idx, *lu_diag, *lu_src, *lu_tpos, *upd_ptr, *upd_dst;
+  const int *blk_ptr, *lu_ptr, *lu_idx, *lu_diag, *lu_src, *lu_tpos, *upd_ptr, *upd_dst, *upd_src;
   const int *levL_ptr, *levL_blk, *levU_ptr, *levU_blk;
   const int *guc_ptr, *guc_row, *guc_src, *gur_ptr, *gur_col, *gur_src;
   const int *bus_pth, *bus_pv;
@@ -71,6 +71,17 @@ struct DevNet {
   const int *u_gen;             // [n_u] generator of a p_g control, −1 for v controls
   BlkSet hb;                    // k_hvp: K's bus blocks (every bus) + A_rᵀ at generator neighbours
   BlkSet mb;                    // k_mu: ∂(P_g, Q_g)/∂(θ_j, v_j) blocks of the generator buses g
+  // Dense front (k_lu): the rows of levels ≥ fr_lev (fr_n ≤ kFrontMax of them, ascending
+  // permuted index fr_row; fr_pos[r] = front index of row r or −1).  Their pivots among
+  // themselves are eliminated as one dense LU of the front Schur complement in SMEM
+  // instead of fr_lev … nlevL−1 cluster-synchronised levels.
+  int fr_lev, fr_n;
+  // k_lu bottom levels (< lu_lev0): per warp pair of the cluster (lu_nteam of them) its subtrees'
+  // blocks in postorder, lu_p1_blk[lu_p1_ptr[t] … lu_p1_ptr[t + 1])
+  int lu_lev0, lu_nteam;
+  const int *lu_p1_blk, *lu_p1_ptr;
+  const int *lu_lev_blk;        // [n_blocks] levL_blk with each level's longest rows first (k_lu)
+  const int *fr_row, *fr_pos;
   int C;                        // directions per tile (slab row width)
   int lu_maxlen;                // longest row of the filled LU pattern
 };

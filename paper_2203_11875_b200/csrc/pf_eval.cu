@@ -264,37 +264,23 @@ struct LuStage {
   double* pin;  // [kLuMaxPiv]
   double* val;  // [kLuStageCap]
   int* off;     // [kLuMaxPiv + 1]
-  int* u0;      // [kLuMaxPiv] start of the pivot's U row in lu
-  int* q0;      // [kLuMaxPiv] start of the pivot's update list in upd_dst
   int* dst;     // [kLuStageCap]
 };
-constexpr size_t kLuStageBytes = (size_t)kLuMaxPiv * 8 + kLuStageCap * 8 + (kLuMaxPiv + 1 + 1) * 4 +
-                                 2 * kLuMaxPiv * 4 + kLuStageCap * 4;
+constexpr size_t kLuStageBytes = (size_t)kLuMaxPiv * 8 + kLuStageCap * 8 + (kLuMaxPiv + 2) * 4 + kLuStageCap * 4;
 
-// Lane-parallel gather of row (base, dl)'s IKJ working set: two dependent waves
-// for the pivot metadata, then every update entry — a flat loop, each lane
-// finding its pivot by binary search, 4 independent loads in flight per lane
-// (values finalized by earlier levels; __ldcg: written by other SMs of the
-// cluster).  False (nothing staged) when the lists exceed the staging area.
+// Lane-parallel gather of row (base, dl)'s IKJ working set.  The row's update lists are one
+// contiguous run of upd_dst / upd_src (entries e = base … base + dl − 1 in order), so the
+// pivot offsets come straight from upd_ptr and every update entry is an independent pair of
+// loads (its target offset, and the U value at upd_src; __ldcg: written by other SMs of the
+// cluster), 4 in flight per lane.  False (nothing staged) when the lists exceed the area.
 __device__ bool stage_row(const DevNet& n, const double* lu, const double* invd, int base, int dl, int lane,
                           const LuStage& st) {
-  for (int a = lane; a < dl; a += 32) {
-    const int e = base + a, k = __ldg(n.lu_idx + e);
-    const int q0 = __ldg(n.upd_ptr + e);
-    st.off[a + 1] = __ldg(n.upd_ptr + e + 1) - q0;
-    st.q0[a] = q0;
-    st.u0[a] = __ldg(n.lu_diag + k) + 1;
-    st.pin[a] = __ldcg(invd + k);
-  }
-  __syncwarp();
-  if (lane == 0) {  // prefix sum of the list lengths (dl ≤ 128: serial is fine)
-    int acc = 0;
-    st.off[0] = 0;
-    for (int a = 0; a < dl; ++a) { acc += st.off[a + 1]; st.off[a + 1] = acc; }
-  }
-  __syncwarp();
-  const int total = st.off[dl];
+  const int q0 = __ldg(n.upd_ptr + base), total = __ldg(n.upd_ptr + base + dl) - q0;
   if (total > kLuStageCap) return false;
+  for (int a = lane; a <= dl; a += 32) {
+    st.off[a] = __ldg(n.upd_ptr + base + a) - q0;
+    if (a < dl) st.pin[a] = __ldcg(invd + __ldg(n.lu_idx + base + a));
+  }
   for (int i0 = 0; i0 < total; i0 += 128) {
     double v[4];
     int dd[4];
@@ -302,14 +288,8 @@ __device__ bool stage_row(const DevNet& n, const double* lu, const double* invd,
     for (int q = 0; q < 4; ++q) {
       const int idx = i0 + 32 * q + lane;
       if (idx < total) {
-        int lo = 0, hi = dl;  // st.off[lo] <= idx < st.off[hi]
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (st.off[mid] <= idx) lo = mid; else hi = mid;
-        }
-        const int t = idx - st.off[lo];
-        v[q] = __ldcg(lu + st.u0[lo] + t);
-        dd[q] = __ldg(n.upd_dst + st.q0[lo] + t);
+        v[q] = __ldcg(lu + __ldg(n.upd_src + q0 + idx));
+        dd[q] = __ldg(n.upd_dst + q0 + idx);
       }
     }
 #pragma unroll
@@ -324,7 +304,88 @@ __device__ bool stage_row(const DevNet& n, const double* lu, const double* invd,
 
 #ifdef PF_LU_TRACE
 __device__ unsigned long long* g_lu_trace;  // tools/lu_trace.py: globaltimer after each level (cluster 0)
+#define LU_PH(lev, ph)                                                                              \
+  do {                                                                                              \
+    if (blockIdx.x == 0 && warp == 0 && lane == 0 && g_lu_trace) {                                  \
+      unsigned long long t_;                                                                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                        \
+      g_lu_trace[1024 + 8 * (lev) + (ph)] = t_;                                                     \
+    }                                                                                               \
+  } while (0)
+#else
+#define LU_PH(lev, ph) (void)0
 #endif
+
+// The dense front of one scenario's LU (levels ≥ fr_lev, after their cluster.sync).
+// (a) Every front row applies its pivots outside the front — rows of lower levels, final —
+//     in ascending order (a front pivot never precedes a non-front one it updates: U(k', k) ≠ 0
+//     makes k depend on k', so a front k' forces k into the front), one warp per row over the
+//     cluster.  (b) CTA 0 gathers the front Schur complement S (F × F, F ≤ kFrontMax) into SMEM
+//     and eliminates it densely in pivot order — l = s_ik · (1 / s_kk), s_ij −= l s_kj, the same
+//     operations the row-wise IKJ applies — with two CTA barriers per pivot instead of one
+//     cluster barrier per level; the pattern entries go back to lu, 1 / u_rr to invd, and the
+//     R18 pivot test to info.
+__device__ void lu_front(const DevNet& n, double* lu, double* invd, const double* rowmax, int* info, double* smem,
+                         int sub, int CS, cg::cluster_group& cluster) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5, F = n.fr_n;
+  double* ws = smem + warp * n.lu_maxlen;
+  for (int f = warp * CS + sub; f < F; f += CS * nwarp) {
+    const int r = __ldg(n.fr_row + f), base = __ldg(n.lu_ptr + r), len = __ldg(n.lu_ptr + r + 1) - base;
+    const int dl = __ldg(n.lu_diag + r) - base;
+    for (int a = lane; a < len; a += 32) ws[a] = __ldcg(lu + base + a);
+    __syncwarp();
+    for (int a = 0; a < dl; ++a) {
+      const int e = base + a, k = __ldg(n.lu_idx + e);
+      if (__ldg(n.fr_pos + k) >= 0) continue;  // a front pivot: the dense phase
+      const double l = ws[a] * __ldcg(invd + k);
+      const int q0 = __ldg(n.upd_ptr + e), cnt = __ldg(n.upd_ptr + e + 1) - q0, u0 = __ldg(n.lu_diag + k) + 1;
+      for (int t = lane; t < cnt; t += 32) ws[__ldg(n.upd_dst + q0 + t)] -= l * __ldcg(lu + u0 + t);
+      __syncwarp();
+      if (lane == 0) ws[a] = l;
+      __syncwarp();
+    }
+    for (int a = lane; a < len; a += 32) __stcg(lu + base + a, ws[a]);
+    __syncwarp();
+  }
+  cluster.sync();
+  if (sub == 0) {
+    const int LDS = F + 1;
+    double* S = smem;  // [F][F + 1]
+    for (int x = threadIdx.x; x < F * LDS; x += blockDim.x) S[x] = 0.0;
+    __syncthreads();
+    for (int f = warp; f < F; f += nwarp) {
+      const int r = __ldg(n.fr_row + f), base = __ldg(n.lu_ptr + r), len = __ldg(n.lu_ptr + r + 1) - base;
+      for (int a = lane; a < len; a += 32) {
+        const int fc = __ldg(n.fr_pos + __ldg(n.lu_idx + base + a));
+        if (fc >= 0) S[f * LDS + fc] = __ldcg(lu + base + a);
+      }
+    }
+    __syncthreads();
+    for (int k = 0; k < F; ++k) {
+      const double piv = 1.0 / S[k * LDS + k];
+      for (int i = k + 1 + threadIdx.x; i < F; i += blockDim.x) S[i * LDS + k] *= piv;
+      __syncthreads();
+      for (int i = k + 1 + warp; i < F; i += nwarp) {  // warp per row, lanes along it
+        const double l = S[i * LDS + k];
+        for (int j = k + 1 + lane; j < F; j += 32) S[i * LDS + j] -= l * S[k * LDS + j];
+      }
+      __syncthreads();
+    }
+    for (int f = warp; f < F; f += nwarp) {
+      const int r = __ldg(n.fr_row + f), base = __ldg(n.lu_ptr + r), len = __ldg(n.lu_ptr + r + 1) - base;
+      for (int a = lane; a < len; a += 32) {
+        const int fc = __ldg(n.fr_pos + __ldg(n.lu_idx + base + a));
+        if (fc >= 0) __stcg(lu + base + a, S[f * LDS + fc]);
+      }
+      if (lane == 0) {
+        const double d = S[f * LDS + f];
+        __stcg(invd + r, 1.0 / d);
+        if (!(fabs(d) >= 1e-12 * rowmax[r]) || !isfinite(d) || d == 0.0) atomicMin(info, r + 1);
+      }
+    }
+  }
+  cluster.sync();
+}
 
 __global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int CS) {
   cg::cluster_group cluster = cg::this_cluster();
@@ -363,9 +424,7 @@ __global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int CS) {
   st.pin = reinterpret_cast<double*>(stb);
   st.val = st.pin + kLuMaxPiv;
   st.off = reinterpret_cast<int*>(st.val + kLuStageCap);
-  st.u0 = st.off + kLuMaxPiv + 2;
-  st.q0 = st.u0 + kLuMaxPiv;
-  st.dst = st.q0 + kLuMaxPiv;
+  st.dst = st.off + kLuMaxPiv + 2;
   double* invd = w.invd + (size_t)s * n.n_x;
   // Blocks go to warp PAIRS: the θ row of a bus block on the even warp, its v row on
   // the odd one.  The v row depends on the θ row only through its last pivot (the
@@ -373,90 +432,105 @@ __global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int CS) {
   // from the θ row's workspace after a pair barrier.
   const int pw = warp >> 1, hv = warp & 1;
   const int gpair = pw * CS + sub, ngpair = CS * (nwarp >> 1);
-  for (int lev = 0; lev < n.nlevL; ++lev) {
-    const int b0 = __ldg(n.levL_ptr + lev), b1 = __ldg(n.levL_ptr + lev + 1);
-    for (int bi = b0 + gpair; bi < b1; bi += ngpair) {
-      const int p = __ldg(n.levL_blk + bi);
-      const int rb = __ldg(n.blk_ptr + p), nrow = __ldg(n.blk_ptr + p + 1) - rb;
-      const int r = rb + hv;
-      int base = 0, len = 0, dl = 0;
-      bool defer = false;
-      if (hv < nrow) {
-        base = __ldg(n.lu_ptr + r); len = __ldg(n.lu_ptr + r + 1) - base;
-        dl = __ldg(n.lu_diag + r) - base;
-        defer = hv == 1 && dl > 0 && __ldg(n.lu_idx + base + dl - 1) == rb;
-        if (hv == 1 && !defer) asm volatile("bar.sync %0, 64;" ::"r"(1 + pw) : "memory");  // no intra entry: wait
-        for (int a = lane; a < len; a += 32) ws[a] = __ldcg(lu + base + a);
-        __syncwarp();
-        const int np = defer ? dl - 1 : dl;  // pivots of this pass
-          if (warp < kLuStageWarps && np >= kLuStageMin && np <= kLuMaxPiv && stage_row(n, lu, invd, base, np, lane, st)) {
-            // long (separator) row: its whole IKJ working set is in SMEM, the chain runs there
-            for (int a = 0; a < np; ++a) {
-              const double l = ws[a] * st.pin[a];
-              const int o = st.off[a], cnt = st.off[a + 1] - o;
-              for (int t = lane; t < cnt; t += 32) ws[st.dst[o + t]] -= l * st.val[o + t];
-              __syncwarp();  // the next pivot's entry may just have been updated
-              if (lane == 0) ws[a] = l;  // (entry a is not read again by the chain)
-            }
-            __syncwarp();
-          } else {
-            // IKJ over the row's L entries; the U row of the next pivot and the
-            // update targets are prefetched into registers while this one runs.
-            double pu[4], pin = 0.0;
-            int pd[4], pq0 = 0, pcnt = 0, pu0 = 0;
-            auto fetch = [&](int a) {
-              const int e = base + a, k = __ldg(n.lu_idx + e);
-              pu0 = __ldg(n.lu_diag + k) + 1;
-              pq0 = __ldg(n.upd_ptr + e);
-              pcnt = __ldg(n.upd_ptr + e + 1) - pq0;
-              pin = __ldcg(invd + k);
-    #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int t = lane + 32 * j;
-                pu[j] = t < pcnt ? __ldcg(lu + pu0 + t) : 0.0;
-                pd[j] = t < pcnt ? __ldg(n.upd_dst + pq0 + t) : 0;
-              }
-            };
-            if (np > 0) fetch(0);
-            for (int a = 0; a < np; ++a) {
-              const double cu[4] = {pu[0], pu[1], pu[2], pu[3]};
-              const int cd[4] = {pd[0], pd[1], pd[2], pd[3]};
-              const double cin = pin;
-              const int q0 = pq0, cnt = pcnt, u0 = pu0;
-              if (a + 1 < np) fetch(a + 1);
-              const double l = ws[a] * cin;
-    #pragma unroll
-              for (int j = 0; j < 4; ++j)
-                if (lane + 32 * j < cnt) ws[cd[j]] -= l * cu[j];
-              for (int t = lane + 128; t < cnt; t += 32) ws[__ldg(n.upd_dst + q0 + t)] -= l * __ldcg(lu + u0 + t);
-              __syncwarp();
-              if (lane == 0) ws[a] = l;
-            }
+  // one bus block (its θ row on the pair's even warp, its v row on the odd one)
+  auto do_block = [&](const int p, const int lev) {
+    const int rb = __ldg(n.blk_ptr + p), nrow = __ldg(n.blk_ptr + p + 1) - rb;
+    const int r = rb + hv;
+    int base = 0, len = 0, dl = 0;
+    bool defer = false;
+    if (hv < nrow) {
+      base = __ldg(n.lu_ptr + r); len = __ldg(n.lu_ptr + r + 1) - base;
+      dl = __ldg(n.lu_diag + r) - base;
+      defer = hv == 1 && dl > 0 && __ldg(n.lu_idx + base + dl - 1) == rb;
+      if (hv == 1 && !defer) asm volatile("bar.sync %0, 64;" ::"r"(1 + pw) : "memory");  // no intra entry: wait
+      LU_PH(lev, 0);
+      for (int a = lane; a < len; a += 32) ws[a] = __ldcg(lu + base + a);
+      __syncwarp();
+      LU_PH(lev, 1);
+      const int np = defer ? dl - 1 : dl;  // pivots of this pass
+        if (warp < kLuStageWarps && np >= kLuStageMin && np <= kLuMaxPiv && stage_row(n, lu, invd, base, np, lane, st)) {
+          LU_PH(lev, 2);
+          // long (separator) row: its whole IKJ working set is in SMEM, the chain runs there
+          for (int a = 0; a < np; ++a) {
+            const double l = ws[a] * st.pin[a];
+            const int o = st.off[a], cnt = st.off[a + 1] - o;
+            for (int t = lane; t < cnt; t += 32) ws[st.dst[o + t]] -= l * st.val[o + t];
+            __syncwarp();  // the next pivot's entry may just have been updated
+            if (lane == 0) ws[a] = l;  // (entry a is not read again by the chain)
           }
-      }
-      if (nrow == 2 && (hv == 0 || defer)) asm volatile("bar.sync %0, 64;" ::"r"(1 + pw) : "memory");
-      if (defer) {  // the θ row's pivot, from its workspace
-        const double* ws0 = lu_ws + (size_t)(warp - 1) * n.lu_maxlen;
-        const int base0 = __ldg(n.lu_ptr + rb), dl0 = __ldg(n.lu_diag + rb) - base0;
-        const int e = base + dl - 1, q0 = __ldg(n.upd_ptr + e), cnt = __ldg(n.upd_ptr + e + 1) - q0;
-        const int o0 = dl0 + 1;  // U part of the θ row in ws0
-        const double l = ws[dl - 1] * (1.0 / ws0[dl0]);
-        for (int t = lane; t < cnt; t += 32) ws[__ldg(n.upd_dst + q0 + t)] -= l * ws0[o0 + t];
-        __syncwarp();
-        if (lane == 0) ws[dl - 1] = l;
-      }
-      if (hv < nrow) {
-        __syncwarp();
-        for (int a = lane; a < len; a += 32) __stcg(lu + base + a, ws[a]);
-        if (lane == 0) {
-          const double d = ws[dl];
-          __stcg(invd + r, 1.0 / d);
-          if (!(fabs(d) >= 1e-12 * rowmax[r]) || !isfinite(d) || d == 0.0) atomicMin(w.info + s, r + 1);
+          __syncwarp();
+        } else {
+          // IKJ over the row's L entries; the U row of the next pivot and the
+          // update targets are prefetched into registers while this one runs.
+          double pu[4], pin = 0.0;
+          int pd[4], pq0 = 0, pcnt = 0, pu0 = 0;
+          auto fetch = [&](int a) {
+            const int e = base + a, k = __ldg(n.lu_idx + e);
+            pu0 = __ldg(n.lu_diag + k) + 1;
+            pq0 = __ldg(n.upd_ptr + e);
+            pcnt = __ldg(n.upd_ptr + e + 1) - pq0;
+            pin = __ldcg(invd + k);
+  #pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int t = lane + 32 * j;
+              pu[j] = t < pcnt ? __ldcg(lu + pu0 + t) : 0.0;
+              pd[j] = t < pcnt ? __ldg(n.upd_dst + pq0 + t) : 0;
+            }
+          };
+          if (np > 0) fetch(0);
+          for (int a = 0; a < np; ++a) {
+            const double cu[4] = {pu[0], pu[1], pu[2], pu[3]};
+            const int cd[4] = {pd[0], pd[1], pd[2], pd[3]};
+            const double cin = pin;
+            const int q0 = pq0, cnt = pcnt, u0 = pu0;
+            if (a + 1 < np) fetch(a + 1);
+            const double l = ws[a] * cin;
+  #pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (lane + 32 * j < cnt) ws[cd[j]] -= l * cu[j];
+            for (int t = lane + 128; t < cnt; t += 32) ws[__ldg(n.upd_dst + q0 + t)] -= l * __ldcg(lu + u0 + t);
+            __syncwarp();
+            if (lane == 0) ws[a] = l;
+          }
         }
-        __syncwarp();
-      }
-      if (nrow == 2) asm volatile("bar.sync %0, 64;" ::"r"(1 + pw) : "memory");  // ws0 free for the next block
     }
+    if (nrow == 2 && (hv == 0 || defer)) asm volatile("bar.sync %0, 64;" ::"r"(1 + pw) : "memory");
+    if (defer) {  // the θ row's pivot, from its workspace
+      const double* ws0 = lu_ws + (size_t)(warp - 1) * n.lu_maxlen;
+      const int base0 = __ldg(n.lu_ptr + rb), dl0 = __ldg(n.lu_diag + rb) - base0;
+      const int e = base + dl - 1, q0 = __ldg(n.upd_ptr + e), cnt = __ldg(n.upd_ptr + e + 1) - q0;
+      const int o0 = dl0 + 1;  // U part of the θ row in ws0
+      const double l = ws[dl - 1] * (1.0 / ws0[dl0]);
+      for (int t = lane; t < cnt; t += 32) ws[__ldg(n.upd_dst + q0 + t)] -= l * ws0[o0 + t];
+      __syncwarp();
+      if (lane == 0) ws[dl - 1] = l;
+    }
+    if (hv < nrow) {
+      __syncwarp();
+      LU_PH(lev, 3);
+      for (int a = lane; a < len; a += 32) __stcg(lu + base + a, ws[a]);
+      if (lane == 0) {
+        const double d = ws[dl];
+        __stcg(invd + r, 1.0 / d);
+        if (!(fabs(d) >= 1e-12 * rowmax[r]) || !isfinite(d) || d == 0.0) atomicMin(w.info + s, r + 1);
+      }
+      __syncwarp();
+    }
+    // ws0 free for the next block; and both rows stored before the pair's next block (in the
+    // bottom subtrees that block may be this one's parent)
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + pw) : "memory");
+    LU_PH(lev, 4);
+  };
+  // Bottom levels (< lu_lev0): each warp pair walks its subtrees of the block elimination
+  // forest in postorder (a block needs only its descendants, done earlier by the same pair),
+  // with no cluster barrier; the schedule is built for lu_nteam pairs (pf_api.cu).
+  for (int t = gpair; t < n.lu_nteam; t += ngpair)
+    for (int q = __ldg(n.lu_p1_ptr + t); q < __ldg(n.lu_p1_ptr + t + 1); ++q) do_block(__ldg(n.lu_p1_blk + q), 0);
+  cluster.sync();
+  for (int lev = n.lu_lev0; lev < n.fr_lev; ++lev) {
+    const int b0 = __ldg(n.levL_ptr + lev), b1 = __ldg(n.levL_ptr + lev + 1);
+    for (int bi = b0 + gpair; bi < b1; bi += ngpair) do_block(__ldg(n.lu_lev_blk + bi), lev);
+    LU_PH(lev, 5);
     cluster.sync();
 #ifdef PF_LU_TRACE
     if (blockIdx.x == 0 && threadIdx.x == 0 && g_lu_trace) {
@@ -466,6 +540,7 @@ __global__ void __launch_bounds__(kLuThreads) k_lu(DevNet n, Work w, int CS) {
     }
 #endif
   }
+  if (n.fr_n > 0) lu_front(n, lu, invd, rowmax, w.info + s, lu_ws, sub, CS, cluster);
   // sweep streams (pf_api.cu segment layout): a diagonal entry (its own transpose position)
   // is packed as 1/u_rr, so the sweeps that divide multiply instead
   double2* swA = w.swA + (size_t)s * n.nsw;
@@ -739,7 +814,8 @@ int launch_eval(const DevNet& n, const Work& w, int n_scen, const double* v, con
 }
 
 static size_t lu_smem(const DevNet& n) {
-  return (size_t)(kLuThreads / 32) * n.lu_maxlen * sizeof(double) + kLuStageWarps * kLuStageBytes;
+  const size_t rows = (size_t)(kLuThreads / 32) * n.lu_maxlen * sizeof(double) + kLuStageWarps * kLuStageBytes;
+  return std::max(rows, (size_t)n.fr_n * (n.fr_n + 1) * sizeof(double));  // the front reuses the area
 }
 
 int lu_cluster_size(const DevNet& n) {

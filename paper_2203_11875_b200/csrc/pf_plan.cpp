@@ -264,7 +264,10 @@ std::string build_plan(int n_b, int n_l, int n_g, const int32_t* lf, const int32
       int kk = P.lu_idx[e];
       if (kk < r)
         for (int s = P.lu_diag[kk] + 1; s < P.lu_ptr[kk + 1]; ++s)
+        {
           P.upd_dst.push_back(find_in_row(P.lu_ptr, P.lu_idx, r, P.lu_idx[s]) - P.lu_ptr[r]);  // offset in row r
+          P.upd_src.push_back(s);  // the U value u_kj (lu index)
+        }
       P.upd_ptr[e + 1] = (int)P.upd_dst.size();
     }
   for (int d : P.upd_dst) if (d < 0) return "internal error: fill pattern not closed";

@@ -38,6 +38,7 @@ struct Plan {
   std::vector<int> bus_order, perm, iperm, blk_ptr, blk_bus, row_blk;
   std::vector<int> lu_ptr, lu_idx, lu_diag, lu_src, lu_tpos;
   std::vector<int> upd_ptr, upd_dst;       // per LU entry: range in upd_dst (L entries only); dst = offset in the row
+  std::vector<int> upd_src;                // … and the lu index of the U value u_kj each update reads
   int lu_maxlen = 0;                       // longest row of the filled pattern
   std::vector<int> levL_ptr, levL_blk, levU_ptr, levU_blk;
   std::vector<double> row_scale_dummy;

@@ -21,7 +21,7 @@ pts = [pt] + [make_scenario(net, pt, s) for s in range(1, S)]
 h = pkg.Network(net, max_batch=64, max_scen=S)
 lib = pkg.load_library()
 nlev = h.dims["n_levels_l"]
-tr = torch.zeros(nlev + 2, dtype=torch.int64, device="cuda")
+tr = torch.zeros(1024 + 8 * (nlev + 2), dtype=torch.int64, device="cuda")
 lib.pf_debug_set_lu_trace(ctypes.c_void_p(tr.data_ptr()))
 dev = lambda k: torch.as_tensor(np.stack([p[k] for p in pts]), device="cuda")  # noqa: E731
 v, th = dev("v"), dev("theta")
@@ -32,6 +32,13 @@ t = tr.cpu().numpy().astype(np.float64)
 dt = np.diff(t[: nlev + 1]) / 1e3
 lp = np.asarray(h.structure("level_l_ptr"))
 cnt = np.diff(lp)
+ph = t[1024:1024 + 8 * nlev].reshape(nlev, 8)
+print("CTA 0 warp 0, per level: load | stage | chain | store+pair | done -> cluster.sync done (us)")
+for l in range(0, nlev, 3):
+    r = ph[l]
+    if r[0] > 0 and t[l + 1] > 0:
+        d = lambda a, b: (r[b] - r[a]) / 1e3 if r[a] > 0 and r[b] > 0 else float("nan")
+        print("  lev %3d  %6.2f %6.2f %6.2f %6.2f  sync %6.2f" % (l, d(0, 1), d(1, 2), d(2, 3) if r[2] > 0 else d(1, 3), d(3, 4), (t[l + 1] - r[5]) / 1e3 if r[5] > 0 else float("nan")))
 print("k_lu levels: total %.1f us over %d levels" % (dt.sum(), nlev))
 order = np.argsort(-dt)[:15]
 for l in sorted(order):
