@@ -641,14 +641,11 @@ __global__ void k_pack_gu(DevNet n, Work w, int n_scen) {
 // e. K̂V = H_u − (P G_u)ᵀ Ψ̃ for a chunk of kCH columns of one tile: a column's
 // packed G_u entries are fetched lane-parallel (the next column's while this one
 // is gathered), its Ψ̃ rows gathered kPG at a time; the chunk is transposed in
-// SMEM so every direction's run of kCH outputs is stored contiguously.
+// SMEM (T) so every direction's run of kCH outputs is stored contiguously.
 template <int C>
-__global__ void __launch_bounds__(kThreads) k_proj(DevNet n, Work w, int N, double* __restrict__ KV) {
+__device__ __forceinline__ void proj_chunk(const DevNet& n, const Work& w, int N, double* __restrict__ KV, int c0,
+                                           int tile, int s, size_t cta, double (*T)[kCH + 1]) {
   constexpr int W = Geo<C>::W, CPL = Geo<C>::CPL, kPG = 4;
-  __shared__ double T[C][kCH + 1];
-  const int ntile = (N + C - 1) / C;
-  const int c0 = blockIdx.x * kCH, tile = blockIdx.y, s = blockIdx.z;
-  const size_t cta = (size_t)s * ntile + tile;
   const int lane = threadIdx.x % W, team = threadIdx.x / W, nteam = blockDim.x / W;
   const unsigned mask = team_mask<W>();
   const int n_u = n.n_u;
@@ -705,6 +702,15 @@ __global__ void __launch_bounds__(kThreads) k_proj(DevNet n, Work w, int N, doub
     const int jj = tile * C + jl;
     if (jj < N && k < cend) KV[((size_t)s * N + jj) * n_u + c0 + k] = T[jl][k];
   }
+  __syncthreads();  // T is reused by the next chunk
+}
+
+template <int C>
+__global__ void __launch_bounds__(kThreads) k_proj(DevNet n, Work w, int N, double* __restrict__ KV) {
+  __shared__ double T[C][kCH + 1];
+  const int ntile = (N + C - 1) / C;
+  const int tile = blockIdx.y, s = blockIdx.z;
+  proj_chunk<C>(n, w, N, KV, blockIdx.x * kCH, tile, s, (size_t)s * ntile + tile, T);
 }
 
 // ---------------------------------------------------------------- NEXT-1 / NEXT-2 single-direction passes
