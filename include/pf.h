@@ -64,6 +64,10 @@ typedef struct {
      tile_cols; rows the adjoint Lᵀ sweep visits (ancestors of G_u's rows);
      distinct rows of G_u (where the projection G_uᵀΨ reads Ψ). */
   int32_t reach_rows_l, reach_rows_ua, gu_rows;
+  /* LU schedule (A5): rows of the dense front (levels >= front_level, at most
+     96, eliminated as one dense LU in SMEM); levels < lu_cut_level run as
+     per-warp-pair subtree walks over lu_pairs pairs (PF_LU_SUBTREE_*).     */
+  int32_t front_level, front_rows, lu_cut_level, lu_pairs;
 } pf_dims;
 
 /* Host copies of the integer structure, for bit-exact tests (R19, P15). */
@@ -86,7 +90,11 @@ typedef enum {
   PF_LEVEL_L_PTR = 15, /* [n_levels_l+1]                                    */
   PF_LEVEL_L_BLK = 16, /* [n_blocks] blocks by forward level, ascending      */
   PF_LEVEL_U_PTR = 17, /* [n_levels_u+1]                                    */
-  PF_LEVEL_U_BLK = 18  /* [n_blocks] blocks by backward level, ascending     */
+  PF_LEVEL_U_BLK = 18, /* [n_blocks] blocks by backward level, ascending     */
+  PF_FRONT_ROW = 19,   /* [front_rows] permuted rows of the dense LU front     */
+  PF_LU_SUBTREE_PTR = 20, /* [lu_pairs+1] per warp pair: its bottom blocks in  */
+  PF_LU_SUBTREE_BLK = 21, /* PF_LU_SUBTREE_BLK[ptr[t] … ptr[t+1]), postorder   */
+  PF_LU_LEVEL_BLK = 22 /* [n_blocks] PF_LEVEL_L_BLK, each level longest rows first */
 } pf_structure;
 
 /*

@@ -30,8 +30,6 @@ struct pf_net {
   bool prof = false;         // instrumentation: events around the hot kernels
   int reach_rows_l = 0, reach_rows_ua = 0, gu_rows = 0;  // sparse-RHS statistics (pf_dims)
   std::vector<int4> p1_task;  // bottom-subtree schedules (host copies for the upload)
-  std::vector<int> lu_p1_blk, lu_p1_ptr;  // … and k_lu's (blocks per warp pair)
-  std::vector<int> lu_lev_blk;            // k_lu's level-synchronous block order
   std::vector<int> p1_ptr;
   std::vector<int4> u_top, u_bot, ua_top, ua_bot;
   std::vector<int> u_top_ptr, u_bot_ptr, ua_top_ptr, ua_bot_ptr;
@@ -42,9 +40,7 @@ struct pf_net {
 #ifndef PF_P1_IMB
 #define PF_P1_IMB 10
 #endif
-#ifndef PF_LU_IMB
-#define PF_LU_IMB 30
-#endif
+
 
 static std::string g_build_err;
 
@@ -238,24 +234,11 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
     levUa_ptr[l + 1] = (int)taskUa.size();
   }
   d.ntc = ntc; d.bmw = bmw;
-  // dense LU front: the lowest level cut whose rows (levels ≥ cut) number at most kFrontMax
-  std::vector<int> fr_row, fr_pos(P.n_x, -1);
-  {
-    std::vector<int> row_lev(P.n_x, 0), cnt_ge(nlevL + 1, 0);
-    for (int l = 0; l < nlevL; ++l)
-      for (int bi = P.levL_ptr[l]; bi < P.levL_ptr[l + 1]; ++bi) {
-        const int p = P.levL_blk[bi];
-        for (int r = P.blk_ptr[p]; r < P.blk_ptr[p + 1]; ++r) row_lev[r] = l;
-      }
-    for (int r = 0; r < P.n_x; ++r) ++cnt_ge[row_lev[r]];
-    for (int l = nlevL - 1; l >= 0; --l) cnt_ge[l] += cnt_ge[l + 1];
-    int cut = nlevL;
-    while (cut > 0 && cnt_ge[cut - 1] <= kFrontMax) --cut;
-    d.fr_lev = cut;
-    for (int r = 0; r < P.n_x; ++r)
-      if (row_lev[r] >= cut) { fr_pos[r] = (int)fr_row.size(); fr_row.push_back(r); }
-    d.fr_n = (int)fr_row.size();
-  }
+  // k_lu schedule (host plan, pf_plan.cpp lu_schedule)
+  std::vector<int> fr_pos(P.n_x, -1);
+  for (size_t f = 0; f < P.fr_row.size(); ++f) fr_pos[P.fr_row[f]] = (int)f;
+  d.fr_lev = P.fr_lev; d.fr_n = (int)P.fr_row.size();
+  d.lu_lev0 = P.lu_lev0; d.lu_nteam = kLuPairs;
   for (size_t k = 0; k < rowbm.size(); ++k) h->reach_rows_l += __builtin_popcount(rowbm[k]);
   for (int r = 0; r < P.n_x; ++r) h->reach_rows_ua += row_mark[r] == ntc;
   for (int r = 0; r < P.n_x; ++r) h->gu_rows += P.gur_ptr[r + 1] > P.gur_ptr[r];
@@ -326,24 +309,7 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
     std::vector<int> best_order, best_ptr;
     int best_lev0 = 0;
     schedule(nteam, nlevL, PF_P1_IMB, best_order, best_ptr, best_lev0);
-    {  // k_lu: warp pairs of a 16-CTA cluster (a smaller cluster walks several pairs' lists)
-      std::vector<int> lo, lp;
-      int l0 = 0;
-      schedule(kLuPairs, d.fr_lev, PF_LU_IMB, lo, lp, l0);
-      h->lu_p1_blk = lo; h->lu_p1_ptr = lp;
-      d.lu_lev0 = l0; d.lu_nteam = kLuPairs;
-      // the level-synchronous levels hand blocks to the pairs in order and only the low pairs
-      // have SMEM staging areas: longest rows first within a level
-      h->lu_lev_blk = P.levL_blk;
-      auto piv = [&](int b) {
-        int m = 0;
-        for (int r = P.blk_ptr[b]; r < P.blk_ptr[b + 1]; ++r) m = std::max(m, P.lu_diag[r] - P.lu_ptr[r]);
-        return m;
-      };
-      for (int l = 0; l < nlevL; ++l)
-        std::stable_sort(h->lu_lev_blk.begin() + P.levL_ptr[l], h->lu_lev_blk.begin() + P.levL_ptr[l + 1],
-                         [&](int x, int y) { return piv(x) > piv(y); });
-    }
+
     std::vector<int4> p1_task(best_order.size());
     for (size_t k = 0; k < best_order.size(); ++k) p1_task[k] = taskL[task_of[best_order[k]]];
     d.p1_lev0 = best_lev0;
@@ -516,8 +482,8 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
             up(h, P.gur_src, &d.gur_src) && up(h, P.bus_pth, &d.bus_pth) && up(h, P.bus_pv, &d.bus_pv) &&
             up(h, gbus, &d.gbus) && up(h, rowmeta, &d.rowmeta) && up(h, hvp_order, &d.hvp_bus) &&
             up(h, taskL, &d.taskL) && up(h, taskU, &d.taskU) && up(h, sw_src, &d.sw_src) &&
-            up(h, fr_row, &d.fr_row) && up(h, fr_pos, &d.fr_pos) && up(h, h->lu_p1_blk, &d.lu_p1_blk) &&
-            up(h, h->lu_p1_ptr, &d.lu_p1_ptr) && up(h, h->lu_lev_blk, &d.lu_lev_blk) &&
+            up(h, P.fr_row, &d.fr_row) && up(h, fr_pos, &d.fr_pos) && up(h, P.lu_p1_blk, &d.lu_p1_blk) &&
+            up(h, P.lu_p1_ptr, &d.lu_p1_ptr) && up(h, P.lu_lev_blk, &d.lu_lev_blk) &&
             up(h, taskLr, &d.taskLr) && up(h, levLr_ptr, &d.levLr_ptr) && up(h, rowbm, &d.rowbm) &&
             up(h, taskUa, &d.taskUa) && up(h, levUa_ptr, &d.levUa_ptr) && up(h, h->p1_task, &d.p1_task) &&
             up(h, h->p1_ptr, &d.p1_ptr) && up(h, h->u_top, &d.u_top) && up(h, h->u_top_ptr, &d.u_top_ptr) &&
@@ -577,6 +543,8 @@ pf_status pf_query(const pf_net* h, pf_dims* o) {
   o->n_levels_l = (int)P.levL_ptr.size() - 1; o->n_levels_u = (int)P.levU_ptr.size() - 1;
   o->max_batch = h->max_batch; o->max_scen = h->max_scen; o->tile_cols = h->C;
   o->reach_rows_l = h->reach_rows_l; o->reach_rows_ua = h->reach_rows_ua; o->gu_rows = h->gu_rows;
+  o->front_level = P.fr_lev; o->front_rows = (int)P.fr_row.size(); o->lu_cut_level = P.lu_lev0;
+  o->lu_pairs = (int)P.lu_p1_ptr.size() - 1;
   return PF_OK;
 }
 
@@ -604,6 +572,10 @@ pf_status pf_get_structure(const pf_net* h, int32_t which, int32_t* out) {
     case PF_LEVEL_L_BLK: v = &P.levL_blk; break;
     case PF_LEVEL_U_PTR: v = &P.levU_ptr; break;
     case PF_LEVEL_U_BLK: v = &P.levU_blk; break;
+    case PF_FRONT_ROW: v = &P.fr_row; break;
+    case PF_LU_SUBTREE_PTR: v = &P.lu_p1_ptr; break;
+    case PF_LU_SUBTREE_BLK: v = &P.lu_p1_blk; break;
+    case PF_LU_LEVEL_BLK: v = &P.lu_lev_blk; break;
     default: return PF_ERR_ARG;
   }
   if (!v->empty()) std::memcpy(out, v->data(), v->size() * sizeof(int32_t));

@@ -1,14 +1,10 @@
 // pf_launch.h — host launchers of the sm_100a kernels (one per hot-path step).
 #pragma once
 #include "pf_dev.cuh"
+#include "pf_plan.h"
 
 namespace pf {
 
-#ifndef PF_FRONT_MAX
-#define PF_FRONT_MAX 96
-#endif
-constexpr int kFrontMax = PF_FRONT_MAX;
-constexpr int kLuPairs = 16 * 8;  // k_lu warp pairs: a 16-CTA cluster of 512-thread CTAs  // rows of the dense LU front (k_lu: F (F + 1) doubles of SMEM)
 
 // A2/A3: line kernel (ψ, flows, H) then bus gather (G).  Returns launches.
 int launch_eval(const DevNet& n, const Work& w, int n_scen, const double* v, const double* th,

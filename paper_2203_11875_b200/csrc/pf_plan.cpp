@@ -22,6 +22,103 @@ int find_in_row(const std::vector<int>& ptr, const std::vector<int>& idx, int ro
 
 }  // namespace
 
+// k_lu's schedule (A5).  (1) The dense front: the rows of levels ≥ fr_lev, the lowest cut that
+// leaves at most kFrontMax rows, ascending permuted index.  The set is closed upwards (a row's
+// L pivots lie in lower levels), so no row outside the front has a front pivot.  (2) Below
+// lu_lev0 the bottom subtrees of the block elimination forest (a block's parent is the block of
+// its last row's first L-column successor), balanced over kLuPairs warp pairs: the deepest cut
+// ≤ fr_lev whose largest pair load stays within PF_LU_IMB % of the mean; each pair's subtrees in
+// postorder (children first).  (3) For the levels between, each level's blocks with the longest
+// rows first (only the low pairs have SMEM staging areas).
+void lu_schedule(Plan& P) {
+  const int n_x = P.n_x, nblk = (int)P.blk_bus.size(), nlev = (int)P.levL_ptr.size() - 1;
+  std::vector<int> row_lev(n_x, 0), blk_lev(nblk, 0), cnt_ge(nlev + 1, 0);
+  for (int l = 0; l < nlev; ++l)
+    for (int bi = P.levL_ptr[l]; bi < P.levL_ptr[l + 1]; ++bi) {
+      const int b = P.levL_blk[bi];
+      blk_lev[b] = l;
+      for (int r = P.blk_ptr[b]; r < P.blk_ptr[b + 1]; ++r) row_lev[r] = l;
+    }
+  for (int r = 0; r < n_x; ++r) ++cnt_ge[row_lev[r]];
+  for (int l = nlev - 1; l >= 0; --l) cnt_ge[l] += cnt_ge[l + 1];
+  int cut = nlev;
+  while (cut > 0 && cnt_ge[cut - 1] <= kFrontMax) --cut;
+  P.fr_lev = cut;
+  P.fr_row.clear();
+  for (int r = 0; r < n_x; ++r) if (row_lev[r] >= cut) P.fr_row.push_back(r);
+  // block elimination forest
+  std::vector<int> parent(n_x, -1), bpar(nblk, -1);
+  for (int r = 0; r < n_x; ++r)
+    for (int e = P.lu_ptr[r]; e < P.lu_diag[r]; ++e)
+      if (parent[P.lu_idx[e]] < 0) parent[P.lu_idx[e]] = r;
+  for (int b = 0; b < nblk; ++b) {
+    const int last = P.blk_ptr[b + 1] - 1;
+    if (parent[last] >= 0) bpar[b] = P.row_blk[parent[last]];
+  }
+  const int nteam = kLuPairs;
+  std::vector<int> root(nblk);
+  P.lu_lev0 = 0;
+  P.lu_p1_blk.clear();
+  P.lu_p1_ptr.assign(nteam + 1, 0);
+  for (int lev0 = 1; lev0 <= cut; ++lev0) {
+    for (int l = lev0 - 1; l >= 0; --l)
+      for (int bi = P.levL_ptr[l]; bi < P.levL_ptr[l + 1]; ++bi) {
+        const int b = P.levL_blk[bi], q = bpar[b];
+        root[b] = (q >= 0 && blk_lev[q] < lev0) ? root[q] : b;
+      }
+    std::vector<std::vector<int>> kids(nblk);
+    std::vector<int> roots, size(nblk, 1);
+    for (int l = 0; l < lev0; ++l)
+      for (int bi = P.levL_ptr[l]; bi < P.levL_ptr[l + 1]; ++bi) {
+        const int b = P.levL_blk[bi];
+        if (root[b] == b) roots.push_back(b); else kids[bpar[b]].push_back(b);
+      }
+    for (int l = 0; l < lev0; ++l)  // subtree sizes, children before parents
+      for (int bi = P.levL_ptr[l]; bi < P.levL_ptr[l + 1]; ++bi) {
+        const int b = P.levL_blk[bi];
+        if (root[b] != b) size[bpar[b]] += size[b];
+      }
+    std::sort(roots.begin(), roots.end(), [&](int x, int y) { return size[x] != size[y] ? size[x] > size[y] : x < y; });
+    std::vector<long long> load(nteam, 0);
+    std::vector<std::vector<int>> mine(nteam);
+    for (int r : roots) {
+      const int t = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+      load[t] += size[r];
+      mine[t].push_back(r);
+    }
+    long long tot = 0, mx = 0;
+    for (long long x : load) { tot += x; mx = std::max(mx, x); }
+    if (lev0 > 1 && mx * 100 > tot * (100 + PF_LU_IMB) / nteam) break;
+    std::vector<int> order, ptr(nteam + 1, 0);
+    for (int t = 0; t < nteam; ++t) {
+      for (int r : mine[t]) {  // iterative postorder of the subtree of r
+        std::vector<std::pair<int, size_t>> st{{r, 0}};
+        while (!st.empty()) {
+          auto& top = st.back();
+          if (top.second < kids[top.first].size()) {
+            const int ch = kids[top.first][top.second++];
+            st.push_back({ch, 0});
+          } else {
+            order.push_back(top.first);
+            st.pop_back();
+          }
+        }
+      }
+      ptr[t + 1] = (int)order.size();
+    }
+    P.lu_p1_blk.swap(order); P.lu_p1_ptr.swap(ptr); P.lu_lev0 = lev0;
+  }
+  P.lu_lev_blk = P.levL_blk;
+  auto piv = [&](int b) {
+    int m = 0;
+    for (int r = P.blk_ptr[b]; r < P.blk_ptr[b + 1]; ++r) m = std::max(m, P.lu_diag[r] - P.lu_ptr[r]);
+    return m;
+  };
+  for (int l = 0; l < nlev; ++l)
+    std::stable_sort(P.lu_lev_blk.begin() + P.levL_ptr[l], P.lu_lev_blk.begin() + P.levL_ptr[l + 1],
+                     [&](int x, int y) { return piv(x) > piv(y); });
+}
+
 std::string build_plan(int n_b, int n_l, int n_g, const int32_t* lf, const int32_t* lt,
                        const int32_t* gen_bus, int ref_bus, const double* F_max, Plan& P,
                        bool* topology) {
@@ -315,6 +412,7 @@ std::string build_plan(int n_b, int n_l, int n_g, const int32_t* lf, const int32
         P.guc_row[fill[c]] = r; P.guc_src[fill[c]] = P.gur_src[e]; fill[c]++;
       }
   }
+  lu_schedule(P);
   P.hvp_bus = P.bus_order;
   P.hvp_bus.push_back(ref_bus);
   P.bus_pth.assign(n_b, -1); P.bus_pv.assign(n_b, -1);

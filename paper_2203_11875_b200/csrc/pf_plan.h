@@ -9,6 +9,15 @@
 
 namespace pf {
 
+#ifndef PF_FRONT_MAX
+#define PF_FRONT_MAX 96
+#endif
+#ifndef PF_LU_IMB
+#define PF_LU_IMB 30
+#endif
+constexpr int kFrontMax = PF_FRONT_MAX;  // rows of the dense LU front (k_lu: F (F + 1) doubles of SMEM)
+constexpr int kLuPairs = 16 * 8;         // k_lu warp pairs: a 16-CTA cluster of 512-thread CTAs
+
 struct Plan {
   int n_b = 0, n_l = 0, n_g = 0, n_x = 0, n_u = 0, m = 0, n_r = 0, n_h = 0;
   int r0 = -1, g_r = -1, n_gb = 0;
@@ -50,7 +59,14 @@ struct Plan {
   // bus -> permuted slab rows
   std::vector<int> bus_pth, bus_pv;
   std::vector<int> hvp_bus;   // elimination order, reference bus last
+
+  // k_lu schedule (lu_schedule): dense front rows (levels ≥ fr_lev, ascending), bottom subtrees
+  // per warp pair below lu_lev0 (lu_p1_blk[lu_p1_ptr[t] …]), per-level order longest rows first
+  int fr_lev = 0, lu_lev0 = 0;
+  std::vector<int> fr_row, lu_p1_blk, lu_p1_ptr, lu_lev_blk;
 };
+
+void lu_schedule(Plan& P);
 
 // Returns "" on success, else an error message; *topology is set when the
 // failure is a topology error (PF_ERR_TOPOLOGY) rather than an argument error.

@@ -20,7 +20,8 @@ _STATUS = {1: "PF_ERR_ARG", 2: "PF_ERR_TOPOLOGY", 3: "PF_ERR_CAPACITY", 4: "PF_E
 
 STRUCTURE = dict(x_theta=0, x_v=1, u_v=2, u_p=3, gx_ptr=4, gx_idx=5, gu_ptr=6, gu_idx=7, a_ptr=8, a_idx=9,
                  bus_order=10, perm=11, block_ptr=12, lu_ptr=13, lu_idx=14, level_l_ptr=15, level_l_blk=16,
-                 level_u_ptr=17, level_u_blk=18)
+                 level_u_ptr=17, level_u_blk=18, front_row=19, lu_subtree_ptr=20, lu_subtree_blk=21,
+                 lu_level_blk=22)
 
 # exported symbols declared in include/pf.h
 SYMBOLS = ["pf_build_network", "pf_build_network_ex", "pf_destroy", "pf_query", "pf_get_structure", "pf_last_error", "pf_build_error",
@@ -39,7 +40,7 @@ class pf_dims(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "n_b", "n_l", "n_g", "n_x", "n_u", "m", "n_r", "n_h", "ref_bus", "ref_gen", "nnz_gx", "nnz_gu", "nnz_a",
         "nnz_lu", "n_blocks", "n_levels_l", "n_levels_u", "max_batch", "max_scen", "tile_cols",
-        "reach_rows_l", "reach_rows_ua", "gu_rows")]
+        "reach_rows_l", "reach_rows_ua", "gu_rows", "front_level", "front_rows", "lu_cut_level", "lu_pairs")]
 
 
 _lib = None
@@ -187,7 +188,10 @@ class Network:
                      gx_idx=d["nnz_gx"], gu_ptr=d["n_x"] + 1, gu_idx=d["nnz_gu"], a_ptr=d["m"] + 1,
                      a_idx=d["nnz_a"], bus_order=d["n_blocks"], perm=d["n_x"], block_ptr=d["n_blocks"] + 1,
                      lu_ptr=d["n_x"] + 1, lu_idx=d["nnz_lu"], level_l_ptr=d["n_levels_l"] + 1,
-                     level_l_blk=d["n_blocks"], level_u_ptr=d["n_levels_u"] + 1, level_u_blk=d["n_blocks"])
+                     level_l_blk=d["n_blocks"], level_u_ptr=d["n_levels_u"] + 1, level_u_blk=d["n_blocks"],
+                     front_row=d["front_rows"], lu_subtree_ptr=d["lu_pairs"] + 1, lu_level_blk=d["n_blocks"])
+        if name == "lu_subtree_blk":
+            sizes[name] = int(self.structure("lu_subtree_ptr")[-1])
         out = np.zeros(max(sizes[name], 1), dtype=np.int32)
         self._check(self._lib.pf_get_structure(self._h, STRUCTURE[name], out.ctypes.data_as(ctypes.c_void_p)),
                     "pf_get_structure")

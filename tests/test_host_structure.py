@@ -103,3 +103,61 @@ def test_host_only_handle_refuses_compute(pfmod):
     st = lib.pf_jacobian(h._h, 1, ctypes.c_void_p(8), ctypes.c_void_p(8), None, None, None, None, None)
     assert st == 5
     h.close()
+
+
+@pytest.mark.parametrize("name,net,pt", _nets())
+def test_lu_schedule(pfmod, name, net, pt):
+    """k_lu's schedule (A5) against the oracle's own symbolic LU: the dense front is the set of
+    rows of levels >= front_level (the lowest cut with at most 96 rows) and is closed upwards
+    (no row outside it has a pivot inside it); the bottom subtree lists cover every block below
+    lu_cut_level exactly once, and every block a listed block depends on (an L pivot's block)
+    comes earlier in the same pair's list; each level's LU order is a permutation of the level."""
+    h = pfmod.Network(net, max_batch=8, max_scen=1, device=-1)
+    part = O.partition(net)
+    d = h.dims
+    (px, ix), _ = O.gx_gu_patterns(net, part)
+    perm, blk = O.permutation(part, O.md_ordering(net, part))
+    F = O.symbolic_lu(px, ix, perm)
+    lp, li = O.filled_csr(F)
+    levL, _ = O.block_levels(F, blk)
+    levL = np.asarray(levL)
+    nblk = len(blk) - 1
+    row_blk = np.repeat(np.arange(nblk), np.diff(blk))
+    row_lev = levL[row_blk]
+    n_x = len(lp) - 1
+    fl = d["front_level"]
+    front = h.structure("front_row")
+    assert np.array_equal(front, np.nonzero(row_lev >= fl)[0])
+    assert d["front_rows"] == len(front) <= 96
+    if fl > 0:
+        assert (row_lev >= fl - 1).sum() > 96, "the cut is not the lowest one"
+    infront = np.zeros(n_x, bool)
+    infront[front] = True
+    for r in np.nonzero(~infront)[0]:
+        piv = li[lp[r]:lp[r + 1]]
+        assert not infront[piv[piv < r]].any(), "row %d outside the front has a front pivot" % r
+    # bottom subtree lists
+    cut = d["lu_cut_level"]
+    assert 0 <= cut <= fl
+    ptr = h.structure("lu_subtree_ptr")
+    lst = h.structure("lu_subtree_blk")
+    assert d["lu_pairs"] == len(ptr) - 1 and ptr[0] == 0 and ptr[-1] == len(lst)
+    assert np.array_equal(np.sort(lst), np.nonzero(levL < cut)[0])
+    deps = [set() for _ in range(nblk)]
+    for r in range(n_x):
+        piv = li[lp[r]:lp[r + 1]]
+        for c in piv[piv < r]:
+            if row_blk[c] != row_blk[r]:
+                deps[row_blk[r]].add(int(row_blk[c]))
+    for t in range(len(ptr) - 1):
+        seen = set()
+        for b in lst[ptr[t]:ptr[t + 1]]:
+            assert deps[b] <= seen, "pair %d: block %d before its dependencies" % (t, b)
+            seen.add(int(b))
+    # per-level LU order: a permutation of each level set
+    lptr = h.structure("level_l_ptr")
+    lblk = h.structure("level_l_blk")
+    lub = h.structure("lu_level_blk")
+    for l in range(len(lptr) - 1):
+        assert np.array_equal(np.sort(lub[lptr[l]:lptr[l + 1]]), np.sort(lblk[lptr[l]:lptr[l + 1]]))
+    h.close()
