@@ -31,6 +31,8 @@ struct pf_net {
   int reach_rows_l = 0, reach_rows_ua = 0, gu_rows = 0;  // sparse-RHS statistics (pf_dims)
   std::vector<int4> p1_task;  // bottom-subtree schedules (host copies for the upload)
   std::vector<int> p1_ptr;
+  std::vector<int4> p1r_task;  // … restricted to each canonical tile's reach ([ntc][teams + 1] pointers)
+  std::vector<int> p1r_ptr;
   std::vector<int4> u_top, u_bot, ua_top, ua_bot;
   std::vector<int> u_top_ptr, u_bot_ptr, ua_top_ptr, ua_bot_ptr;
   std::vector<int> hvp_order;  // k_hvp bus order (elimination-forest postorder)
@@ -315,6 +317,23 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
     d.p1_lev0 = best_lev0;
     h->p1_task = p1_task;
     h->p1_ptr = best_ptr;
+    // k_fwd's reach-restricted L sweep (unit directions of canonical tile t): the same bottom
+    // lists filtered to the tile's reach blocks (postorder kept), then its reach levels ≥ lev0
+    // (own marks: blk_mark still holds the ancestor pass's stamps for the Lᵀ lists below)
+    h->p1r_task.clear();
+    h->p1r_ptr.assign((size_t)ntc * (nteam + 1), 0);
+    std::vector<int> rmk(P.n_x, -1), bmk(nblk, -1);
+    for (int t = 0; t < ntc; ++t) {
+      for (int c = t * TC; c < std::min(P.n_u, (t + 1) * TC); ++c)
+        for (int e = P.guc_ptr[c]; e < P.guc_ptr[c + 1]; ++e)
+          for (int r = P.guc_row[e]; r >= 0 && rmk[r] != t; r = parent[r]) { rmk[r] = t; bmk[P.row_blk[r]] = t; }
+      for (int tm = 0; tm < nteam; ++tm) {
+        h->p1r_ptr[(size_t)t * (nteam + 1) + tm] = (int)h->p1r_task.size();
+        for (int k = best_ptr[tm]; k < best_ptr[tm + 1]; ++k)
+          if (bmk[best_order[k]] == t) h->p1r_task.push_back(taskL[task_of[best_order[k]]]);
+      }
+      h->p1r_ptr[(size_t)t * (nteam + 1) + nteam] = (int)h->p1r_task.size();
+    }
     // UPPER sweeps (parents before children): the blocks above the cut in U-level
     // order, then each team's bottom subtrees in reverse postorder; once over all
     // blocks (U sweep) and once over the ancestors of G_u's rows (Lᵀ sweep).
@@ -486,7 +505,7 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
             up(h, P.lu_p1_ptr, &d.lu_p1_ptr) && up(h, P.lu_lev_blk, &d.lu_lev_blk) &&
             up(h, taskLr, &d.taskLr) && up(h, levLr_ptr, &d.levLr_ptr) && up(h, rowbm, &d.rowbm) &&
             up(h, taskUa, &d.taskUa) && up(h, levUa_ptr, &d.levUa_ptr) && up(h, h->p1_task, &d.p1_task) &&
-            up(h, h->p1_ptr, &d.p1_ptr) && up(h, h->u_top, &d.u_top) && up(h, h->u_top_ptr, &d.u_top_ptr) &&
+            up(h, h->p1_ptr, &d.p1_ptr) && up(h, h->p1r_task, &d.p1r_task) && up(h, h->p1r_ptr, &d.p1r_ptr) && up(h, h->u_top, &d.u_top) && up(h, h->u_top_ptr, &d.u_top_ptr) &&
             up(h, h->u_bot, &d.u_bot) && up(h, h->u_bot_ptr, &d.u_bot_ptr) && up(h, h->ua_top, &d.ua_top) &&
             up(h, h->ua_top_ptr, &d.ua_top_ptr) && up(h, h->ua_bot, &d.ua_bot) && up(h, h->ua_bot_ptr, &d.ua_bot_ptr) &&
             up(h, P.perm, &d.perm) && up(h, P.iperm, &d.iperm) && up(h, row_g, &d.row_g) &&

@@ -58,6 +58,8 @@ struct DevNet {
   const int4 *p1_task;          // bottom-subtree schedule of the LOWER sweeps: per team, its subtrees in postorder
   const int *p1_ptr;            // [teams per CTA + 1]
   int p1_lev0;                  // levels < p1_lev0 run from p1_task, the rest level by level
+  const int4 *p1r_task;         // per canonical tile: p1_task restricted to the tile's reach blocks
+  const int *p1r_ptr;           // [ntc][teams + 1] absolute offsets into p1r_task
   // UPPER sweeps: blocks above the cut by U level (u_top, [nlevU+1] pointers), then the
   // bottom subtrees per team parents-first (u_bot, [teams+1]); ua_*: the same restricted
   // to the ancestors of G_u's rows (the Lᵀ sweep)

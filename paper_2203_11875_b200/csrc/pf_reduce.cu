@@ -448,7 +448,8 @@ __global__ void __launch_bounds__(kThreads, kSweepMinBlocks) k_fwd(DevNet n, Wor
         X[(size_t)__ldg(n.guc_row + e) * C + c] = -gu[__ldg(n.guc_src + e)];
     __syncthreads();
     sweep<C, true, true>(n.taskLr, n.levLr_ptr + (size_t)(rt + tile) * (n.nlevL + 1), n.nlevL, pk, X, false, lane, team,
-                   nteam, ent, FromSlabMarked{rhs_sm}, bm_sm, nullptr, nullptr, 0, 0);                                   // L^{-1} B
+                         nteam, ent, FromSlabMarked{rhs_sm}, bm_sm, n.p1r_task,
+                         n.p1r_ptr + (size_t)(rt + tile) * (nteam + 1), n.p1_lev0, 0);                                   // L^{-1} B
     sweep<C, false>(n.u_top, n.u_top_ptr, n.nlevU, pk, X, true, lane, team, nteam, ent, FromSlabReach{bm_sm}, nullptr,
                     n.u_bot, n.u_bot_ptr, 0, 1);                                                 // U^{-1}
   } else {
