@@ -346,7 +346,7 @@ __device__ int potrf64(double* Cs, double* rdv, int* sh) {
       double* row = Cs + (b0 + r) * LDC + b0;
       double x[SB];
 #pragma unroll
-      for (int k = 0; k < SB; ++k) x[k] = row[k];
+      for (int k = 0; k < SB; ++k) x[k] = lane < SB ? row[k] : 0.0;  // lanes ≥ 16 only join the shuffles
       int bad = 0;
 #pragma unroll
       for (int c = 0; c < SB; ++c) {
@@ -427,20 +427,29 @@ __device__ void trinv64(const double* Cs, const double* rdv, double* Li, double*
     for (int r = 0; r < SB; ++r) Li[(b0 + c) * LDT + b0 + r] = y[r];
   }
   cons_sync();
+  // block diagonals d = 1 … 3 on DMMA (m8n8k4): each 16×16 block is 2×2 output tiles of 8×8,
+  // warps round-robin over the diagonal's tiles
+  const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
   for (int d = 1; d < NB / SB; ++d) {
-    const int nblk = NB / SB - d;  // blocks (i, i − d), i = d … 3
-    for (int e = tid; e < nblk * SB * SB; e += kCons) {
-      const int bi = e >> 8, r = (e >> 4) & (SB - 1), c = e & (SB - 1), i = d + bi, j = bi;
-      double v = 0.0;
-      for (int k = j * SB; k < i * SB; ++k) v += Cs[(i * SB + r) * LDC + k] * Li[(j * SB + c) * LDT + k];
-      tmp[e] = v;  // T_ij(r, c) = Σ_k L_ik L⁻¹_kj
+    const int ntl = (NB / SB - d) * 4;  // blocks (i, i − d), i = d … 3, × 4 tiles
+    for (int tt = warp; tt < ntl; tt += kCons / 32) {  // T_ij = Σ_{k=j}^{i−1} L_ik L⁻¹_kj
+      const int bi = tt >> 2, i = d + bi, j = bi, r0 = i * SB + (tt & 2) * 4, c0 = j * SB + (tt & 1) * 8;
+      double t0 = 0.0, t1 = 0.0;
+      for (int k0 = j * SB; k0 < i * SB; k0 += 4)
+        dmma_8x8x4(t0, t1, Cs[(r0 + g) * LDC + k0 + q], Li[(c0 + g) * LDT + k0 + q]);
+      const int rr = r0 - i * SB, cc = c0 - j * SB;  // position inside the 16×16 block
+      tmp[(bi << 8) + (rr + g) * SB + cc + 2 * q] = t0;
+      tmp[(bi << 8) + (rr + g) * SB + cc + 2 * q + 1] = t1;
     }
     cons_sync();
-    for (int e = tid; e < nblk * SB * SB; e += kCons) {
-      const int bi = e >> 8, r = (e >> 4) & (SB - 1), c = e & (SB - 1), i = d + bi, j = bi;
-      double v = 0.0;
-      for (int k = 0; k <= r; ++k) v += Li[(i * SB + k) * LDT + i * SB + r] * tmp[(bi << 8) + (k << 4) + c];
-      Li[(j * SB + c) * LDT + i * SB + r] = -v;
+    for (int tt = warp; tt < ntl; tt += kCons / 32) {  // L⁻¹_ij = −L⁻¹_ii T_ij
+      const int bi = tt >> 2, i = d + bi, j = bi, rr = (tt & 2) * 4, cc = (tt & 1) * 8;
+      double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+      for (int k0 = 0; k0 < SB; k0 += 4)
+        dmma_8x8x4(v0, v1, -Li[(i * SB + k0 + q) * LDT + i * SB + rr + g], tmp[(bi << 8) + (k0 + q) * SB + cc + g]);
+      Li[(j * SB + cc + 2 * q) * LDT + i * SB + rr + g] = v0;
+      Li[(j * SB + cc + 2 * q + 1) * LDT + i * SB + rr + g] = v1;
     }
     cons_sync();
   }
