@@ -97,11 +97,17 @@ __device__ __forceinline__ void fence_proxy_shared() { asm volatile("fence.proxy
 __device__ __forceinline__ void mbar_expect(uint64_t* b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
 }
+#ifndef PF_CHOL_SPIN_NS
+#define PF_CHOL_SPIN_NS 64
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
   unsigned done = 0;
-  while (!done)
+  for (;;) {
     asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
                  : "=r"(done) : "r"(saddr(b)), "r"(parity) : "memory");
+    if (done) break;
+    if (PF_CHOL_SPIN_NS) __nanosleep(PF_CHOL_SPIN_NS);  // let the co-resident CTA's warps issue
+  }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"

@@ -27,6 +27,9 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kCH = 64;        // u-columns per transposed output chunk
+#ifndef PF_BLK_SPIN_NS
+#define PF_BLK_SPIN_NS 64
+#endif
 #ifndef PF_SWEEP_MIN_BLOCKS
 #define PF_SWEEP_MIN_BLOCKS 3
 #endif
@@ -531,54 +534,87 @@ __global__ void __launch_bounds__(kThreads, 4) k_blk(DevNet n, Work w, const dou
   double* Hs = w.hu + cta * n.n_u * C;
   const double* bsv = w.bs + (size_t)s * BS_N * n.n_b;
   {
+    // back off between polls: the co-resident CTAs' computing warps keep the issue slots
     unsigned done = 0;
-    while (!done)
+    for (;;) {
       asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
                    : "=r"(done) : "r"(sm_addr(&bar)) : "memory");
+      if (done) break;
+      __nanosleep(PF_BLK_SPIN_NS);
+    }
   }
   const double2* vv = reinterpret_cast<const double2*>(vals);
+  const double* myrow = stg + lane * CPL;  // this lane's columns of staged row 0
   for (int p = team; p < p1 - p0; p += nteam) {
     const int4 me = bmeta[p];
     double ath[CPL], av[CPL];
 #pragma unroll
     for (int j = 0; j < CPL; ++j) { ath[j] = 0.0; av[j] = 0.0; }
     const int eb = __ldg(B.ptr + p0 + p) - e0, ee = __ldg(B.ptr + p0 + p + 1) - e0;
-    double th_i[CPL];  // dθ of the bus itself (its block comes first)
-    for (int e = eb; e < ee; ++e) {
-      const int4 m = meta[e];
-      const double2 b0 = vv[4 * e], b1 = vv[4 * e + 1];
-      double dth[CPL], dv[CPL];
-      if (m.x >= 0) row_ld<C>(stg, m.x, lane, dth);
-      else
-#pragma unroll
-        for (int j = 0; j < CPL; ++j) dth[j] = 0.0;
-      if (m.y >= 0) row_ld<C>(stg, m.y, lane, dv);
-      else
-#pragma unroll
-        for (int j = 0; j < CPL; ++j) dv[j] = d.vdir(-1 - m.y, j);
-      if (e == eb) {
-#pragma unroll
-        for (int j = 0; j < CPL; ++j) th_i[j] = dth[j];  // the diagonal θ column is Σ_x (k_hvp) or 0 (k_mu)
+    auto rld = [&](int slot, double* o) {
+      if constexpr (CPL == 2) {
+        const double2 v = *reinterpret_cast<const double2*>(myrow + (size_t)slot * C);
+        o[0] = v.x; o[1] = v.y;
       } else {
 #pragma unroll
-        for (int j = 0; j < CPL; ++j) dth[j] -= th_i[j];  // θ columns act on angle differences
+        for (int j = 0; j < CPL; ++j) o[j] = myrow[(size_t)slot * C + j];
       }
-#pragma unroll
-      for (int j = 0; j < CPL; ++j) {  // explicit FMAs: the same rounding for every tile width (T3)
-        ath[j] = fma(b0.y, dv[j], fma(b0.x, dth[j], ath[j]));
-        av[j] = fma(b1.y, dv[j], fma(b1.x, dth[j], av[j]));
-      }
-      if (!MU && m.z >= 0) {  // A_rᵀ μ_A: generator bus j (μ^P, μ^Q rows staged at m.z, m.z + 1)
+    };
+    auto jt = [&](int e, const int4& m) {  // A_rᵀ μ_A: generator bus j (μ^P, μ^Q rows staged at m.z, m.z + 1)
+      if (!MU && m.z >= 0) {
         const double2 j0 = vv[4 * e + 2], j1 = vv[4 * e + 3];
         double mp[CPL], mq[CPL];
-        row_ld<C>(stg, m.z, lane, mp);
-        row_ld<C>(stg, m.z + 1, lane, mq);
+        rld(m.z, mp);
+        rld(m.z + 1, mq);
 #pragma unroll
         for (int j = 0; j < CPL; ++j) {
           ath[j] = fma(j0.y, mq[j], fma(j0.x, mp[j], ath[j]));
           av[j] = fma(j1.y, mq[j], fma(j1.x, mp[j], av[j]));
         }
       }
+    };
+    double th_i[CPL];  // dθ of the bus itself: its own block comes first, its θ column is Σ_x (k_hvp) or 0 (k_mu)
+    {
+      const int4 m = meta[eb];
+      const double2 b0 = vv[4 * eb], b1 = vv[4 * eb + 1];
+      double dv[CPL];
+      if (m.x >= 0) rld(m.x, th_i);
+      else
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) th_i[j] = 0.0;
+      if (m.y >= 0) rld(m.y, dv);
+      else
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) dv[j] = d.vdir(-1 - m.y, j);
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {  // explicit FMAs: the same rounding for every tile width (T3)
+        ath[j] = fma(b0.y, dv[j], fma(b0.x, th_i[j], ath[j]));
+        av[j] = fma(b1.y, dv[j], fma(b1.x, th_i[j], av[j]));
+      }
+      jt(eb, m);
+    }
+    for (int e = eb + 1; e < ee; ++e) {  // neighbours: θ columns act on angle differences dθ_j − dθ_i
+      const int4 m = meta[e];
+      const double2 b0 = vv[4 * e], b1 = vv[4 * e + 1];
+      double dth[CPL], dv[CPL];
+      if (m.x >= 0) {
+        rld(m.x, dth);
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) dth[j] -= th_i[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) dth[j] = 0.0 - th_i[j];
+      }
+      if (m.y >= 0) rld(m.y, dv);
+      else
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) dv[j] = d.vdir(-1 - m.y, j);
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        ath[j] = fma(b0.y, dv[j], fma(b0.x, dth[j], ath[j]));
+        av[j] = fma(b1.y, dv[j], fma(b1.x, dth[j], av[j]));
+      }
+      jt(e, m);
     }
     if (MU) {  // me = {bus, gen}: μ^P = Σ_rP dP, μ^Q = Σ_rQ dQ
       const double srp = bsv[BS_SRP * n.n_b + me.x], srq = bsv[BS_SRQ * n.n_b + me.x];
