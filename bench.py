@@ -497,9 +497,15 @@ def main():
                 "peak_source": FP64_PEAK_SOURCE}
     lu = None
     if "k_lu" in kstats:
+        sync_levels = max(1, d["front_level"] - d["lu_cut_level"])
         lu = {"kernel": "k_lu", "ms": kstats["k_lu"]["ms"], "levels": d["n_levels_l"],
-              "us_per_level": 1e3 * kstats["k_lu"]["ms"] / d["n_levels_l"], "bound": "latency (cluster barrier "
-              "per level × the longest row's IKJ chain)", "scenarios": S}
+              "us_per_level": 1e3 * kstats["k_lu"]["ms"] / d["n_levels_l"],
+              "schedule": {"subtree_walk_levels": d["lu_cut_level"], "synchronised_levels": sync_levels,
+                           "dense_front_rows": d["front_rows"], "front_level": d["front_level"]},
+              "us_per_synchronised_level": 1e3 * kstats["k_lu"]["ms"] / sync_levels,
+              "bound": "latency: each cluster-synchronised level waits for its longest row's IKJ chain "
+                       "(staging + pivots); the bottom subtrees and the dense front are off that chain",
+              "scenarios": S}
     roof = {"bound": "hbm", "achieved": kstats[dom]["GBps"], "peak": hbm, "unit": "GB/s",
             "frac": kstats[dom]["frac"], "traffic": traffic.get(dom), "kernel": dom,
             "algorithmic_bytes_per_direction": per_dir[dom], "directions_per_launch": dirs,
