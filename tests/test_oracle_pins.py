@@ -12,20 +12,21 @@ from oracle import pf_oracle as O
 from synth import TABLE1, case9, counts
 from synth.case9 import case9_multipliers
 from synth.grid import pi_model, table1_grid
+from tests import golden_data
 from tests.nets import all_small, rich_small, two_bus
 
 
 # --------------------------------------------------------------------- P1
 def test_table1_dimensions():
-    """Table 1 n_x, n_u for the BASELINE shapes."""
-    want = {"case118": (181, 107), "case1354": (2447, 519), "case2869": (5227, 1019),
-            "case9241": (17036, 2889), "case300": (530, 137)}
-    for name, (nx, nu) in want.items():
-        n_b, n_l, n_g = TABLE1[name]
+    """Table 1 (tests/golden/table1_instances.tsv): n_x, n_u for the BASELINE shapes."""
+    want = golden_data.table1()
+    assert set(want) == set(TABLE1)
+    for name, (n_b, n_l, n_g, nx, nu) in want.items():
+        assert TABLE1[name] == (n_b, n_l, n_g), name
         net, _ = table1_grid(name)
         part = O.partition(net)
         assert (part["n_x"], part["n_u"]) == (nx, nu), name
-        assert net["n_l"] == n_l
+        assert (net["n_b"], net["n_l"], net["n_g"]) == (n_b, n_l, n_g)
 
 
 def test_case9_counts_and_patterns():
@@ -38,18 +39,26 @@ def test_case9_counts_and_patterns():
 
 
 def test_pi_model_examples():
-    """SPEC.md L93–95 examples of the MATPOWER π-model."""
-    Yff, Yft, Ytf, Ytt = pi_model(np.array([0.0]), np.array([0.1]), np.array([0.0]), np.array([1.0]), np.array([0.0]))
-    assert np.allclose([Yff[0], Ytt[0]], [-10j, -10j]) and np.allclose([Yft[0], Ytf[0]], [10j, 10j])
+    """SPEC.md L93–95 examples of the MATPOWER π-model (tests/golden/spec_pi_model.txt)."""
+    g = golden_data.spec_pi_model()
+    r, x, bc, tau, sh = (float(v) for v in g["series_line"][:5])
+    want = dict(kv.split("=") for kv in g["series_line"][5:])
+    Yff, Yft, Ytf, Ytt = pi_model(np.array([r]), np.array([x]), np.array([bc]), np.array([tau]), np.array([sh]))
+    for k, y in zip(("Yff", "Yft", "Ytf", "Ytt"), (Yff, Yft, Ytf, Ytt)):
+        assert np.isclose(y[0], golden_data.complex_pair(want[k])), k
+    tau2, scale = (float(v) for v in g["tap_ratio_scale"])
     a = pi_model(np.array([0.01]), np.array([0.1]), np.array([0.02]), np.array([1.0]), np.array([0.0]))
-    b = pi_model(np.array([0.01]), np.array([0.1]), np.array([0.02]), np.array([1.05]), np.array([0.0]))
-    assert np.isclose(b[0][0], a[0][0] / 1.1025)
+    b = pi_model(np.array([0.01]), np.array([0.1]), np.array([0.02]), np.array([tau2]), np.array([0.0]))
+    assert np.isclose(b[0][0], a[0][0] / scale)
+    ys = 1.0 / complex(0.01, 0.1)  # SPEC L94: Y_ff = y_s + j b_c/2
+    assert np.isclose(a[0][0], ys + 0.01j)
 
 
 def test_ybus_two_bus():
-    """one series line x = 0.1 → Y_bus = [[−10j, 10j], [10j, −10j]]."""
+    """one series line x = 0.1 → Y_bus = [[−10j, 10j], [10j, −10j]] (tests/golden/spec_pi_model.txt)."""
     net, _ = two_bus()
-    assert np.allclose(O.ybus(net), [[-10j, 10j], [10j, -10j]])
+    want = [golden_data.complex_pair(v) for v in golden_data.spec_pi_model()["two_bus_ybus"]]
+    assert np.allclose(O.ybus(net), np.array(want).reshape(2, 2))
 
 
 # --------------------------------------------------------------------- P2 / P5 / P17
@@ -75,9 +84,10 @@ def test_case9_textbook_power_flow():
     part = O.partition(net)
     sol, it, hist = O.newton(net, part, pt)
     p, q = O.injections(net, sol["v"], sol["theta"])
-    assert abs((p[0] + net["p_d"][0]) * 100 - 71.641) < 1e-3
-    assert np.allclose((q[:3] + net["q_d"][:3]) * 100, [27.046, 6.654, -10.860], atol=1e-3)
-    assert np.allclose(sol["v"][3:], [1.0258, 1.0127, 1.0324, 1.0159, 1.0258, 0.9956], atol=1e-4)
+    g = golden_data.keyed("case9_powerflow.txt")
+    assert abs((p[0] + net["p_d"][0]) * 100 - g["p_g1_mw"][0]) < 1e-3
+    assert np.allclose((q[:3] + net["q_d"][:3]) * 100, g["q_g_mvar"], atol=1e-3)
+    assert np.allclose(sol["v"][3:], g["vm_4_9"], atol=1e-4)
     assert np.allclose(np.degrees(sol["theta"][1:]),
                        [9.280, 4.665, -2.217, -3.687, 1.967, 0.728, 3.720, -3.989], atol=1e-3)
 
