@@ -859,6 +859,127 @@ __global__ void k_pf_update(DevNet n, Work w, int n_scen, double* __restrict__ v
   }
 }
 
+// ---------------------------------------------------------------- single-direction solves in SMEM
+// The NEXT passes (condensed rhs, step recovery, reduced gradient, Newton) solve with ONE
+// direction per scenario: the tile layout above would run each sweep's ~1,150 blocks per team
+// as a chain of global-memory round trips on one CTA.  Here the whole permuted vector (n_x
+// doubles) lives in SMEM and every level of the full level schedule (taskL / taskU) runs
+// across the CTA's 1024 threads: a block is taken by a team of TW lanes (TW from the
+// level's width: one warp per block on the narrow top levels, one lane per block on the
+// wide bottom ones), the lanes split its segment's gathers (read from the same sweep
+// streams as the tiled sweeps; columns are SMEM indices) and reduce by shuffles, and lane 0
+// finishes the block (row A, then row B through the intra entry).  One __syncthreads per level.
+constexpr int kTri1Threads = 1024;
+
+template <int TW>
+__device__ __forceinline__ void tri1_level(const int4* __restrict__ tasks, int b0, int b1,
+                                           const double2* __restrict__ sv, double* xs, bool divide, bool lower,
+                                           int shift) {
+  const int lane = threadIdx.x & (TW - 1), team = threadIdx.x / TW, nteam = kTri1Threads / TW;
+  const unsigned mask = TW == 32 ? 0xffffffffu : (((1u << TW) - 1u) << ((threadIdx.x & 31) & ~(TW - 1)));
+  for (int bi = b0 + team; bi < b1; bi += nteam) {
+    const Task k = unpack(__ldg(tasks + bi));
+    const double2* e = sv + k.s;
+    const int n = k.m * (1 + k.two) + 2;
+    double2 sc0 = make_double2(0.0, 0.0), sc1 = sc0;
+    if (lane == 0) { sc0 = __ldg(e + n - 2); sc1 = __ldg(e + n - 1); }  // in flight with the gathers
+    double sA = 0.0, sB = 0.0;
+    if (k.two) {
+#pragma unroll 2
+      for (int i = lane; i < k.m; i += TW) {
+        const double2 qa = __ldg(e + i), qb = __ldg(e + k.m + i);
+        sA = fma(qa.x, xs[(unsigned)__double2loint(qa.y) >> shift], sA);
+        sB = fma(qb.x, xs[(unsigned)__double2loint(qb.y) >> shift], sB);
+      }
+    } else {
+#pragma unroll 4
+      for (int i = lane; i < k.m; i += TW) {
+        const double2 qa = __ldg(e + i);
+        sA = fma(qa.x, xs[(unsigned)__double2loint(qa.y) >> shift], sA);
+      }
+    }
+#pragma unroll
+    for (int o = TW / 2; o > 0; o >>= 1) {
+      sA += __shfl_xor_sync(mask, sA, o, TW);
+      sB += __shfl_xor_sync(mask, sB, o, TW);
+    }
+    if (lane == 0) {
+      const int rA = k.r0 + (!lower && k.two), rB = k.r0 + (lower ? 1 : 0);
+      double a = xs[rA] - sA;
+      if (divide) a *= sc0.x;
+      xs[rA] = a;
+      if (k.two) {
+        double b = xs[rB] - sB - sc0.y * a;
+        if (divide) b *= sc1.x;
+        xs[rB] = b;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void tri1_sweep(const int4* __restrict__ tasks, const int* __restrict__ lptr, int nlev,
+                                           const double2* __restrict__ sv, double* xs, bool divide, bool lower,
+                                           int shift) {
+  for (int lev = 0; lev < nlev; ++lev) {
+    const int b0 = __ldg(lptr + lev), b1 = __ldg(lptr + lev + 1), nb = b1 - b0;
+    if (nb * 32 <= kTri1Threads) tri1_level<32>(tasks, b0, b1, sv, xs, divide, lower, shift);
+    else if (nb * 8 <= kTri1Threads) tri1_level<8>(tasks, b0, b1, sv, xs, divide, lower, shift);
+    else if (nb * 2 <= kTri1Threads) tri1_level<2>(tasks, b0, b1, sv, xs, divide, lower, shift);
+    else tri1_level<1>(tasks, b0, b1, sv, xs, divide, lower, shift);
+    __syncthreads();
+  }
+}
+
+// mode 0 (forward): Z = −G_x⁻¹ P (G_u V + X4) → slabZ column 0 (the right-hand side as FromRhs
+// builds it); mode 1 (adjoint): Ψ = G_x⁻ᵀ (slabW column 0) in place, Lᵀ over every row (full)
+// or over the ancestors of G_u's rows.  One CTA per scenario.
+template <int C>
+__global__ void __launch_bounds__(kTri1Threads) k_tri1(DevNet n, Work w, int mode, bool full,
+                                                         const double* __restrict__ V,
+                                                         const double* __restrict__ X4,
+                                                         const int* __restrict__ x4map, int x4ld) {
+  extern __shared__ double xs[];
+  constexpr int shift = C == 8 ? 3 : C == 16 ? 4 : C == 32 ? 5 : 6;
+  const int s = blockIdx.x, n_x = n.n_x;
+  if (mode == 0) {
+    double* X = w.slabZ + (size_t)s * n_x * C;
+    const double* gu = w.gu + (size_t)s * n.nnz_gu;
+    const double* Vs = V + (size_t)s * n.n_u;
+    const double* X4s = X4 ? X4 + (size_t)s * x4ld : nullptr;
+    for (int r = threadIdx.x; r < n_x; r += blockDim.x) {
+      double a = X4s ? -X4s[__ldg(x4map + r)] : 0.0;
+      for (int e = __ldg(n.gur_ptr + r); e < __ldg(n.gur_ptr + r + 1); ++e)
+        a -= gu[__ldg(n.gur_src + e)] * Vs[__ldg(n.gur_col + e)];
+      xs[r] = a;
+    }
+    __syncthreads();
+    const double2* pk = w.swA + (size_t)s * n.nsw;
+    tri1_sweep(n.taskL, n.levL_ptr, n.nlevL, pk, xs, false, true, shift);   // L⁻¹
+    tri1_sweep(n.taskU, n.levU_ptr, n.nlevU, pk, xs, true, false, shift);   // U⁻¹
+    for (int r = threadIdx.x; r < n_x; r += blockDim.x) X[(size_t)r * C] = xs[r];
+  } else {
+    double* Y = w.slabW + (size_t)s * n_x * C;
+    for (int r = threadIdx.x; r < n_x; r += blockDim.x) xs[r] = Y[(size_t)r * C];
+    __syncthreads();
+    const double2* pk = w.swT + (size_t)s * n.nsw;
+    tri1_sweep(n.taskL, n.levL_ptr, n.nlevL, pk, xs, true, true, shift);    // U⁻ᵀ
+    if (full) tri1_sweep(n.taskU, n.levU_ptr, n.nlevU, pk, xs, false, false, shift);   // L⁻ᵀ
+    else tri1_sweep(n.taskUa, n.levUa_ptr, n.nlevU, pk, xs, false, false, shift);
+    for (int r = threadIdx.x; r < n_x; r += blockDim.x) Y[(size_t)r * C] = xs[r];
+  }
+}
+
+// whether the vector fits the SMEM of one CTA (else the tiled sweeps run the pass)
+inline bool tri1_fits(const DevNet& n) { return (size_t)n.n_x * sizeof(double) <= 200 * 1024; }
+
+template <int C>
+void tri1_launch(const DevNet& n, const Work& w, int n_scen, int mode, bool full, const double* V, const double* X4,
+                 const int* map, int x4ld, cudaStream_t st) {
+  const int smem = (int)((size_t)n.n_x * sizeof(double));
+  cudaFuncSetAttribute(k_tri1<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);  // per device: every launch
+  k_tri1<C><<<n_scen, kTri1Threads, smem, st>>>(n, w, mode, full, V, X4, map, x4ld);
+}
+
 inline int grid_for(long long n) { return (int)std::max<long long>(1, std::min<long long>(148LL * 16, (n + kThreads - 1) / kThreads)); }
 
 template <int C, bool MU>
@@ -873,10 +994,17 @@ size_t blk_smem(const DevNet& n) {
 template <int C>
 void one_dir_fwd_hvp(const DevNet& n, const Work& w, int n_scen, const double* V, const double* X4, const int* map,
                      int x4ld, bool hvp, cudaStream_t st) {
-  k_fwd<C, false><<<dim3(1, n_scen), kThreads, 0, st>>>(n, w, V, 0, 1, -1, X4, map, x4ld);
+  if (tri1_fits(n)) tri1_launch<C>(n, w, n_scen, 0, true, V, X4, map, x4ld, st);
+  else k_fwd<C, false><<<dim3(1, n_scen), kThreads, 0, st>>>(n, w, V, 0, 1, -1, X4, map, x4ld);
   if (!hvp) return;
   k_blk<C, true><<<dim3(n.mb.nchunk, 1, n_scen), kThreads, blk_smem<C, true>(n), st>>>(n, w, V, 0, 1);
   k_blk<C, false><<<dim3(n.hb.nchunk, 1, n_scen), kThreads, blk_smem<C, false>(n), st>>>(n, w, V, 0, 1);
+}
+
+template <int C>
+void one_dir_adj(const DevNet& n, const Work& w, int n_scen, bool full, cudaStream_t st) {
+  if (tri1_fits(n)) tri1_launch<C>(n, w, n_scen, 1, full, nullptr, nullptr, nullptr, 0, st);
+  else k_adj<C><<<dim3(1, n_scen), kThreads, 0, st>>>(n, w, 1, full);
 }
 
 template <int C>
@@ -893,11 +1021,11 @@ int step_all(int what, const DevNet& n, const Work& w, int n_scen, const double*
   if (what == 0 || what == 1) {  // condensed rhs / recovery: forward pass with r₄, K·d
     one_dir_fwd_hvp<C>(n, w, n_scen, what == 0 ? w.zero : p_u, r + n.n_u + n.n_x + n.m, n.perm, ld, true, st);
     k_kkt_vec<C><<<grid_for((long long)n_scen * nz), kThreads, 0, st>>>(n, w, n_scen, KV_RHS, r, sig_s, nullptr, nullptr);
-    k_adj<C><<<dim3(1, n_scen), kThreads, 0, st>>>(n, w, 1, what == 1);
+    one_dir_adj<C>(n, w, n_scen, what == 1, st);
     launches += 6;
   } else {  // reduced gradient
     k_kkt_vec<C><<<grid_for((long long)n_scen * nz), kThreads, 0, st>>>(n, w, n_scen, KV_GRAD, nullptr, nullptr, y, p_g);
-    k_adj<C><<<dim3(1, n_scen), kThreads, 0, st>>>(n, w, 1, true);
+    one_dir_adj<C>(n, w, n_scen, true, st);
     launches += 2;
   }
   if (what == 0 || what == 2) {
