@@ -33,6 +33,51 @@ __global__ void dmma_kernel(double* out, int iters) {
   for (int k = 0; k < 8; ++k) s += c[k][0] + c[k][1];
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
+// the sm_90+ f64 shapes: m16n8k4 (A 2, B 1, C 4 doubles per lane), m16n8k8 (A 4, B 2), m16n8k16 (A 8, B 4)
+template <int K>
+__global__ void dmma16_kernel(double* out, int iters) {
+  double a[K / 2], b[K / 4];
+#pragma unroll
+  for (int i = 0; i < K / 2; ++i) a[i] = threadIdx.x * 1e-9 + i;
+#pragma unroll
+  for (int i = 0; i < K / 4; ++i) b[i] = 1.0 - threadIdx.x * 1e-9 - i;
+  double c[4][4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) c[k][0] = c[k][1] = c[k][2] = c[k][3] = 0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if constexpr (K == 4)
+          asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                       : "+d"(c[k][0]), "+d"(c[k][1]), "+d"(c[k][2]), "+d"(c[k][3]) : "d"(a[0]), "d"(a[1]), "d"(b[0]));
+        else if constexpr (K == 8)
+          asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                       : "+d"(c[k][0]), "+d"(c[k][1]), "+d"(c[k][2]), "+d"(c[k][3])
+                       : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+        else
+          asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};"
+                       : "+d"(c[k][0]), "+d"(c[k][1]), "+d"(c[k][2]), "+d"(c[k][3])
+                       : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+                         "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+      }
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) s += c[k][0] + c[k][1] + c[k][2] + c[k][3];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+template <int K>
+void run16(int blocks, int threads, int iters, double* out, cudaEvent_t e0, cudaEvent_t e1) {
+  dmma16_kernel<K><<<blocks, threads>>>(out, 16);
+  cudaEventRecord(e0); dmma16_kernel<K><<<blocks, threads>>>(out, iters); cudaEventRecord(e1);
+  cudaEventSynchronize(e1); float ms; cudaEventElapsedTime(&ms, e0, e1);
+  const double flops = 2.0 * 16 * 8 * K * 4 * 16 * (double)iters * blocks * (threads / 32);
+  printf("DMMA m16n8k%d: %.3f ms  %.2f TFLOP/s\n", K, ms, flops / ms / 1e9);
+}
+
 int main() {
   int dev = 0; cudaDeviceProp p; cudaGetDeviceProperties(&p, dev);
   printf("device %s SMs %d clock %d kHz\n", p.name, p.multiProcessorCount, p.clockRate);
@@ -51,6 +96,9 @@ int main() {
     cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
     flops = 2.0 * 8 * 8 * 4 * 8 * 16 * (double)iters * blocks * (threads / 32);
     printf("DMMA m8n8k4: %.3f ms  %.2f TFLOP/s\n", ms, flops / ms / 1e9);
+    run16<4>(blocks, threads, iters / 2, out, e0, e1);
+    run16<8>(blocks, threads, iters / 4, out, e0, e1);
+    run16<16>(blocks, threads, iters / 8, out, e0, e1);
   }
   cudaError_t err = cudaGetLastError(); printf("err %s\n", cudaGetErrorString(err));
   return 0;
