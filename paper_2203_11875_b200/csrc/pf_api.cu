@@ -37,6 +37,9 @@ struct pf_net {
   std::vector<int> u_top_ptr, u_bot_ptr, ua_top_ptr, ua_bot_ptr;
   std::vector<int> hvp_order;  // k_hvp bus order (elimination-forest postorder)
   cudaEvent_t ev[10] = {};   // [0..4] k_fwd/k_mu/k_hvp/k_adj, [5..6] k_lu, [4..7] k_proj, [8..9] k_chol_dag
+  // the reduction's fork/join: the ψ-weight prep kernels (A6) run on `side` while k_fwd sweeps
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 #ifndef PF_P1_IMB
@@ -535,6 +538,13 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
   // launch geometry that depends on the device (cluster support, SM count): per handle
   h->lu_cs = lu_cluster_size(d);
   h->chol_grid = chol_grid_max();
+  if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->join, cudaEventDisableTiming) != cudaSuccess) {
+    g_build_err = std::string("stream/event creation: ") + cudaGetErrorString(cudaGetLastError());
+    pf_destroy(h);
+    return PF_ERR_CUDA;
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) {
     g_build_err = std::string("build sync: ") + cudaGetErrorString(cudaGetLastError());
     pf_destroy(h);
@@ -548,6 +558,9 @@ void pf_destroy(pf_net* h) {
   if (!h) return;
   if (h->device >= 0) cudaSetDevice(h->device);
   for (auto& e : h->ev) if (e) cudaEventDestroy(e);
+  if (h->fork) cudaEventDestroy(h->fork);
+  if (h->join) cudaEventDestroy(h->join);
+  if (h->side) cudaStreamDestroy(h->side);
   for (void* p : h->allocs) cudaFree(p);
   delete h;
 }
@@ -646,8 +659,13 @@ pf_status pf_reduced_hessian_batch(pf_net* h, int32_t n_scen, const double* v, c
   if (N == 0) return PF_OK;
   if (!set_device(h)) return h->device < 0 ? PF_ERR_STATE : PF_ERR_CUDA;
   cudaStream_t st = (cudaStream_t)stream;
-  h->launches += launch_prep(h->dn, h->w, n_scen, p_d, lambda, y, sigma_s, sigma_x, st);
-  h->launches += launch_reduce(h->dn, h->w, h->C, n_scen, V, col0, N, KV, st, h->prof ? h->ev : nullptr);
+  // fork: A6 (ψ weights, bus blocks) on the side stream, concurrent with A7.1–A7.2 (k_fwd needs
+  // only the LU); k_blk joins it (graph-capture safe: the side stream rejoins `st`)
+  if (cudaEventRecord(h->fork, st) != cudaSuccess || cudaStreamWaitEvent(h->side, h->fork, 0) != cudaSuccess)
+    return cuda_check(h, "pf_reduced_hessian_batch");
+  h->launches += launch_prep(h->dn, h->w, n_scen, p_d, lambda, y, sigma_s, sigma_x, h->side);
+  if (cudaEventRecord(h->join, h->side) != cudaSuccess) return cuda_check(h, "pf_reduced_hessian_batch");
+  h->launches += launch_reduce(h->dn, h->w, h->C, n_scen, V, col0, N, KV, st, h->prof ? h->ev : nullptr, h->join);
   return cuda_check(h, "pf_reduced_hessian_batch");
 }
 

@@ -25,7 +25,8 @@ int launch_prep(const DevNet& n, const Work& w, int n_scen, const double* p_d, c
 // A7.1–A7.5 fused: RHS, L/U sweeps, matrix-free K·[V;Z], Uᵀ/Lᵀ sweeps, projection.
 int launch_reduce(const DevNet& n, const Work& w, int C, int n_scen, const double* V, int col0,
                   int N, double* KV, cudaStream_t st,
-                  cudaEvent_t* ev = nullptr /* optional: [5] around k_fwd, k_mu, k_hvp, k_adj */);
+                  cudaEvent_t* ev = nullptr /* optional: [5] around k_fwd, k_mu, k_hvp, k_adj */,
+                  cudaEvent_t after_fwd = nullptr /* optional: waited for between k_fwd and k_blk */);
 
 // A9: symmetrize + shift + pack, tile-DAG FP64 Cholesky (DMMA updates) with the solves fused in.
 int launch_chol(const DevNet& n, const Work& w, int n_scen, double* K, const double* sigma_u, double delta_w,

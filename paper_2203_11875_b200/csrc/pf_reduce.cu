@@ -1052,7 +1052,7 @@ int newton_step(const DevNet& n, const Work& w, int n_scen, double* v, double* t
 
 template <int C>
 void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int col0, int N, double* KV,
-                cudaStream_t st, cudaEvent_t* ev) {
+                cudaStream_t st, cudaEvent_t* ev, cudaEvent_t after_fwd) {
   const int ntile = (N + C - 1) / C;
   k_pack_gu<<<(int)std::min<long long>(4096, ((long long)n_scen * n.nnz_gu + kThreads - 1) / kThreads), kThreads, 0,
               st>>>(n, w, n_scen);
@@ -1066,6 +1066,7 @@ void launch_all(const DevNet& n, const Work& w, int n_scen, const double* V, int
   if (rt >= 0) k_fwd<C, true><<<dim3(ntile, n_scen), kThreads, 2 * n.bmw * sizeof(unsigned), st>>>(n, w, V, col0, N, rt);
   else k_fwd<C, false><<<dim3(ntile, n_scen), kThreads, 0, st>>>(n, w, V, col0, N, rt);
   if (ev) cudaEventRecord(ev[1], st);
+  if (after_fwd) cudaStreamWaitEvent(st, after_fwd, 0);
   k_blk<C, true><<<dim3(n.mb.nchunk, ntile, n_scen), kThreads, blk_smem<C, true>(n), st>>>(n, w, V, col0, N);
   if (ev) cudaEventRecord(ev[2], st);
   k_blk<C, false><<<dim3(n.hb.nchunk, ntile, n_scen), kThreads, blk_smem<C, false>(n), st>>>(n, w, V, col0, N);
@@ -1142,12 +1143,12 @@ void set_sweep_trace(unsigned long long* p) { cudaMemcpyToSymbol(g_sw_trace, &p,
 #endif
 
 int launch_reduce(const DevNet& n, const Work& w, int C, int n_scen, const double* V, int col0,
-                  int N, double* KV, cudaStream_t st, cudaEvent_t* ev) {
+                  int N, double* KV, cudaStream_t st, cudaEvent_t* ev, cudaEvent_t after_fwd) {
   switch (C) {
-    case 64: launch_all<64>(n, w, n_scen, V, col0, N, KV, st, ev); break;
-    case 32: launch_all<32>(n, w, n_scen, V, col0, N, KV, st, ev); break;
-    case 16: launch_all<16>(n, w, n_scen, V, col0, N, KV, st, ev); break;
-    default: launch_all<8>(n, w, n_scen, V, col0, N, KV, st, ev); break;
+    case 64: launch_all<64>(n, w, n_scen, V, col0, N, KV, st, ev, after_fwd); break;
+    case 32: launch_all<32>(n, w, n_scen, V, col0, N, KV, st, ev, after_fwd); break;
+    case 16: launch_all<16>(n, w, n_scen, V, col0, N, KV, st, ev, after_fwd); break;
+    default: launch_all<8>(n, w, n_scen, V, col0, N, KV, st, ev, after_fwd); break;
   }
   return 6;
 }
