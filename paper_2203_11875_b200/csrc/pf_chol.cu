@@ -6,10 +6,9 @@
 //
 // Tile algorithm on 64×64 tiles, run as ONE persistent, dependency-driven
 // kernel (k_chol_dag) over every scenario at once:
-//   k_chol_pack    symmetrize + shift K̂ into packed lower tiles (column-major
-//                  inside a tile, leading dimension 68 so DMMA fragment loads
-//                  are bank-conflict free and a tile half is one contiguous
-//                  16-byte-aligned run); padding past n is the identity.
+//   k_chol_reset   clear the ready flags, info, ticket (the K_cond entries are not
+//                  packed ahead: each tile task reads its tile of sym(K̂) + Σ_u + δ_w I
+//                  straight from K̂ into its DMMA accumulators, identity past n).
 //   k_chol_dag     CTAs take tasks from a ticket counter in a topological order
 //                  (column by column, all scenarios interleaved) and wait on
 //                  per-tile ready flags (release/acquire):
@@ -59,6 +58,13 @@ struct DagArgs {
   double* rhs;     // [S][rhs_ld][n], already offset to the first vector of this run
   int* crit;       // [kMaxSm] per-SM count of critical-path tasks in their triangular phase
   const int* sidx; // [S] caller scenario of each (virtual) scenario s, or null = identity (rhs indexing)
+  // K_cond's entries are read straight from the caller's K̂ by each tile task (sym + shift + identity
+  // padding, k_cond_entry): K [caller scenarios][n][n] column-major, Σ_u [caller scenarios][n], δ_w or
+  // per-scenario dvec (regularization retries)
+  const double* K;
+  const double* sig_u;
+  double delta;
+  const double* dvec;
 };
 constexpr int kMaxSm = 1024;
 #ifndef PF_CHOL_LOOK
@@ -127,61 +133,31 @@ __device__ __forceinline__ void record_fail(int* info, int code) {
   }
 }
 
-// sym + shift + pack: tile (I, J), I ≥ J, of scenario s, in two 32-column
-// halves; the tile and its mirror are both read down their columns (coalesced).
-// sidx (optional): caller scenario of virtual scenario s; dvec (optional): per-scenario δ_w.
-__global__ void __launch_bounds__(256) k_chol_pack(int n, int nt, const double* __restrict__ K,
-                                                   const double* __restrict__ sig_u, double delta,
-                                                   double* __restrict__ tiles, int* __restrict__ flags,
-                                                   int* __restrict__ ticket, int* __restrict__ info,
-                                                   int* __restrict__ crit, const int* __restrict__ sidx,
-                                                   const double* __restrict__ dvec) {
-  __shared__ double a[32][NB + 1];  // a[c][r] = K(R, C)
-  __shared__ double b[NB][33];      // b[r][c] = K(C, R)  (mirror)
-  const int s = blockIdx.y, ntri = nt * (nt + 1) / 2, sr = sidx ? sidx[s] : s;
-  if (dvec) delta = dvec[s];
-  int J = 0, t = blockIdx.x;
-  while (t >= nt - J) { t -= nt - J; ++J; }
-  const int I = J + t;
-  const double* A = K + (size_t)sr * n * n;
-  double* T = tiles + ((size_t)s * tstride(nt) + tidx(nt, I, J)) * TILE_D;
-  for (int ch = 0; ch < NB; ch += 32) {
-    {
-      const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 × 4
-      for (int c = ty; c < 32; c += 4) {
-        const int R = I * NB + tx, C = J * NB + ch + c;
-        a[c][tx] = (R < n && C < n) ? A[(size_t)C * n + R] : 0.0;
-      }
-    }
-    {
-      const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 × 8
-      for (int r = ty; r < NB; r += 8) {  // K(J·64 + ch + tx, I·64 + r)
-        const int R2 = J * NB + ch + tx, C2 = I * NB + r;
-        b[r][tx] = (R2 < n && C2 < n) ? A[(size_t)C2 * n + R2] : 0.0;
-      }
-    }
-    __syncthreads();
-    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
-    for (int c = ty; c < 32; c += 4) {
-      const int R = I * NB + tx, C = J * NB + ch + c;
-      double v;
-      if (R >= n || C >= n) v = (R == C) ? 1.0 : 0.0;  // identity padding
-      else if (R > C) v = 0.5 * (a[c][tx] + b[tx][c]);
-      else if (R == C) v = a[c][tx] + (sig_u ? sig_u[(size_t)sr * n + R] : 0.0) + delta;
-      else v = 0.0;
-      T[(ch + c) * LDT + tx] = v;
-    }
-    __syncthreads();
-  }
-  const int nflag = ntri + 2 * nt;
-  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nflag; f += gridDim.x * blockDim.x)
-    flags[(size_t)s * nflag + f] = 0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    info[s] = 0;
-    if (s == 0) *ticket = 0;
-  }
-  if (blockIdx.x == 0 && s == 0)
+// K_cond(R, C) for R ≥ C of (virtual) scenario s: sym(K̂) + diag(Σ_u) + δ_w I (Theorem 2 with
+// R9), the identity past n.  K̂ stays untouched, so a failed scenario can be retried.
+__device__ __forceinline__ double k_cond_entry(const DagArgs& a, int s, int R, int C) {
+  const int n = a.n;
+  if (R >= n || C >= n) return R == C ? 1.0 : 0.0;  // identity padding
+  const int sr = a.sidx ? a.sidx[s] : s;
+  const double* A = a.K + (size_t)sr * n * n;
+  if (R > C) return 0.5 * (__ldg(A + (size_t)C * n + R) + __ldg(A + (size_t)R * n + C));
+  if (R == C) return __ldg(A + (size_t)C * n + R) + (a.sig_u ? __ldg(a.sig_u + (size_t)sr * n + R) : 0.0) +
+                     (a.dvec ? __ldg(a.dvec + s) : a.delta);
+  return 0.0;
+}
+
+// per run: clear every scenario's tile / fwd / bwd flags, its info, the ticket and the per-SM counters
+__global__ void __launch_bounds__(256) k_chol_reset(int nt, int S, int* __restrict__ flags, int* __restrict__ ticket,
+                                                    int* __restrict__ info, int* __restrict__ crit) {
+  const int nflag = nt * (nt + 1) / 2 + 2 * nt;
+  const long long total = (long long)S * nflag;
+  for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < total; f += (long long)gridDim.x * blockDim.x)
+    flags[f] = 0;
+  if (blockIdx.x == 0) {
+    for (int k = threadIdx.x; k < S; k += blockDim.x) info[k] = 0;
     for (int k = threadIdx.x; k < kMaxSm; k += blockDim.x) crit[k] = 0;
+    if (threadIdx.x == 0) *ticket = 0;
+  }
 }
 
 // L back into K: lower (incl. diagonal) from the tiles, strict upper zeroed — only for the
@@ -467,7 +443,7 @@ __device__ void cons_tile(const TaskCtx& t, Pipe& p, double* sm, int* sh) {
   const int wr = warp >> 2, wc = warp & 3, g = lane >> 2, q = lane & 3;
   const bool diag = t.i == t.j;
   // acc = −A_ij + Σ_k L_ik L_jkᵀ, so C = −acc; A is loaded before the first chunk lands
-  const double* Aij = t.tile(t.i, t.j);
+  double* Out = const_cast<double*>(t.tile(t.i, t.j));
   double acc[4][2][2];
 #pragma unroll
   for (int m = 0; m < 4; ++m)
@@ -475,7 +451,7 @@ __device__ void cons_tile(const TaskCtx& t, Pipe& p, double* sm, int* sh) {
     for (int x = 0; x < 2; ++x)
 #pragma unroll
       for (int h = 0; h < 2; ++h)
-        acc[m][x][h] = -Aij[(wc * 16 + x * 8 + 2 * q + h) * LDT + wr * 32 + m * 8 + g];
+        acc[m][x][h] = -k_cond_entry(*t.a, t.s, t.i * NB + wr * 32 + m * 8 + g, t.j * NB + wc * 16 + x * 8 + 2 * q + h);
 #ifdef PF_CHOL_CONS_THROTTLE
   const bool crit_task = t.i <= t.j + 1;
   const int* critc = t.a->crit + smid();
@@ -506,7 +482,6 @@ __device__ void cons_tile(const TaskCtx& t, Pipe& p, double* sm, int* sh) {
   }
   cons_sync();  // every warp is past the ring before the epilogue reuses it
   PF_MARK(0);
-  double* Out = const_cast<double*>(Aij);
   const bool critical = t.i <= t.j + 1;
   int* crit = t.a->crit + smid();
   if (diag) {
@@ -854,8 +829,8 @@ int launch_chol(const DevNet& net, const Work& w, int n_scen, double* K, const d
   const int n = net.n_u, nt = (n + NB - 1) / NB, ntri = nt * (nt + 1) / 2;
   cudaFuncSetAttribute(k_chol_dag, cudaFuncAttributeMaxDynamicSharedMemorySize, kDagSmem);  // per device, idempotent
   int launches = 0;
-  k_chol_pack<<<dim3(ntri, n_scen), 256, 0, st>>>(n, nt, K, sigma_u, delta_w, w.ctile, w.cflag, w.cticket, info_ws,
-                                                   w.cticket + 1, sidx, dvec);
+  k_chol_reset<<<(int)std::min<long long>(1024, ((long long)n_scen * (ntri + 2 * nt) + 255) / 256), 256, 0, st>>>(
+      nt, n_scen, w.cflag, w.cticket, info_ws, w.cticket + 1);
   ++launches;
   // the factorization runs with the first kRhsCap right-hand sides fused in; further
   // ones (rare) in solve-only runs over the finished factor
@@ -871,6 +846,7 @@ int launch_chol(const DevNet& net, const Work& w, int n_scen, double* K, const d
     a.ntask = n_scen * ((first ? ntri : 0) + f * nt) + f * n_scen * nt;
     a.tiles = w.ctile; a.flags = w.cflag; a.ticket = w.cticket; a.info = info_ws;
     a.cy = w.cy; a.rhs = rhs ? rhs + (size_t)r0 * n : nullptr; a.crit = w.cticket + 1; a.sidx = sidx;
+    a.K = K; a.sig_u = sigma_u; a.delta = delta_w; a.dvec = dvec;
     if (a.ntask > 0) {
       k_chol_dag<<<std::min(grid_max, a.ntask), kDagThreads, kDagSmem, st>>>(a);
       ++launches;

@@ -30,6 +30,9 @@ constexpr int kCH = 64;        // u-columns per transposed output chunk
 #ifndef PF_BLK_SPIN_NS
 #define PF_BLK_SPIN_NS 64
 #endif
+#ifndef PF_BLK_PF_DIST
+#define PF_BLK_PF_DIST 296
+#endif
 #ifndef PF_SWEEP_MIN_BLOCKS
 #define PF_SWEEP_MIN_BLOCKS 3
 #endif
@@ -529,6 +532,25 @@ __global__ void __launch_bounds__(kThreads, 4) k_blk(DevNet n, Work w, const dou
       bulk(stg + (size_t)k * C, row < n.n_x ? X + (size_t)row * C : MU_ + (size_t)(row - n.n_x) * C, C * 8);
     }
   }
+#if PF_BLK_PF_DIST > 0
+  else if (threadIdx.x < 64) {
+    // L2 prefetch of the rows a CTA about one resident wave later will stage (no SMEM held):
+    // more DRAM bytes in flight than the staged chunks alone allow
+    const long long lin = ((long long)s * ntile + tile) * gridDim.x + ck + PF_BLK_PF_DIST;
+    if (lin < (long long)gridDim.x * ntile * gridDim.z) {
+      const int ck2 = (int)(lin % gridDim.x);
+      const long long c2 = lin / gridDim.x;  // s2 * ntile + tile2
+      const double* X2 = w.slabZ + (size_t)c2 * n.n_x * C;
+      const double* M2 = w.mu + (size_t)c2 * n.n_g * 2 * C;
+      const int q0 = __ldg(B.st_ptr + ck2), nq = __ldg(B.st_ptr + ck2 + 1) - q0;
+      for (int k = threadIdx.x - 32; k < nq; k += 32) {
+        const int row = __ldg(B.st_row + q0 + k);
+        const double* src = row < n.n_x ? X2 + (size_t)row * C : M2 + (size_t)(row - n.n_x) * C;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((unsigned)(C * 8)) : "memory");
+      }
+    }
+  }
+#endif
   const Dir<C> d = make_dir<C>(n, w, V, col0, N, s, tile, cta, lane);
   double* Y = w.slabW + cta * n.n_x * C;
   double* Hs = w.hu + cta * n.n_u * C;
