@@ -224,3 +224,20 @@ def opf_bounds(net, seed=None):
     q_hi = 0.5 * p_hi + 0.3
     return dict(v_lo=np.full(n_b, 0.9), v_hi=np.full(n_b, 1.1), p_lo=np.zeros(n_g), p_hi=p_hi,
                 q_lo=-q_hi, q_hi=q_hi)
+
+
+def opf_feasible(net, point, margin=1.25, seed=None):
+    """A feasible-by-construction OPF instance around a synthetic operating point
+    (NEXT-4 at scale): the seeded bounds of opf_bounds, with each generator's p_hi
+    raised to ≥ margin·p_g and each limited line's F_max raised to ≥ margin·|s| at
+    the point (both line ends), so the point itself is strictly feasible.  Returns
+    (net copy, bounds).  Only input recipe: no method arithmetic beyond |s|² of the
+    π-model flows the caller passes in as point["s_abs"] (per line, max of the ends)."""
+    b = opf_bounds(net, seed)
+    net2 = dict(net)
+    b["p_hi"] = np.maximum(b["p_hi"], margin * np.asarray(point["p_g"]))
+    F = np.asarray(net["F_max"], dtype=np.float64).copy()
+    lim = F > 0
+    F[lim] = np.maximum(F[lim], margin * np.asarray(point["s_abs"])[lim])
+    net2["F_max"] = F
+    return net2, b
