@@ -944,10 +944,24 @@ __device__ __forceinline__ void tri1_sweep(const int4* __restrict__ tasks, const
                                            int shift) {
   for (int lev = 0; lev < nlev; ++lev) {
     const int b0 = __ldg(lptr + lev), b1 = __ldg(lptr + lev + 1), nb = b1 - b0;
+    // the next level's tasks and segments do not depend on x: thread t loads task t of the next
+    // level now and, once this level is done, prefetches its segment into L1, so the next level
+    // starts from L1 instead of two dependent L2 round trips
+    int4 nxt = make_int4(0, 0, -1, 0);
+    if (lev + 1 < nlev) {
+      const int c0 = __ldg(lptr + lev + 1);
+      if (c0 + (int)threadIdx.x < __ldg(lptr + lev + 2)) nxt = __ldg(tasks + c0 + threadIdx.x);
+    }
     if (nb * 32 <= kTri1Threads) tri1_level<32>(tasks, b0, b1, sv, xs, divide, lower, shift);
     else if (nb * 8 <= kTri1Threads) tri1_level<8>(tasks, b0, b1, sv, xs, divide, lower, shift);
     else if (nb * 2 <= kTri1Threads) tri1_level<2>(tasks, b0, b1, sv, xs, divide, lower, shift);
     else tri1_level<1>(tasks, b0, b1, sv, xs, divide, lower, shift);
+    if (nxt.z >= 0) {
+      const Task k = unpack(nxt);
+      const char* p = reinterpret_cast<const char*>(sv + k.s);
+      const int bytes = (k.m * (1 + k.two) + 2) * 16;
+      for (int o = 0; o < bytes; o += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(p + o));
+    }
     __syncthreads();
   }
 }
