@@ -5,6 +5,7 @@
 #include "pf_plan.h"
 
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <numeric>
 #include <cstring>
@@ -166,9 +167,11 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
   d.lu_maxlen = P.lu_maxlen;
   // Sweep entry streams (pf_reduce.cu run_seq): per block and orientation one contiguous
   // segment  [row A gathers, m][row B gathers, m (two-row blocks)][{d_A, intra}, {d_B, 0}]
-  // with row A the row solved first (LOWER: θ, UPPER: v) and m = the longer row's gather
-  // count rounded up to even; a short row is padded with {0, a column the block gathers}
-  // (a zero product with a final row).  The task is {r0 | two << 31, segment start, m, 0}.
+  // with row A the row solved first (LOWER: θ, UPPER: v).  A two-row block lists both rows
+  // over the union of their columns in one order (entry k of each row names the same column;
+  // a column a row lacks is a zero-valued pad), so the sweep gathers each column once for both
+  // rows — 54% of the gathers of two separate lists at case9241; m = the list length rounded
+  // up to even, a last pad {0, a column the block gathers} (a zero product with a final row).  The task is {r0 | two << 31, segment start, m, 0}.
   // sw_src says where each slot comes from (k_lu packs the L/U and Lᵀ/Uᵀ value streams):
   //   {e, -1} gather {v(e), column(e)·C};  {e, -2} pad {0, column(e)·C};
   //   {a, b ≥ 0} scalars {v(a), v(b)};     {a, -3} scalars {v(a) or 0 if a < 0, 0}
@@ -188,12 +191,29 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
       if (two) { intra = P.lu_diag[rB] + 1; b0 = intra + 1; b1 = P.lu_ptr[rB + 1]; }
     }
     if (two && P.lu_idx[intra] != rA) { fprintf(stderr, "pf: intra-block entry missing\n"); abort(); }
-    const int m = (std::max(a1 - a0, b1 - b0) + 1) & ~1;
     const int any = a1 > a0 ? a0 : b0;  // a gathered column for the pads
     const int start = (int)sw_src.size();
-    for (int k = 0; k < m; ++k) sw_src.push_back(a0 + k < a1 ? make_int2(a0 + k, -1) : make_int2(any, -2));
-    if (two)
-      for (int k = 0; k < m; ++k) sw_src.push_back(b0 + k < b1 ? make_int2(b0 + k, -1) : make_int2(any, -2));
+    int m;
+    if (!two) {
+      m = (a1 - a0 + 1) & ~1;
+      for (int k = 0; k < m; ++k) sw_src.push_back(a0 + k < a1 ? make_int2(a0 + k, -1) : make_int2(any, -2));
+    } else {
+      // both rows over the UNION of their (ascending) columns, in the same order: entry k of
+      // row A and of row B name the same column, so the sweep gathers it once for both rows
+      // (a row's missing columns are zero-valued pads; each row keeps its own entry order)
+      std::vector<int> ea, eb;
+      for (int i = a0, j = b0; i < a1 || j < b1;) {
+        const int ci = i < a1 ? P.lu_idx[i] : INT_MAX, cj = j < b1 ? P.lu_idx[j] : INT_MAX;
+        ea.push_back(ci <= cj ? i++ : -1);
+        eb.push_back(cj <= ci ? j++ : -1);
+      }
+      const int u = (int)ea.size();
+      m = (u + 1) & ~1;
+      for (int k = 0; k < m; ++k)
+        sw_src.push_back(k >= u ? make_int2(any, -2) : ea[k] >= 0 ? make_int2(ea[k], -1) : make_int2(eb[k], -2));
+      for (int k = 0; k < m; ++k)
+        sw_src.push_back(k >= u ? make_int2(any, -2) : eb[k] >= 0 ? make_int2(eb[k], -1) : make_int2(ea[k], -2));
+    }
     sw_src.push_back(two ? make_int2(P.lu_diag[rA], intra) : make_int2(P.lu_diag[rA], -3));
     sw_src.push_back(make_int2(two ? P.lu_diag[rB] : -1, -3));
     return make_int4(r0 | (two ? (int)0x80000000u : 0), start, m, 0);

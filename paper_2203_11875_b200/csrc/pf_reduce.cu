@@ -139,46 +139,42 @@ __device__ __forceinline__ void gather_c(const double* Xl, unsigned c, const uns
 }
 
 // accA[j] −= Σ_{i<m} v_i · X[column_i + lane·CPL + j] over the entries e[0, m) in order, and
-// for two-row blocks accB likewise over e[m, 2m) (m even).  Four entries of each row per
-// step: all their slab loads are issued before the first FMA (one memory round trip per step).
+// for two-row blocks accB likewise over the values of e[m, 2m), whose columns are those of
+// e[0, m) (m even).  Four entries per step: all their slab loads are issued before the first
+// FMA (one memory round trip per step).
 template <int C, bool REACH, bool G>
 __device__ __forceinline__ void dot_seg(const double2* e, int m, bool two, const double* Xl, const unsigned* bm,
                                         double* accA, double* accB) {
   constexpr int CPL = Geo<C>::CPL;
   int i = 0;
   if (two) {
+    // both rows list the same columns (pf_api.cu segment): one gather feeds both rows
 #pragma unroll 1
     for (; i + 4 <= m; i += 4) {
-      double xa[4][CPL], xb[4][CPL];
+      double x[4][CPL];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        gather_c<C, REACH>(Xl, ent_col<G>(e, i + k), bm, xa[k]);
-        gather_c<C, REACH>(Xl, ent_col<G>(e, m + i + k), bm, xb[k]);
-      }
+      for (int k = 0; k < 4; ++k) gather_c<C, REACH>(Xl, ent_col<G>(e, i + k), bm, x[k]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const double va = ent_val<G>(e, i + k), vb = ent_val<G>(e, m + i + k);
 #pragma unroll
         for (int j = 0; j < CPL; ++j) {
-          accA[j] -= va * xa[k][j];
-          accB[j] -= vb * xb[k][j];
+          accA[j] -= va * x[k][j];
+          accB[j] -= vb * x[k][j];
         }
       }
     }
     if (i < m) {  // m is even: one pair left
-      double xa[2][CPL], xb[2][CPL];
+      double x[2][CPL];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        gather_c<C, REACH>(Xl, ent_col<G>(e, i + k), bm, xa[k]);
-        gather_c<C, REACH>(Xl, ent_col<G>(e, m + i + k), bm, xb[k]);
-      }
+      for (int k = 0; k < 2; ++k) gather_c<C, REACH>(Xl, ent_col<G>(e, i + k), bm, x[k]);
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         const double va = ent_val<G>(e, i + k), vb = ent_val<G>(e, m + i + k);
 #pragma unroll
         for (int j = 0; j < CPL; ++j) {
-          accA[j] -= va * xa[k][j];
-          accB[j] -= vb * xb[k][j];
+          accA[j] -= va * x[k][j];
+          accB[j] -= vb * x[k][j];
         }
       }
     }
