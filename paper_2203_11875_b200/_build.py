@@ -1,6 +1,7 @@
 """In-tree build of libpf.so (the C-ABI of include/pf.h) for sm_100a."""
 import os
 import subprocess
+import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -29,8 +30,9 @@ def build(verbose=False, force=False):
         return LIB
     cmd = [_nvcc()] + NVCC_FLAGS + ["-o", LIB + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
     if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
+        print(" ".join(cmd), file=sys.stderr)
+    # compiler output to stderr: bench.py's stdout carries exactly one JSON line
+    subprocess.run(cmd, check=True, stdout=sys.stderr)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 
