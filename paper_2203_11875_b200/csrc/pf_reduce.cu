@@ -36,6 +36,9 @@ constexpr int kCH = 64;        // u-columns per transposed output chunk
 #ifndef PF_INIT_PF
 #define PF_INIT_PF 1  // sweeps from the slab: L2 prefetch of the initial rows PF_INIT_DIST blocks ahead
 #endif
+#ifndef PF_SEG_PF
+#define PF_SEG_PF 1
+#endif
 #ifndef PF_INIT_DIST
 #define PF_INIT_DIST 3
 #endif
@@ -273,7 +276,10 @@ __device__ __forceinline__ void run_seq(const int4* __restrict__ tasks, int firs
     // once its task has arrived, at the end of this block (k_adj 3.17 → 2.80 ms); the other
     // sweeps start from rows their previous sweep just wrote (L2-hot) and gain nothing
     const bool pf3 = std::is_same<Init, FromSlab>::value && bi + PF_INIT_DIST * stride < end;
-    const int4 t3 = pf3 ? __ldg(tasks + bi + PF_INIT_DIST * stride) : make_int4(0, 0, 0, 0);
+    // k_fwd's sweeps (not from the slab): the segment of the block PF_INIT_DIST ahead instead
+    // (k_fwd 1.89 → 1.86 ms; in k_adj it costs more than it saves)
+    const bool pfs = PF_SEG_PF && !std::is_same<Init, FromSlab>::value && bi + PF_INIT_DIST * stride < end;
+    const int4 t3 = (pf3 || pfs) ? __ldg(tasks + bi + PF_INIT_DIST * stride) : make_int4(0, 0, 0, 0);
 #endif
     const int rA = k.r0 + (!LOWER && k.two), rB = k.r0 + (LOWER ? 1 : 0);
     double* xa = X + (size_t)rA * C + lane * CPL;
@@ -327,6 +333,13 @@ __device__ __forceinline__ void run_seq(const int4* __restrict__ tasks, int firs
         if (PF_INIT_PF == 2) asm volatile("prefetch.global.L1 [%0];" ::"l"(pr));
         else asm volatile("prefetch.global.L2 [%0];" ::"l"(pr));
       }
+    }
+    if (pfs) {  // … and that block's segment (the stream lines the cp.async copy will read)
+      const Task k3 = unpack(t3);
+      const char* b = reinterpret_cast<const char*>(sv + k3.s);
+      const char* e = reinterpret_cast<const char*>(sv + k3.s + len(k3));
+      const char* pl = reinterpret_cast<const char*>(reinterpret_cast<size_t>(b) & ~(size_t)127) + lane * 128;
+      if (pl < e) asm volatile("prefetch.global.L2 [%0];" ::"l"(pl));
     }
 #endif
     __syncwarp(mask);  // every lane is done with this buffer before it is refilled
