@@ -36,6 +36,9 @@ constexpr int kCH = 64;        // u-columns per transposed output chunk
 #ifndef PF_INIT_PF
 #define PF_INIT_PF 1  // sweeps from the slab: L2 prefetch of the initial rows PF_INIT_DIST blocks ahead
 #endif
+#ifndef PF_PROJ_PF
+#define PF_PROJ_PF 1
+#endif
 #ifndef PF_SEG_PF
 #define PF_SEG_PF 1
 #endif
@@ -759,6 +762,16 @@ __device__ __forceinline__ void proj_chunk(const DevNet& n, const Work& w, int N
     if (cc + nteam < cend) {
       e0n = __ldg(n.guc_ptr + c + nteam); nen = __ldg(n.guc_ptr + c + nteam + 1) - e0n;
       qn = lane < nen ? __ldg(pg + e0n + lane) : make_double2(0.0, 0.0);
+#if PF_PROJ_PF
+      // the next column's Ψ rows and H_u row into L2 while this column is gathered (k_adj and
+      // k_hvp wrote them; they come from DRAM)
+      constexpr int NL = C * 8 / 128 > 0 ? C * 8 / 128 : 1;
+      if (lane < nen && lane < W)
+        for (int l = 0; l < NL; ++l)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(Y + __double2loint(qn.y)) + l * 128));
+      if (lane < NL)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(Hs + (size_t)(c + nteam) * C) + lane * 128));
+#endif
     }
     double acc[CPL];
     row_ld<C>(Hs, c, lane, acc);
