@@ -301,3 +301,47 @@ def test_regularized_condensed_solve(pfmod, name):
     assert np.array_equal(K.cpu().numpy()[1], Kh[1]) and np.array_equal(rhs.cpu().numpy()[1], b[1])
     assert i2[0] == 0
     h.close()
+
+
+def test_single_direction_passes_beyond_smem(pfmod):
+    """The single-direction passes keep the whole vector in SMEM (k_tri1) only while
+    8·n_x ≤ 200 KB; a 13,600-bus grid (n_x = 25,899) takes the tiled one-CTA sweeps
+    instead.  Both directions are checked: the adjoint (pf_reduced_gradient: λ and
+    ∇f_r against the oracle) and the forward solve (pf_power_flow's Newton
+    steps from a perturbed start reach the constructed solution x* to 1e-9 in ≤ 8
+    iterations, ‖g‖∞ ≤ 1e-10)."""
+    import torch
+    from synth.grid import make_grid
+    net, pt = make_grid(13600, 18600, 1300, 21)
+    part = O.partition(net)
+    assert 8 * part["n_x"] > 200 * 1024
+    h = pfmod.Network(net, max_batch=1, max_scen=1)
+    v, th = dev(pt["v"][None]), dev(pt["theta"][None])
+    h.pf_jacobian(1, v, th)
+    lam = torch.empty(1, part["n_x"], dtype=torch.float64, device="cuda")
+    _, g = h.pf_reduced_gradient(1, v, th, dev(pt["p_g"][None]), dev(pt["y"][None]), lam=lam,
+                                 p_d=dev(pt["p_d"][None]))
+    torch.cuda.synchronize()
+    lo, go = O.reduced_gradient(net, part, pt, pt["y"])
+    assert rel_err(lam[0].cpu().numpy(), lo) <= TOL
+    assert rel_err(g[0].cpu().numpy(), go) <= TOL
+    # forward: constructive point (loads / dispatch from the point), started from a seeded
+    # perturbation of x* (1e-3 in v, 2e-3 in θ; Newton's basin on this random grid is smaller
+    # than a flat start — tools/newton_probe.py: the same on the k_tri1 path at 12,000 buses);
+    # Newton only converges in a few steps if every solve G_x Z = g is right
+    p, q = O.injections(net, pt["v"], pt["theta"])
+    gb = net["gen_bus"]
+    star = dict(pt, p_d=np.where(part["is_gen"], 0.0, -p), q_d=np.where(part["is_gen"], 0.0, -q),
+                p_g=p[gb].copy(), q_g=q[gb].copy())
+    rng = np.random.default_rng(5)
+    v0 = dev(np.where(part["is_gen"], star["v"], star["v"] + 1e-3 * rng.standard_normal(net["n_b"]))[None])
+    th0 = dev((star["theta"] + 2e-3 * rng.standard_normal(net["n_b"]) * (np.arange(net["n_b"]) != net["ref_bus"]))[None])
+    it, res, info = h.pf_power_flow(1, v0, th0, dev(star["p_g"][None]), dev(star["q_g"][None]),
+                                    dev(star["p_d"][None]), dev(star["q_d"][None]), tol=1e-10, max_iter=20)
+    torch.cuda.synchronize()
+    assert int(info[0]) == 0 and res[0] <= 1e-10 and int(it[0]) <= 8, (it, res, info)
+    assert np.abs(v0[0].cpu().numpy() - star["v"]).max() <= 1e-9
+    assert np.abs(th0[0].cpu().numpy() - star["theta"]).max() <= 1e-9
+    record("beyond_smem", n_x=part["n_x"], lam_rel_err=float(rel_err(lam[0].cpu().numpy(), lo)),
+           grad_rel_err=float(rel_err(g[0].cpu().numpy(), go)), newton_iters=int(it[0]), resid=float(res[0]))
+    h.close()
