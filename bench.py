@@ -66,6 +66,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-generic", action="store_true", help="skip the dense-V generic-HVP timing")
     ap.add_argument("--no-next", action="store_true", help="skip the NEXT-row call timings")
+    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay timing")
     ap.add_argument("--profile-steps", type=int, default=0, help="run N untimed steps and exit (for ncu)")
     return ap.parse_args()
 
@@ -368,6 +369,50 @@ def main():
         generic = {"value": S * ncols / (statistics.mean(gms) / 1e3), "unit": "HVP/s", "ms": statistics.mean(gms),
                    "directions": S * ncols, "V": "dense N(0,1), seed 7 (A7.1 a real SpMM)"}
 
+    # ------------------------------------------------------------ the step's device work as one CUDA graph
+    # (captured once, replayed: no host launch gaps); the condensed solve runs at the δ_w the loop
+    # found (the loop's host decisions cannot be captured).  Context, not the headline.
+    graph = None
+    if ncols > 0 and (not directions or world == 1) and not args.no_graph:
+        dmax = float(max(deltas))
+        rhs_g = torch.empty(S, n_u, dtype=f64, device=dev)
+        info_g = torch.empty(S, dtype=torch.int32, device=dev)
+        h.profile(False)
+
+        def gbody():
+            rhs_g.copy_(devt["rhs"])
+            h.pf_eval_constraints(S, devt["v"], devt["theta"], devt["p_g"], devt["q_g"], devt["p_d"], devt["q_d"], G, H)
+            h.pf_jacobian(S, devt["v"], devt["theta"], info=info_j)
+            h.pf_reduced_hessian_batch(S, devt["v"], devt["theta"], devt["lam"], devt["y"], KV[:, :ncols],
+                                       sigma_s=devt["sigma_s"], sigma_x=devt["sigma_x"], N=ncols, p_d=devt["p_d"])
+            h.pf_condensed_kkt_solve(S, KV[:, :n_u], devt["sigma_u"], dmax, rhs=rhs_g, nrhs=1, info=info_g)
+
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            gbody()
+        stream.wait_stream(side)
+        torch.cuda.synchronize()
+        cg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(cg):
+            gbody()
+        gms = []
+        for k in range(args.warmup + args.steps):
+            flush.fill_(1.0)
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+            cg.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if k >= args.warmup:
+                gms.append(e0.elapsed_time(e1))
+        assert not torch.any(info_g != 0)
+        graph = {"value": S * ncols / (statistics.mean(gms) / 1e3), "unit": "HVP/s", "ms_per_step": statistics.mean(gms),
+                 "delta_w": dmax, "note": "eval + jacobian + reduction + condensed solve captured once as a CUDA "
+                 "graph and replayed (L2 flushed between replays); the δ_w loop's host decisions are not captured"}
+        del cg
+        h.profile(True)
+
     # ------------------------------------------------------------ the NEXT rows' calls at the same point (ms per call, all S scenarios)
     next_rows = None
     if not args.no_next and rank == 0:
@@ -545,7 +590,7 @@ def main():
         "chol_ms_per_iter": chol_avg, "reduction_ms_per_iter": red_avg,
         "reduction_ms_includes": "pf_jacobian (LU refactor) + pf_reduced_hessian_batch" +
                                  (" + NCCL all-gather" if directions and world > 1 else ""),
-        "generic_hvp": generic, "next_rows": next_rows,
+        "generic_hvp": generic, "cuda_graph": graph, "next_rows": next_rows,
         "roofline": roof, "roofline_fp64": fp64, "lu_latency": lu,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk.summary(), "per_rank": per_rank,
