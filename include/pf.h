@@ -207,6 +207,10 @@ pf_status pf_jacobian(pf_net *net, int32_t n_scen, const double *v,
  *   V: [n_scen][N][n_u] directions, or NULL = unit columns col0..col0+N−1;
  *   out KV: [n_scen][N][n_u] = K̂ V (each direction a contiguous column, so
  *   N = n_u, col0 = 0 yields K̂ column-major).
+ * Stream semantics: ordered on `stream`; internally the A6 prep kernels run on
+ * the handle's helper stream, forked from and joined back into `stream` with
+ * events (so the call is CUDA-graph capturable and a single handle must not be
+ * used from two host threads at once).
  */
 pf_status pf_reduced_hessian_batch(pf_net *net, int32_t n_scen,
                                    const double *v, const double *theta,
