@@ -45,7 +45,8 @@ typedef enum {
   PF_ERR_ARG = 1,       /* bad pointer / size / negative count */
   PF_ERR_TOPOLOGY = 2,  /* no/invalid ref bus, gen bus with != 1 generator (R21),
                            out-of-range index, self-loop, disconnected grid */
-  PF_ERR_CAPACITY = 3,  /* N > max_batch or n_scen > max_scen */
+  PF_ERR_CAPACITY = 3,  /* N > max_batch or n_scen > max_scen; at build: a filled-LU row too long
+                           for k_lu's SMEM row workspace (pf_build_error says by how much) */
   PF_ERR_CUDA = 4,      /* CUDA runtime error (see pf_last_error) */
   PF_ERR_STATE = 5      /* call order violated (e.g. no pf_jacobian before a reduction) */
 } pf_status;

@@ -555,7 +555,20 @@ pf_status pf_build_network_ex(int32_t n_b, int32_t n_l, int32_t n_g, const int32
     pf_destroy(h);
     return PF_ERR_CUDA;
   }
-  // launch geometry that depends on the device (cluster support, SM count): per handle
+  // launch geometry that depends on the device (cluster support, SM count): per handle.
+  // k_lu keeps one dense row workspace per warp in SMEM: a filled-LU row longer than that
+  // allows (lu_maxlen ≳ 1,250 on a B200) has no fallback — refuse the network here, clearly
+  {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+    if (lu_smem_bytes(d) > (size_t)optin) {
+      g_build_err = "k_lu needs " + std::to_string(lu_smem_bytes(d)) + " B of SMEM per CTA (longest filled-LU row " +
+                    std::to_string(P.lu_maxlen) + " entries) > the device's " + std::to_string(optin) +
+                    " B: network too dense for this build";
+      pf_destroy(h);
+      return PF_ERR_CAPACITY;
+    }
+  }
   h->lu_cs = lu_cluster_size(d);
   h->chol_grid = chol_grid_max();
   if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||

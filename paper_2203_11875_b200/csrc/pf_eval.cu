@@ -818,6 +818,8 @@ static size_t lu_smem(const DevNet& n) {
   return std::max(rows, (size_t)n.fr_n * (n.fr_n + 1) * sizeof(double));  // the front reuses the area
 }
 
+size_t lu_smem_bytes(const DevNet& n) { return lu_smem(n); }
+
 int lu_cluster_size(const DevNet& n) {
   // 16-CTA clusters (non-portable) when the part supports them, else 8, 4, …
   const size_t smem = lu_smem(n);

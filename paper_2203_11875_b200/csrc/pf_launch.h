@@ -17,6 +17,8 @@ int launch_jacobian(const DevNet& n, const Work& w, int n_scen, const double* v,
                     cudaEvent_t* ev = nullptr /* optional: [2] around k_lu */);
 // k_lu cluster size supported on the current device (sets k_lu's function attributes there)
 int lu_cluster_size(const DevNet& n);
+// k_lu's dynamic SMEM (per-warp dense row workspaces of lu_maxlen doubles + staging areas, or the dense front)
+size_t lu_smem_bytes(const DevNet& n);
 
 // A6: per-scenario ψ weights w̄ and bus/line state for the HVP.
 int launch_prep(const DevNet& n, const Work& w, int n_scen, const double* p_d, const double* lam,

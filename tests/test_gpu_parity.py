@@ -608,3 +608,25 @@ def test_cuda_graph_capture_replay(pfmod):
         assert torch.equal(a, b)
     assert not torch.equal(ref2[1], ref[1])
     h.close()
+
+
+def test_lu_row_workspace_capacity_error(pfmod):
+    """k_lu keeps a dense workspace of the longest filled-LU row per warp in SMEM; a
+    network whose longest row does not fit (a 1,500-leaf star around a PQ hub, the
+    generator / reference at a leaf: the hub's rows span every other state, 3,000
+    entries) is refused at build with PF_ERR_CAPACITY and a message naming the row
+    length — not a CUDA launch failure at the first pf_jacobian."""
+    from synth.grid import pi_model
+    nl = 1500
+    n_b = nl + 1
+    r = np.full(nl, 0.01)
+    x = np.full(nl, 0.1)
+    Yff, Yft, Ytf, Ytt = pi_model(r, x, np.zeros(nl), np.ones(nl), np.zeros(nl))
+    net = dict(n_b=n_b, n_l=nl, n_g=1, line_from=np.zeros(nl, np.int32), line_to=np.arange(1, n_b, dtype=np.int32),
+               Y_ff=Yff, Y_ft=Yft, Y_tf=Ytf, Y_tt=Ytt, Y_sh=np.zeros(n_b, complex), gen_bus=np.array([1], np.int32),
+               ref_bus=1, p_d=np.full(n_b, 0.001), q_d=np.zeros(n_b), F_max=np.ones(nl),
+               c_quad=np.array([1.0]), c_lin=np.array([1.0]), seed=3)
+    with pytest.raises(pfmod.PFError) as e:
+        pfmod.Network(net, max_batch=1, max_scen=1)
+    assert e.value.status == 3  # PF_ERR_CAPACITY
+    assert "SMEM" in str(e.value) and "3000" in str(e.value)
